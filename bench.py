@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""Benchmark of the implicit data-sharing hot path on B200.
+
+One *step* = one generic-mode target region launch of BASELINE config 4:
+``teams`` CTAs (OpenMP teams) of W workers + the reserved master warp; each
+team runs kernel_init, pushes its kernel depot on the master's data-sharing
+stack, shares 8 scalars through prepare_parallel / the shared-memory args
+window, releases its workers with a named barrier, the workers read the
+shared-variable list (warp-shuffle broadcast) and stream
+``y[i] = fma(c1, x[i], y[i]) + (c2+...+c8)`` over 2^28 fp64 elements on the
+cyclic schedule, retire, join, deinit.
+
+Metric: body HBM GB/s (24 algorithmic bytes per element) -- BASELINE.json
+"parallel regions/sec + body HBM GB/s vs 8 TB/s; smem bytes/CTA & occupancy".
+Config-1 latency (ns per parallel region) and the team region's smem/CTA and
+occupancy are reported alongside.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU (torchrun, one process per GPU): every rank runs the same region on
+its own element range (weak scaling: 2^28 elements per GPU, no data-path
+collective); the checksum of y is all-reduced once after timing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_ELEM = 24  # read x (8) + read y (8) + write y (8)
+SEED_X, SEED_Y = 0x5EED01AB, 0x5EED01AC
+COEF = [k / 8 for k in range(1, 9)]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1 << 28, help="elements per GPU")
+    ap.add_argument("--teams", type=int, default=0, help="0: 148 x teams-per-SM")
+    ap.add_argument("--workers", type=int, default=0, help="W (0: tuned default)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ptxas_regs(kernel_substr):
+    log = os.path.join(ROOT, "paper_1711_10413_b200", "_build", "ptxas.log")
+    try:
+        lines = open(log).read().splitlines()
+    except OSError:
+        return None
+    for i, l in enumerate(lines):
+        if "Compiling entry function" in l and kernel_substr in l:
+            for m in lines[i + 1:i + 4]:
+                if "Used" in m and "registers" in m:
+                    return int(m.split("Used")[1].split("registers")[0])
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(n_sample, threads):
+    """The C oracle port (fp64, OpenMP over the host's cores) on a bounded sample."""
+    import numpy as np
+    from oracle import oracle as O
+    L = O.lib()
+    x = np.empty(n_sample)
+    y = np.empty(n_sample)
+    L.orc_fill(1, O.ptr(x), n_sample, SEED_X, 0)
+    L.orc_fill(1, O.ptr(y), n_sample, SEED_Y, 0)
+    coef = np.array(COEF)
+    L.orc_stream(1, n_sample, O.ptr(x), O.ptr(y), O.ptr(coef), threads)  # warm
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        L.orc_stream(1, n_sample, O.ptr(x), O.ptr(y), O.ptr(coef), threads)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el > 3.0 or reps >= 20:
+            break
+    gbs = BYTES_PER_ELEM * n_sample * reps / el / 1e9
+    return {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"{n_sample} fp64 elements x {reps} passes of the config-4 body "
+                      f"(oracle/ompds_oracle.c orc_stream, OpenMP {threads} threads)"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU path (oracle/_ref, the
+    unmodified omplab simulator running the integer analog of the region)."""
+    import ctypes as C
+    import numpy as np
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    shim = os.path.join(ROOT, "oracle", "_ref", "libomplab_ref.so")
+    threads = os.cpu_count() or 1
+    base = {"metric": "stream region body GB/s (config 4, 24 B/elem)", "impl": "reference",
+            "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "dtype": "int32 (reference language is integer-only)", "data": "synthetic",
+            "config": {"workload": "config4_stream_region", "teams": 4, "workers": 96,
+                       "elements_per_step": None, "parallelism": f"{threads} host threads"}}
+    if not os.path.exists(shim):
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libomplab_ref.so not built (needs /root/reference)"}))
+        return
+    L = C.CDLL(shim)
+    L.omplab_ref_stream.argtypes = [C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                    C.c_void_p, C.c_int]
+    chunk = 4096
+    nchunks = 2 * threads
+    n = chunk * nchunks
+    x = np.array([(int(v) % 201) - 100 for v in range(n)], dtype=np.int64)
+    y = np.zeros(n, dtype=np.int64)
+    xp, yp = C.c_void_p(x.ctypes.data), C.c_void_p(y.ctypes.data)
+    for _ in range(max(args.warmup, 0)):
+        assert L.omplab_ref_stream(0, chunk, nchunks, 4, 96, xp, yp, threads) == 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        assert L.omplab_ref_stream(0, chunk, nchunks, 4, 96, xp, yp, threads) == 0
+    el = time.perf_counter() - t0
+    gbs = BYTES_PER_ELEM * n * args.steps / el / 1e9
+    base["value"] = round(gbs, 6)
+    base["ms_per_step"] = round(el / args.steps * 1e3, 3)
+    base["config"]["elements_per_step"] = n
+    base["cpu_baseline"] = {"value": base["value"], "unit": "GB/s", "cores": threads,
+                            "kind": "reference",
+                            "sample": f"{nchunks} chunks x {chunk} int elements per step, "
+                                      "omplab simulate() (Simulator.cpp) per chunk"}
+    base["e2e"] = {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}
+    print(json.dumps(base))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_1711_10413_b200 import _lib as PL
+    from paper_1711_10413_b200 import regions as RG
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n_total = args.n * world if args.scaling == "weak" else args.n
+    lo = rank * n_total // world
+    hi = (rank + 1) * n_total // world
+    n = hi - lo
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    workers = args.workers or 992
+    teams = args.teams or sms * (2048 // (((workers + 31) // 32) * 32 + 32))
+
+    x = torch.empty(n, dtype=torch.float64, device=dev)
+    y = torch.empty(n, dtype=torch.float64, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        RG.fill_uniform(x, SEED_X, lo, stream=stream)
+        RG.fill_uniform(y, SEED_Y, lo, stream=stream)
+    stream.synchronize()
+
+    def step():
+        RG.run_stream(x, y, COEF, teams, workers, stats=False, stream=stream)
+
+    # parity of the first launch against the oracle on a slice (cheap, size-independent)
+    stats_out = RG.run_stream(x, y, COEF, teams, workers, stream=stream)
+    stream.synchronize()
+    st = stats_out.team_stats()
+    assert all(s.trap == 0 and s.regions == 1 for s in st)
+    smem_bytes = st[0].smem_bytes
+
+    for _ in range(args.warmup):
+        step()
+    stream.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    ms_per_step = ms_max / args.steps
+    value = BYTES_PER_ELEM * n_total / (ms_per_step * 1e-3) / 1e9
+
+    # checksum gather (once, outside the timed region)
+    c = RG.checksum(y, stream=stream)
+    cks = torch.tensor([c - (1 << 64) if c >= 1 << 63 else c], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(cks)
+    checksum = int(cks.item()) & ((1 << 64) - 1)
+
+    # config-1 latency: 1 team x 32 workers, R regions in a loop, 4 shared scalars
+    R = 10_000
+    a = torch.zeros(32, dtype=torch.int32, device=dev)
+    RG.run_regions(a, 1, 32, 10, stream=stream)
+    stream.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    RG.run_regions(a, 1, 32, R, stream=stream)
+    e1.record(stream)
+    e1.synchronize()
+    ns_per_region = e0.elapsed_time(e1) * 1e6 / R
+
+    peak, peak_src = measured_peaks()
+    roofline = {"bound": "hbm", "achieved": round(value / world, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(value / world / peak, 4), "traffic": None,
+                "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": BYTES_PER_ELEM * n}
+    tr = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr):
+        try:
+            t = json.load(open(tr))
+            if t.get("n") == n:
+                roofline["traffic"] = t["dram_bytes_per_launch"]
+        except (OSError, ValueError, KeyError):
+            pass
+
+    line = {
+        "metric": "stream region body GB/s (config 4, 24 B/elem)",
+        "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config4_stream_region", "elements_per_gpu": n,
+                   "elements_total": n_total, "teams": teams, "workers": workers,
+                   "threads_per_team": ((workers + 31) // 32) * 32 + 32,
+                   "shared_scalars": 8, "parallelism": f"team-range shards x{world}",
+                   "l2": "inputs (2 x 8 B x n) larger than the 126 MB L2, no flush needed"},
+        "roofline": roofline,
+        "regions": {"ns_per_region": round(ns_per_region, 1),
+                    "regions_per_s": round(1e9 / ns_per_region, 1),
+                    "workload": "config 1: 1 team x 32 workers, 4 shared scalars, "
+                                f"{R} regions in a sequential loop"},
+        "smem_bytes_per_cta": smem_bytes,
+        "smem_layout": "depot 80 + args window 160 + runtime span 49 (reference footprint 289)",
+        "regs_per_thread": ptxas_regs("StreamProgIdE"),
+        "checksum": f"{checksum:#018x}",
+        "gpu_launches": args.steps,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_e2e:
+        line["e2e"] = e2e(args, teams, workers, n, dev)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(1 << 26, os.cpu_count() or 1)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line))
+
+
+def e2e(args, teams, workers, n, dev):
+    """Same region through the C ABI's host-buffer entry point: H2D x,y from
+    pinned memory, region, D2H y -- all inside the timed region."""
+    import torch
+    from paper_1711_10413_b200 import regions as RG
+    xh = torch.empty(n, dtype=torch.float64).pin_memory()
+    yh = torch.empty(n, dtype=torch.float64).pin_memory()
+    xd = torch.empty(n, dtype=torch.float64, device=dev)
+    yd = torch.empty(n, dtype=torch.float64, device=dev)
+    RG.fill_uniform(xd, SEED_X)
+    RG.fill_uniform(yd, SEED_Y)
+    xh.copy_(xd)
+    yh.copy_(yd)
+    stream = torch.cuda.Stream(device=dev)
+    RG.run_stream_host(xh, yh, COEF, teams, workers, xd, yd, stream=stream)  # warm
+    t0 = time.perf_counter()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.e2e_steps):
+        RG.run_stream_host(xh, yh, COEF, teams, workers, xd, yd, stream=stream)
+    ev1.record(stream)
+    ev1.synchronize()
+    wall = time.perf_counter() - t0
+    ms = ev0.elapsed_time(ev1) / args.e2e_steps
+    return {"value": round(BYTES_PER_ELEM * n / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 8 * n,
+            "ms_per_step": round(ms, 3), "wall_ms_per_step": round(wall / args.e2e_steps * 1e3, 3),
+            "path": "ompds_run_stream_host (C ABI, pinned host buffers)"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,337 @@
+/*
+ * ompds.h -- C ABI of the B200-native implicit data-sharing runtime for
+ * OpenMP generic-mode target regions (arXiv 1711.10413).
+ *
+ * This is the drop-in boundary for the hot path named by BASELINE.json's
+ * north_star.  The reference (`omplab`, /root/reference/proj) exposes the path
+ * as C++ classes; each entry point below names the reference interface it
+ * replaces (file:line, relative to proj/).  Plain pointers and sizes only: no
+ * C++ or torch types cross this boundary.  Every entry point returns an
+ * `ompds_status` (0 = OK); runtime protocol traps return the trap code whose
+ * exact reference string `ompds_trap_reason` yields.
+ *
+ * Compute entry points run on the GPU (sm_100a) and fail with
+ * OMPDS_ERR_CUDA when no device is usable -- there is no CPU fallback.
+ */
+#ifndef OMPDS_H
+#define OMPDS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------------ */
+/* Constants  (proj/include/omplab/DeviceRuntime.h:26-38)                    */
+/* ------------------------------------------------------------------------ */
+#define OMPDS_DEFAULT_PREALLOC_ENTRIES 20 /* DefaultPreallocEntries  :27 */
+#define OMPDS_SHARED_ARG_ENTRY_BYTES 8    /* SharedArgEntryBytes     :29 */
+#define OMPDS_RUNTIME_PRIVATE_BYTES 49    /* RuntimePrivateBytes     :31 */
+#define OMPDS_RESERVED_WARP 32            /* Codegen.h:25 ReservedWarpSize */
+
+/* ------------------------------------------------------------------------ */
+/* Status / trap codes.  Codes 1..17 are the reference's RtResult trap      */
+/* reasons (DeviceRuntime.cpp:33-143), strings via ompds_trap_reason().      */
+/* ------------------------------------------------------------------------ */
+typedef enum ompds_status {
+  OMPDS_OK = 0,
+  OMPDS_TRAP_INIT_FROM_WORKER = 1,
+  OMPDS_TRAP_INIT_TWICE = 2,
+  OMPDS_TRAP_INIT_NO_WORKERS = 3,
+  OMPDS_TRAP_PREPARE_FROM_WORKER = 4,
+  OMPDS_TRAP_PREPARE_BEFORE_INIT = 5,
+  OMPDS_TRAP_PREPARE_AFTER_DEINIT = 6,
+  OMPDS_TRAP_PREPARE_IN_FLIGHT = 7,
+  OMPDS_TRAP_NEGATIVE_NARGS = 8,
+  OMPDS_TRAP_ARGS_ALLOC_FAILED = 9,
+  OMPDS_TRAP_PARALLEL_FROM_MASTER = 10,
+  OMPDS_TRAP_PARALLEL_NOT_STAGED = 11,
+  OMPDS_TRAP_END_FROM_MASTER = 12,
+  OMPDS_TRAP_END_NOT_ACTIVE = 13,
+  OMPDS_TRAP_DEINIT_FROM_WORKER = 14,
+  OMPDS_TRAP_DEINIT_BEFORE_INIT = 15,
+  OMPDS_TRAP_DEINIT_IN_FLIGHT = 16,
+  OMPDS_TRAP_DEINIT_TWICE = 17,
+  /* data-sharing stack (new; no reference counterpart) */
+  OMPDS_TRAP_STACK_OVERFLOW = 18,  /* global overflow chain exhausted */
+  OMPDS_TRAP_STACK_UNDERFLOW = 19, /* pop of a frame that is not the top */
+  /* host-side errors */
+  OMPDS_ERR_CUDA = 100,    /* no usable CUDA device / launch or copy failed */
+  OMPDS_ERR_INVALID = 101, /* invalid argument */
+  OMPDS_ERR_CAPACITY = 102 /* caller-provided output array too small */
+} ompds_status;
+
+/* Exact reference trap string for codes 1..17 ("" for OK). */
+const char *ompds_trap_reason(int32_t code);
+/* Last CUDA error text recorded by this library (thread-local). */
+const char *ompds_last_error(void);
+/* Library/ABI version, e.g. 0x00010000. */
+uint32_t ompds_version(void);
+/* Number of usable CUDA devices (0 when none). */
+int32_t ompds_device_count(void);
+
+/* ------------------------------------------------------------------------ */
+/* Team runtime protocol: omplab::TeamRuntime  (DeviceRuntime.h:81-119)     */
+/*                                                                          */
+/* The five operations run on the GPU through the same __device__ code the */
+/* generic-mode kernels inline (paper_1711_10413_b200/csrc/ompds_device.cuh).*/
+/* A script of calls is replayed in order by one device thread against one */
+/* team's shared-memory runtime state; every call's outcome is returned.   */
+/* ------------------------------------------------------------------------ */
+typedef struct ompds_runtime_config {  /* RuntimeConfig DeviceRuntime.h:40-43 */
+  int32_t prealloc_entries;   /* PreallocEntries (default 20)              */
+  int32_t fail_dynamic_alloc; /* FailDynamicAlloc test hook                */
+} ompds_runtime_config;
+
+enum { OMPDS_ROLE_MASTER = 0, OMPDS_ROLE_WORKER = 1 }; /* RtRole :54 */
+enum {
+  OMPDS_OP_KERNEL_INIT = 0,      /* TeamRuntime::kernelInit      cpp:33  */
+  OMPDS_OP_PREPARE_PARALLEL = 1, /* TeamRuntime::prepareParallel cpp:46  */
+  OMPDS_OP_KERNEL_PARALLEL = 2,  /* TeamRuntime::kernelParallel  cpp:81  */
+  OMPDS_OP_END_PARALLEL = 3,     /* TeamRuntime::endParallel     cpp:102 */
+  OMPDS_OP_KERNEL_DEINIT = 4     /* TeamRuntime::kernelDeinit    cpp:130 */
+};
+enum { /* where an args list lives */
+  OMPDS_ADDR_NULL = 0,     /* termination sentinel (kernelParallel, cpp:87-92) */
+  OMPDS_ADDR_PREALLOC = 1, /* the team's shared-memory window (PreallocBase)   */
+  OMPDS_ADDR_DYNAMIC = 2   /* a global-memory block (Heap.allocate)            */
+};
+
+typedef struct ompds_rt_call {
+  int32_t op;   /* OMPDS_OP_*                                   */
+  int32_t role; /* OMPDS_ROLE_*                                 */
+  int64_t arg;  /* workers for init, nargs for prepare_parallel */
+} ompds_rt_call;
+
+typedef struct ompds_rt_result {
+  int32_t status;      /* 0 or trap code                               */
+  int32_t addr_kind;   /* OMPDS_ADDR_* (prepare / kernel_parallel)     */
+  int32_t wf;          /* staged work-function id, -1 = none (sentinel) */
+  int32_t participate; /* kernel_parallel's Participate                */
+  int64_t live_bytes;  /* bytes of the live dynamic block, else 0      */
+  int64_t heap_live;   /* live dynamic blocks after the call           */
+} ompds_rt_result;
+
+enum { /* RuntimeEvent::Kind, DeviceRuntime.h:64-79 */
+  OMPDS_EV_INIT = 0,
+  OMPDS_EV_PREPARE_PREALLOC = 1,
+  OMPDS_EV_PREPARE_DYNAMIC = 2,
+  OMPDS_EV_FETCH = 3,
+  OMPDS_EV_RETIRE = 4,
+  OMPDS_EV_DYNAMIC_FREE = 5,
+  OMPDS_EV_DEINIT = 6
+};
+typedef struct ompds_event {
+  int32_t kind;  /* OMPDS_EV_*                                   */
+  int32_t fn;    /* work-function id (-1 when not applicable)    */
+  int64_t nargs; /* NArgs field: workers / nargs / remaining     */
+  int64_t bytes; /* Bytes field                                  */
+} ompds_event;
+
+typedef struct ompds_rt_summary { /* TeamRuntime accessors DeviceRuntime.h:97-102 */
+  int32_t workers;
+  int32_t terminated;
+  int64_t dynamic_allocs;
+  int64_t dynamic_frees;
+  int64_t leaked_blocks;
+  int32_t n_events; /* total events logged (may exceed max_events) */
+  int32_t _pad;
+} ompds_rt_summary;
+
+int32_t ompds_rt_replay(const ompds_runtime_config *config,
+                        const ompds_rt_call *calls, int32_t n_calls,
+                        ompds_rt_result *results, ompds_event *events,
+                        int32_t max_events, ompds_rt_summary *summary);
+
+/* Capacity law dynamicArgsBytes (DeviceRuntime.h:35-38). */
+int64_t ompds_dynamic_args_bytes(int64_t nargs, int32_t prealloc_entries);
+
+/* ------------------------------------------------------------------------ */
+/* Frame-layout descriptors: DepotSlot / DepotLayout / FrameGroup           */
+/* (IR.h:219-254) built by the reference's frame pipeline                   */
+/* (LoweringPasses.cpp: buildDepots :264-305, lowerSharedFrames :345-380,   */
+/*  colorStack :458-538, repackOffsets :556-593, audit :617-665).           */
+/* ------------------------------------------------------------------------ */
+enum { /* ompds_frame_var.flags */
+  OMPDS_VAR_ESCAPES = 1u << 0, /* address stored as a value (captured):
+                                  escapedAllocas, LoweringPasses.cpp:107-139 */
+  OMPDS_VAR_PINNED = 1u << 1   /* frame value stored / passed to a call:
+                                  never merged by coloring (:506-509)        */
+};
+enum { /* PipelineKind, LoweringPasses.h:43 */
+  OMPDS_PIPELINE_DEFAULT = 0,
+  OMPDS_PIPELINE_O0 = 1,
+  OMPDS_PIPELINE_BAD_ORDER = 2
+};
+
+typedef struct ompds_frame_var { /* one alloca, in emission order */
+  int32_t group;    /* frame group (0 = kernel + __omp_worker, then one per
+                       outlined / wrapper function; LoweringPasses.cpp:270-280) */
+  int32_t func;     /* member function within the group (coloring scope)  */
+  uint32_t flags;   /* OMPDS_VAR_*                                        */
+  int32_t def_pos;  /* position of the alloca in its function             */
+  int64_t bytes;    /* allocation size before rounding                    */
+  int32_t live_first; /* first / last position where the frame value      */
+  int32_t live_last;  /* itself is an operand (-1: never)                 */
+} ompds_frame_var;
+/* Liveness is given in post-codegen instruction positions.  The builder
+ * works in doubled coordinates (position p -> 2p) so that the address-space
+ * cast the frame pipeline inserts right after an escaping alloca sits at
+ * 2*def_pos+1 -- that cast is the escaping variable's only direct use when
+ * coloring runs (LoweringPasses.cpp:212-258, 393-422). */
+
+typedef struct ompds_depot_slot { /* DepotSlot IR.h:219-228 */
+  int64_t offset;
+  int64_t size;
+  int32_t align;
+  int32_t shared;      /* SharedResident                           */
+  int32_t owner_begin; /* index into the owners array (var indices) */
+  int32_t n_owners;
+} ompds_depot_slot;
+
+typedef struct ompds_depot_layout { /* DepotLayout IR.h:230-244 */
+  int64_t total_local;
+  int64_t total_shared; /* mirror of total_local */
+  int32_t has_shared_depot;
+  int32_t slot_begin; /* index into the slots array */
+  int32_t n_slots;
+  int32_t overlap_slot; /* findSharedLocalOverlap (IR.cpp:228-242), -1 none */
+} ompds_depot_layout;
+
+/* Runs the frame pipeline over `vars` (grouped by .group, n_groups groups).
+ * Writes n_groups layouts, their slots and owner lists.  Returns
+ * OMPDS_ERR_CAPACITY if max_slots / max_owners are too small. */
+int32_t ompds_layout_build(const ompds_frame_var *vars, int32_t n_vars,
+                           int32_t n_groups, int32_t pipeline,
+                           ompds_depot_layout *layouts,
+                           ompds_depot_slot *slots, int32_t max_slots,
+                           int32_t *owners, int32_t max_owners);
+
+/* Per-team shared footprint: depot + prealloc window + runtime span
+ * (Simulator.cpp:281-284, Occupancy.h:49-51). */
+int64_t ompds_shared_footprint(int64_t total_shared, int32_t prealloc_entries);
+
+/* ------------------------------------------------------------------------ */
+/* Occupancy model (Occupancy.h / Occupancy.cpp:77-105) + a B200 row.       */
+/* ------------------------------------------------------------------------ */
+typedef struct ompds_gpu_spec { /* GpuSpec Occupancy.h:24-31 */
+  int64_t shared_bytes_per_sm;
+  int64_t registers_per_sm;
+  int64_t max_blocks_per_sm;
+  int32_t warp_size;
+  int32_t max_regs_per_thread;
+  int64_t max_threads_per_sm;      /* 0 = unlimited (reference model)      */
+  int64_t reserved_smem_per_block; /* 0 in the reference model; 1 KB B200  */
+} ompds_gpu_spec;
+
+typedef struct ompds_occupancy { /* OccupancyResult Occupancy.h:62-68 */
+  int64_t teams_by_regs;
+  int64_t teams_by_smem;
+  int64_t potential;
+  int64_t actual;
+  int64_t smem_used;
+} ompds_occupancy;
+
+/* name: "k40-16k", "k40-32k", "k40-48k", "p100" (Occupancy.cpp:14-22) or
+ * "b200" (new). */
+int32_t ompds_gpu_spec_get(const char *name, ompds_gpu_spec *out);
+int32_t ompds_occupancy_for(const ompds_gpu_spec *gpu, int64_t footprint,
+                            int32_t regs_per_thread, int32_t threads_per_team,
+                            ompds_occupancy *out);
+int64_t ompds_max_regs_for_teams(const ompds_gpu_spec *gpu, int64_t teams,
+                                 int32_t threads_per_team);
+int64_t ompds_max_shared_vars(const ompds_gpu_spec *gpu, int64_t teams);
+
+/* ------------------------------------------------------------------------ */
+/* Generic-mode target-region launches (the sm_100a hot path).              */
+/*                                                                          */
+/* Each launch runs `teams` CTAs of roundup32(workers)+32 threads: workers  */
+/* [0,W), the master = first lane of the reserved last warp (Codegen.h:25-30,*/
+/* Codegen.cpp:345-397).  Per team the CTA's dynamic shared memory is the   */
+/* reference's team region [depot | 8*prealloc args window | 49 B runtime]  */
+/* (Simulator.cpp:281-292).  The master stages every region through        */
+/* prepare_parallel + named-barrier release/join; workers fetch it, read the */
+/* shared-variable list (warp-shuffle broadcast) and retire it.             */
+/* All pointers are DEVICE pointers unless the name says host.             */
+/* ------------------------------------------------------------------------ */
+typedef struct ompds_launch {
+  int32_t teams;            /* CTAs                                       */
+  int32_t workers;          /* W (thread_limit)                           */
+  int32_t prealloc_entries; /* shared-args window entries (default 20)     */
+  int32_t fail_dynamic_alloc;
+  int64_t depot_capacity;   /* master data-sharing slot bytes in smem;
+                               <0 = the layout's TotalShared (reference) */
+  int32_t log_events;       /* record per-team runtime events             */
+  int32_t max_events;       /* per-team event capacity when logging       */
+  void *stream;             /* cudaStream_t (NULL = default stream)       */
+} ompds_launch;
+
+typedef struct ompds_team_stats { /* per team, written by the kernel */
+  int32_t trap;                   /* first trap code, 0 = none            */
+  int32_t master_barriers;        /* master handoff barrier entries (2/region) */
+  int32_t barrier_releases;       /* handoff barrier releases (2R+1)      */
+  int32_t regions;                /* regions staged                       */
+  int64_t dynamic_alloc_bytes;
+  int32_t dynamic_allocs;
+  int32_t dynamic_frees;
+  int32_t depot_in_smem;          /* 1 = master frame in the smem slot, 0 = global overflow */
+  int32_t n_events;
+  int64_t depot_offset;           /* frame offset inside its slot         */
+  int64_t smem_bytes;             /* dynamic smem per CTA for this launch */
+} ompds_team_stats;
+
+/* Config 1: `regions` parallel regions in a sequential loop; the master
+ * shares 4 scalars (c1,c2 int32 = 1,2; c3,c4 = 3,4 stored as `elem`) and
+ * bumps c4 by 1 after every region; body a[team*W + tid] += c1+c2+c3+c4.
+ * elem: 0 = int32 (reference analog, a is int32[teams*W]),
+ *       1 = float64 (a is double[teams*W]; sum ((c1+c2) + c3) + c4 in fp64). */
+int32_t ompds_run_regions(const ompds_launch *launch, int32_t elem,
+                          int32_t regions, void *a,
+                          ompds_team_stats *stats_dev, ompds_event *events_dev);
+
+/* Config 2: a statically allocated shared array d[256] (depot slot
+ * 256*sizeof(elem)), d[k] = 3k+1 staged by the master -- by
+ * cp.async.bulk from `d_init` (device, 256 elems) when non-NULL, else by
+ * the master's own loop -- then `parallel for i<n: a[i] += d[i & 255]`
+ * on the cyclic schedule (AstLowering.cpp:429-462).
+ * elem: 0 = int32, 1 = float64. */
+int32_t ompds_run_shared_array(const ompds_launch *launch, int32_t elem,
+                               int64_t n, void *a, const void *d_init,
+                               ompds_team_stats *stats_dev,
+                               ompds_event *events_dev);
+
+/* Config 4/5: streaming region with 8 implicitly shared scalars
+ * c_k (k=1..8) on the cyclic schedule over elements [0, n):
+ *   float64: y[i] = fma(c1, x[i], y[i]) + s,  s = ((((((c2+c3)+c4)+c5)+c6)+c7)+c8)
+ *   int32  : y[i] = y[i] + (c1*x[i] + c2 + ... + c8)   (wrapping int32)
+ * `coef` (host, 8 values of elem type) are the master's initial values. */
+int32_t ompds_run_stream(const ompds_launch *launch, int32_t elem, int64_t n,
+                         const void *x, void *y, const void *coef_host,
+                         ompds_team_stats *stats_dev, ompds_event *events_dev);
+
+/* The same region end to end from HOST buffers (pinned recommended): copies
+ * x,y in, runs, copies y out, on `launch->stream`; synchronises. */
+int32_t ompds_run_stream_host(const ompds_launch *launch, int32_t elem,
+                              int64_t n, const void *x_host, void *y_host,
+                              const void *coef_host, void *x_dev_scratch,
+                              void *y_dev_scratch);
+
+/* Counter-based inputs: out[i] = U[-1,1) from splitmix64(seed + first + i)
+ * (float64), or (splitmix64(..) % 201) - 100 (int32). */
+int32_t ompds_fill_uniform(int32_t elem, void *out, int64_t n, uint64_t seed,
+                           int64_t first, void *stream);
+/* Order-independent checksum: sum of the elements' bit patterns mod 2^64
+ * (float64: 64-bit patterns; int32: sign-extended values).  Writes 8 bytes
+ * to `out_dev` (device). */
+int32_t ompds_checksum(int32_t elem, const void *data, int64_t n,
+                       uint64_t *out_dev, void *stream);
+
+/* Dynamic smem bytes per CTA the launchers request for a team region with
+ * depot `total_shared` (== ompds_shared_footprint for the reference layout). */
+int64_t ompds_team_smem_bytes(int64_t depot_capacity, int32_t prealloc_entries);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OMPDS_H */

@@ -1,0 +1,66 @@
+"""In-tree build of the sm_100a library (``_build/libompds_b200.so``).
+
+``nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo`` over
+``csrc/ompds_kernels.cu`` (device runtime + generic-mode kernels + C-ABI
+launchers) and ``csrc/ompds_host.cpp`` (layout builder, occupancy, trap
+strings).  nvcc cross-compiles without a GPU, so this runs in the CPU
+container; the .so travels to the GPU box with the repo snapshot.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OUT_DIR = os.path.join(HERE, "_build")
+LIB = os.path.join(OUT_DIR, "libompds_b200.so")
+SOURCES = [os.path.join(CSRC, "ompds_kernels.cu"), os.path.join(CSRC, "ompds_host.cpp")]
+HEADERS = [os.path.join(CSRC, "ompds_device.cuh"),
+           os.path.join(os.path.dirname(HERE), "include", "ompds.h")]
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC,-O2",
+    "-Xptxas", "-v",
+    "-shared",
+]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (os.path.sep not in cand or os.path.exists(cand)):
+            return cand
+    return "nvcc"
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(s) > t for s in SOURCES + HEADERS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    os.makedirs(OUT_DIR, exist_ok=True)
+    tmp = LIB + ".tmp"
+    cmd = [nvcc()] + NVCC_FLAGS + ["-o", tmp] + SOURCES
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    log = res.stdout + res.stderr
+    with open(os.path.join(OUT_DIR, "ptxas.log"), "w") as f:
+        f.write(" ".join(cmd) + "\n" + log)
+    if res.returncode != 0:
+        sys.stderr.write(log)
+        raise RuntimeError(f"nvcc failed ({res.returncode}) building {LIB}")
+    if verbose:
+        sys.stderr.write(log)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,551 @@
+// ompds_device.cuh -- sm_100a device runtime for implicit OpenMP data
+// sharing in generic-mode target regions (arXiv 1711.10413), B200-native.
+//
+// What the reference models on the host (proj/src/DeviceRuntime.cpp and the
+// team execution model of proj/src/Simulator.cpp) lives here as __device__
+// code that generic-mode kernels inline:
+//
+//   * team runtime state machine (Uninitialized -> Idle -> Staged -> ... ->
+//     Terminated) in the team's 49-byte runtime-private shared-memory span,
+//     with the reference's exact trap semantics (DeviceRuntime.cpp:33-143);
+//   * the shared-args list: 8*PreallocEntries bytes of shared memory right
+//     after the depot, or a block of the team's global overflow slab when a
+//     region captures more (DeviceRuntime.cpp:61-74, 108-121);
+//   * named-barrier region handoff (bar.sync <id>, <count>) replacing the
+//     simulator's "all live threads blocked" barrier (Simulator.cpp:481-499);
+//     every lane of the reserved warp stays resident and arrives, because
+//     exited threads never arrive at a hardware barrier;
+//   * warp-aggregated fetch/retire (one shared-memory atomic per warp instead
+//     of one per thread) and a warp-shuffle broadcast of the shared-variable
+//     pointer list (get-shared-variables, Codegen.cpp:215-267);
+//   * data-sharing stacks: per warp, a statically sized shared-memory slot
+//     plus a global-memory overflow chain, managed in registers by the warp
+//     that owns it (the master's kernel depot is its first frame,
+//     Simulator.cpp:439-479, 651-669).
+//
+// Entry points keep the reference / LLVM runtime names as aliases:
+//   __kmpc_kernel_init / _prepare_parallel / _parallel / _end_parallel /
+//   _deinit, __kmpc_data_sharing_push_stack / _pop_stack,
+//   __kmpc_get_shared_variables.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/ompds.h"
+
+namespace ompds {
+
+constexpr int kWarp = 32;
+constexpr uint32_t kBarHandoff = 1; // master <-> worker region handoff
+constexpr uint32_t kBarWorkers = 2; // worker-only sync inside a region
+
+enum Phase : uint8_t { kUninit = 0, kIdle = 1, kStaged = 2, kTerminated = 3 };
+enum Role : int { kMaster = OMPDS_ROLE_MASTER, kWorker = OMPDS_ROLE_WORKER };
+
+// Byte offsets inside the runtime-private span.  Exactly 49 bytes, the
+// reference's RuntimePrivateBytes (DeviceRuntime.h:31), so the team region
+// footprint is depot + 8*PreallocEntries + 49 as in Simulator.cpp:281-284.
+struct Rt {
+  static constexpr int kArgs = 0;      // u64 args list (generic address)
+  static constexpr int kWorkFn = 8;    // i32 staged work function, -1 none
+  static constexpr int kNArgs = 12;    // i32 staged nargs
+  static constexpr int kWorkers = 16;  // i32 Workers
+  static constexpr int kActive = 20;   // i32 Active
+  static constexpr int kHeapTop = 24;  // u32 bytes in use in the global slab
+  static constexpr int kDynAllocs = 28;// u32
+  static constexpr int kDynFrees = 32; // u32
+  static constexpr int kTrap = 36;     // i32 first trap code
+  static constexpr int kDynBytes = 40; // u32 dynamic args bytes allocated
+  static constexpr int kEvents = 44;   // u32 events logged
+  static constexpr int kPhase = 48;    // u8 phase
+  static constexpr int kBytes = 49;
+};
+static_assert(Rt::kBytes == OMPDS_RUNTIME_PRIVATE_BYTES, "rt span");
+
+__host__ __device__ constexpr int64_t round_up(int64_t v, int64_t a) {
+  return (v + a - 1) / a * a;
+}
+
+// Dynamic shared memory of one team: [depot | window | rt].
+__host__ __device__ constexpr int64_t team_region_bytes(int64_t depot,
+                                                        int prealloc) {
+  return depot + int64_t(prealloc) * OMPDS_SHARED_ARG_ENTRY_BYTES +
+         OMPDS_RUNTIME_PRIVATE_BYTES;
+}
+
+//===----------------------------------------------------------------------===//
+// Low-level primitives
+//===----------------------------------------------------------------------===//
+
+__device__ __forceinline__ void bar_sync(uint32_t id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ uint32_t lane_id() {
+  uint32_t l;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+  return l;
+}
+
+__device__ __forceinline__ bool is_shared_addr(const void *p) {
+  return __isShared(p);
+}
+
+//===----------------------------------------------------------------------===//
+// Team context
+//===----------------------------------------------------------------------===//
+
+struct TeamCtx {
+  unsigned char *region;   // team region in shared memory (generic address)
+  int64_t depot_cap;       // master data-sharing slot bytes at region[0..)
+  void **window;           // the preallocated shared-args list
+  unsigned char *rt;       // runtime-private span
+  unsigned char *slab;     // team's global overflow slab (args lists + frames)
+  uint32_t slab_bytes;
+  int32_t prealloc;        // PreallocEntries
+  int32_t fail_dyn;        // FailDynamicAlloc
+  ompds_event *events;     // per-team event log (nullptr: off)
+  int32_t max_events;
+
+  template <class T> __device__ __forceinline__ T &at(int off) const {
+    return *reinterpret_cast<T *>(rt + off);
+  }
+  __device__ __forceinline__ uint8_t &phase() const { return at<uint8_t>(Rt::kPhase); }
+  __device__ __forceinline__ int32_t &active() const { return at<int32_t>(Rt::kActive); }
+  __device__ __forceinline__ void *&args() const { return at<void *>(Rt::kArgs); }
+  __device__ __forceinline__ int32_t &work_fn() const { return at<int32_t>(Rt::kWorkFn); }
+  __device__ __forceinline__ int32_t &nargs() const { return at<int32_t>(Rt::kNArgs); }
+
+  __device__ __forceinline__ bool args_dynamic() const {
+    void *a = args();
+    return a != nullptr && a != static_cast<void *>(window);
+  }
+
+  // Records the first trap of the team (Simulator's R.Trapped semantics).
+  __device__ __forceinline__ int32_t trap(int32_t code) const {
+    atomicCAS(&at<int32_t>(Rt::kTrap), 0, code);
+    return code;
+  }
+
+  __device__ __forceinline__ void log(int32_t kind, int32_t fn, int64_t nargs,
+                                      int64_t bytes) const {
+    if (!events)
+      return;
+    uint32_t i = atomicAdd(&at<uint32_t>(Rt::kEvents), 1u);
+    if (static_cast<int32_t>(i) < max_events)
+      events[i] = ompds_event{kind, fn, nargs, bytes};
+  }
+  // Reserves `n` consecutive event slots, returns the first (or -1 if off).
+  __device__ __forceinline__ int64_t log_reserve(uint32_t n) const {
+    if (!events)
+      return -1;
+    return atomicAdd(&at<uint32_t>(Rt::kEvents), n);
+  }
+  __device__ __forceinline__ void log_at(int64_t i, int32_t kind, int32_t fn,
+                                         int64_t nargs, int64_t bytes) const {
+    if (i >= 0 && i < max_events)
+      events[i] = ompds_event{kind, fn, nargs, bytes};
+  }
+
+  // LIFO allocator over the team's global slab.  The reference heap never
+  // reuses memory (Simulator.cpp:150-162); ours is a stack because at most
+  // one args list per team level is live (the phase machine forbids a new
+  // prepare while a region is in flight).
+  __device__ __forceinline__ void *slab_alloc(int64_t bytes) const {
+    uint32_t &top = at<uint32_t>(Rt::kHeapTop);
+    int64_t need = round_up(bytes, 16);
+    if (slab == nullptr || top + need > slab_bytes)
+      return nullptr;
+    void *p = slab + top;
+    top += static_cast<uint32_t>(need);
+    return p;
+  }
+  __device__ __forceinline__ void slab_free(void *p) const {
+    at<uint32_t>(Rt::kHeapTop) =
+        static_cast<uint32_t>(static_cast<unsigned char *>(p) - slab);
+  }
+};
+
+// Carves the team region out of dynamic shared memory and zero-initialises
+// the runtime span (the simulator zero-fills team memory, Simulator.cpp:286).
+__device__ __forceinline__ TeamCtx make_team(unsigned char *smem,
+                                             int64_t depot_cap, int prealloc,
+                                             int fail_dyn, unsigned char *slab,
+                                             uint32_t slab_bytes,
+                                             ompds_event *events,
+                                             int max_events) {
+  TeamCtx t;
+  t.region = smem;
+  t.depot_cap = depot_cap;
+  t.window = reinterpret_cast<void **>(smem + depot_cap);
+  t.rt = smem + depot_cap + int64_t(prealloc) * OMPDS_SHARED_ARG_ENTRY_BYTES;
+  t.slab = slab;
+  t.slab_bytes = slab_bytes;
+  t.prealloc = prealloc;
+  t.fail_dyn = fail_dyn;
+  t.events = events;
+  t.max_events = max_events;
+  return t;
+}
+
+__device__ __forceinline__ void rt_zero(const TeamCtx &t) {
+  for (int i = 0; i < Rt::kBytes; ++i)
+    t.rt[i] = 0;
+  t.work_fn() = -1;
+}
+
+//===----------------------------------------------------------------------===//
+// Team runtime protocol -- single-caller semantics, identical to
+// omplab::TeamRuntime (DeviceRuntime.cpp:33-143), trap order included.
+//===----------------------------------------------------------------------===//
+
+__device__ inline int32_t kernel_init(const TeamCtx &t, int role,
+                                      int32_t workers) {
+  if (role != kMaster)
+    return OMPDS_TRAP_INIT_FROM_WORKER;
+  if (t.phase() != kUninit)
+    return OMPDS_TRAP_INIT_TWICE;
+  if (workers <= 0)
+    return OMPDS_TRAP_INIT_NO_WORKERS;
+  t.phase() = kIdle;
+  t.at<int32_t>(Rt::kWorkers) = workers;
+  t.log(OMPDS_EV_INIT, -1, workers, 0);
+  return OMPDS_OK;
+}
+
+// __kmpc_kernel_prepare_parallel / begin-sharing-variables: stages work
+// function `fn` and returns the list the master fills with nargs pointers.
+__device__ inline int32_t prepare_parallel(const TeamCtx &t, int role,
+                                           int32_t fn, int64_t nargs,
+                                           void ***out) {
+  if (role != kMaster)
+    return OMPDS_TRAP_PREPARE_FROM_WORKER;
+  uint8_t ph = t.phase();
+  if (ph == kUninit)
+    return OMPDS_TRAP_PREPARE_BEFORE_INIT;
+  if (ph == kTerminated)
+    return OMPDS_TRAP_PREPARE_AFTER_DEINIT;
+  if (ph == kStaged || t.active() > 0)
+    return OMPDS_TRAP_PREPARE_IN_FLIGHT;
+  if (nargs < 0)
+    return OMPDS_TRAP_NEGATIVE_NARGS;
+  void **list;
+  if (nargs <= t.prealloc) {
+    list = t.window;
+    t.log(OMPDS_EV_PREPARE_PREALLOC, fn, nargs, 0);
+  } else {
+    int64_t bytes = nargs * OMPDS_SHARED_ARG_ENTRY_BYTES;
+    void *p = t.fail_dyn ? nullptr : t.slab_alloc(bytes);
+    if (p == nullptr)
+      return OMPDS_TRAP_ARGS_ALLOC_FAILED;
+    list = static_cast<void **>(p);
+    t.at<uint32_t>(Rt::kDynAllocs) += 1;
+    t.at<uint32_t>(Rt::kDynBytes) += static_cast<uint32_t>(bytes);
+    t.log(OMPDS_EV_PREPARE_DYNAMIC, fn, nargs, bytes);
+  }
+  t.args() = list;
+  t.nargs() = static_cast<int32_t>(nargs);
+  t.work_fn() = fn;
+  t.phase() = kStaged;
+  *out = list;
+  return OMPDS_OK;
+}
+
+// __kmpc_kernel_parallel: a worker fetches the staged region.
+__device__ inline int32_t kernel_parallel(const TeamCtx &t, int role,
+                                          int32_t *fn, void ***args,
+                                          bool *participate) {
+  if (role != kWorker)
+    return OMPDS_TRAP_PARALLEL_FROM_MASTER;
+  uint8_t ph = t.phase();
+  if (ph == kTerminated) {
+    *fn = -1;
+    *args = nullptr;
+    *participate = false;
+    return OMPDS_OK;
+  }
+  if (ph != kStaged)
+    return OMPDS_TRAP_PARALLEL_NOT_STAGED;
+  *fn = t.work_fn();
+  *args = static_cast<void **>(t.args());
+  *participate = true;
+  t.active() += 1;
+  t.log(OMPDS_EV_FETCH, *fn, 0, 0);
+  return OMPDS_OK;
+}
+
+__device__ __forceinline__ void retire_last(const TeamCtx &t) {
+  if (t.args_dynamic()) {
+    int64_t bytes = int64_t(t.nargs()) * OMPDS_SHARED_ARG_ENTRY_BYTES;
+    t.slab_free(t.args());
+    t.at<uint32_t>(Rt::kDynFrees) += 1;
+    t.log(OMPDS_EV_DYNAMIC_FREE, -1, 0, bytes);
+  }
+  t.work_fn() = -1;
+  t.args() = nullptr;
+  t.nargs() = 0;
+  t.phase() = kIdle;
+}
+
+// __kmpc_kernel_end_parallel: a worker retires; the last one frees the
+// dynamic list and returns the team to Idle.
+__device__ inline int32_t end_parallel(const TeamCtx &t, int role) {
+  if (role != kWorker)
+    return OMPDS_TRAP_END_FROM_MASTER;
+  if (t.phase() != kStaged || t.active() <= 0)
+    return OMPDS_TRAP_END_NOT_ACTIVE;
+  int32_t rem = --t.active();
+  t.log(OMPDS_EV_RETIRE, -1, rem, 0);
+  if (rem == 0)
+    retire_last(t);
+  return OMPDS_OK;
+}
+
+__device__ inline int32_t kernel_deinit(const TeamCtx &t, int role) {
+  if (role != kMaster)
+    return OMPDS_TRAP_DEINIT_FROM_WORKER;
+  uint8_t ph = t.phase();
+  if (ph == kUninit)
+    return OMPDS_TRAP_DEINIT_BEFORE_INIT;
+  if (ph == kStaged || t.active() > 0)
+    return OMPDS_TRAP_DEINIT_IN_FLIGHT;
+  if (ph == kTerminated)
+    return OMPDS_TRAP_DEINIT_TWICE;
+  t.phase() = kTerminated;
+  t.log(OMPDS_EV_DEINIT, -1, 0, 0);
+  return OMPDS_OK;
+}
+
+//===----------------------------------------------------------------------===//
+// Warp-aggregated fetch / retire used by the generic-mode worker loop.  A
+// warp call with m participating lanes is equivalent to m single calls in
+// lane order: one shared-memory atomic per warp.
+//===----------------------------------------------------------------------===//
+
+struct Fetch {
+  int32_t fn;        // -1: termination sentinel (wf == null)
+  void **args;
+  int32_t nargs;
+  int32_t status;
+};
+
+// All 32 lanes of a worker warp call this after the release barrier.
+// `mine` = this lane is a requested worker (tid < W).
+__device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
+                                                     bool mine) {
+  Fetch f;
+  uint8_t ph = t.phase();
+  f.status = OMPDS_OK;
+  if (ph == kTerminated) {
+    f.fn = -1;
+    f.args = nullptr;
+    f.nargs = 0;
+    return f;
+  }
+  f.fn = t.work_fn();
+  f.args = static_cast<void **>(t.args());
+  f.nargs = t.nargs();
+  if (ph != kStaged) {
+    f.status = mine ? t.trap(OMPDS_TRAP_PARALLEL_NOT_STAGED) : OMPDS_OK;
+    f.fn = -1;
+    return f;
+  }
+  const uint32_t ballot = __ballot_sync(0xffffffffu, mine);
+  const uint32_t lane = lane_id();
+  const uint32_t n = __popc(ballot);
+  if (n) {
+    const uint32_t leader = __ffs(ballot) - 1;
+    int64_t ev = -1;
+    if (lane == leader) {
+      atomicAdd(&t.active(), static_cast<int32_t>(n));
+      ev = t.log_reserve(n);
+    }
+    ev = __shfl_sync(0xffffffffu, ev, leader);
+    if (mine && ev >= 0)
+      t.log_at(ev + __popc(ballot & ((1u << lane) - 1u)), OMPDS_EV_FETCH, f.fn,
+               0, 0);
+  }
+  return f;
+}
+
+// All 32 lanes of a worker warp call this when the region body is done.
+__device__ __forceinline__ void end_parallel_warp(const TeamCtx &t, bool mine) {
+  const uint32_t ballot = __ballot_sync(0xffffffffu, mine);
+  const uint32_t n = __popc(ballot);
+  if (n == 0)
+    return;
+  const uint32_t lane = lane_id();
+  const uint32_t leader = __ffs(ballot) - 1;
+  if (lane == leader) {
+    int32_t old = atomicSub(&t.active(), static_cast<int32_t>(n));
+    if (t.events) {
+      int64_t ev = t.log_reserve(n);
+      for (uint32_t k = 0; k < n; ++k)
+        t.log_at(ev + k, OMPDS_EV_RETIRE, -1, old - 1 - int32_t(k), 0);
+    }
+    if (old == static_cast<int32_t>(n))
+      retire_last(t); // this warp retired the region's last participant
+  }
+  __syncwarp();
+}
+
+//===----------------------------------------------------------------------===//
+// get-shared-variables with a warp-shuffle broadcast.  Lane j < nargs loads
+// entry j of the list (one coalesced 8-byte-per-lane load, from shared memory
+// or the global overflow block); capture j is then a register shuffle away.
+//===----------------------------------------------------------------------===//
+
+struct SharedVars {
+  void *mine; // this lane's entry (lane j holds entry j)
+  __device__ __forceinline__ void *get(int j) const {
+    return reinterpret_cast<void *>(__shfl_sync(
+        0xffffffffu, reinterpret_cast<unsigned long long>(mine), j));
+  }
+};
+
+__device__ __forceinline__ SharedVars get_shared_variables(void **args,
+                                                           int32_t nargs) {
+  SharedVars v;
+  const uint32_t lane = lane_id();
+  v.mine = (args != nullptr && static_cast<int32_t>(lane) < nargs) ? args[lane]
+                                                                   : nullptr;
+  return v;
+}
+
+// Loads capture j's value through its pointer: lane j dereferences, then a
+// shuffle broadcasts the value (T is 4 or 8 bytes).
+template <class T>
+__device__ __forceinline__ T shared_value(const SharedVars &v, int j) {
+  T x{};
+  if (static_cast<int>(lane_id()) == j && v.mine)
+    x = *static_cast<const volatile T *>(v.mine);
+  return __shfl_sync(0xffffffffu, x, j);
+}
+
+//===----------------------------------------------------------------------===//
+// Data-sharing stack: one per warp, owned and managed in registers by that
+// warp.  A statically sized slot in shared memory holds frames while they
+// fit; once a push does not fit, frames continue on the warp's global-memory
+// overflow chain until popped back (strict LIFO).  The master (1 lane)
+// pushes DataSize; a worker warp pushes one DataSize frame per lane.
+//===----------------------------------------------------------------------===//
+
+struct Frame {
+  unsigned char *base; // lane 0's frame (lane l: base + l*bytes_per_lane)
+  int64_t offset;      // offset inside its segment
+  int32_t in_smem;     // 1: shared-memory slot, 0: global overflow chain
+  int32_t status;
+};
+
+struct DsStack {
+  unsigned char *slot; // shared-memory slot (generic address)
+  int64_t slot_cap;
+  int64_t top;         // bytes used in the slot
+  unsigned char *ovf;  // global overflow chain for this warp
+  int64_t ovf_cap;
+  int64_t ovf_top;     // bytes used on the chain
+  int32_t depth;
+  int32_t max_depth;
+  int64_t high_water;  // max bytes in use (slot + chain)
+
+  __device__ __forceinline__ void init(unsigned char *s, int64_t cap,
+                                       unsigned char *o, int64_t ocap) {
+    slot = s;
+    slot_cap = cap;
+    top = 0;
+    ovf = o;
+    ovf_cap = ocap;
+    ovf_top = 0;
+    depth = 0;
+    max_depth = 0;
+    high_water = 0;
+  }
+
+  // __kmpc_data_sharing_push_stack(bytes_per_lane * lanes)
+  __device__ __forceinline__ Frame push(int64_t bytes_per_lane, int lanes) {
+    Frame f;
+    const int64_t need = round_up(bytes_per_lane * lanes, 8);
+    f.status = OMPDS_OK;
+    if (ovf_top == 0 && top + need <= slot_cap) {
+      f.base = slot + top;
+      f.offset = top;
+      f.in_smem = 1;
+      top += need;
+    } else if (ovf != nullptr && ovf_top + need <= ovf_cap) {
+      f.base = ovf + ovf_top;
+      f.offset = ovf_top;
+      f.in_smem = 0;
+      ovf_top += need;
+    } else {
+      f.base = nullptr;
+      f.offset = -1;
+      f.in_smem = 0;
+      f.status = OMPDS_TRAP_STACK_OVERFLOW;
+      return f;
+    }
+    ++depth;
+    if (depth > max_depth)
+      max_depth = depth;
+    if (top + ovf_top > high_water)
+      high_water = top + ovf_top;
+    return f;
+  }
+
+  // __kmpc_data_sharing_pop_stack(frame)
+  __device__ __forceinline__ int32_t pop(const Frame &f) {
+    if (depth <= 0 || f.offset < 0)
+      return OMPDS_TRAP_STACK_UNDERFLOW;
+    if (f.in_smem) {
+      if (ovf_top != 0 || f.offset > top)
+        return OMPDS_TRAP_STACK_UNDERFLOW;
+      top = f.offset;
+    } else {
+      if (f.offset > ovf_top)
+        return OMPDS_TRAP_STACK_UNDERFLOW;
+      ovf_top = f.offset;
+    }
+    --depth;
+    return OMPDS_OK;
+  }
+};
+
+//===----------------------------------------------------------------------===//
+// Reference / LLVM-runtime entry-point names.
+//===----------------------------------------------------------------------===//
+
+__device__ __forceinline__ int32_t __kmpc_kernel_init(const TeamCtx &t,
+                                                      int32_t workers) {
+  return kernel_init(t, kMaster, workers);
+}
+__device__ __forceinline__ int32_t
+__kmpc_kernel_prepare_parallel(const TeamCtx &t, int32_t fn, int64_t nargs,
+                               void ***args) {
+  return prepare_parallel(t, kMaster, fn, nargs, args);
+}
+__device__ __forceinline__ int32_t __kmpc_kernel_parallel(const TeamCtx &t,
+                                                          int32_t *fn,
+                                                          void ***args,
+                                                          bool *p) {
+  return kernel_parallel(t, kWorker, fn, args, p);
+}
+__device__ __forceinline__ int32_t __kmpc_kernel_end_parallel(const TeamCtx &t) {
+  return end_parallel(t, kWorker);
+}
+__device__ __forceinline__ int32_t __kmpc_kernel_deinit(const TeamCtx &t) {
+  return kernel_deinit(t, kMaster);
+}
+__device__ __forceinline__ SharedVars __kmpc_get_shared_variables(void **args,
+                                                                  int32_t n) {
+  return get_shared_variables(args, n);
+}
+__device__ __forceinline__ Frame
+__kmpc_data_sharing_push_stack(DsStack &s, int64_t bytes, int lanes) {
+  return s.push(bytes, lanes);
+}
+__device__ __forceinline__ int32_t __kmpc_data_sharing_pop_stack(DsStack &s,
+                                                                 const Frame &f) {
+  return s.pop(f);
+}
+
+} // namespace ompds

@@ -1,0 +1,313 @@
+// ompds_host.cpp -- host half of the C ABI (include/ompds.h): trap strings,
+// the frame-layout descriptor builder and the occupancy model.  No CUDA here;
+// these are the compile-time / launch-planning parts of the path that the
+// reference also runs on the host (proj/src/LoweringPasses.cpp,
+// proj/src/Occupancy.cpp), restated from their published behaviour.
+#include "../../include/ompds.h"
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+namespace {
+
+// proj/src/DeviceRuntime.cpp:33-143, byte for byte.
+const char *const kTrapStrings[] = {
+    "",
+    "protocol error: kernel_init from a worker thread",
+    "protocol error: kernel_init called twice",
+    "protocol error: kernel_init with no workers",
+    "protocol error: prepare_parallel from a worker thread",
+    "protocol error: prepare_parallel before init",
+    "protocol error: prepare_parallel after deinit",
+    "protocol error: prepare_parallel while a region is in flight",
+    "protocol error: negative shared-args count",
+    "shared-args-alloc-failed",
+    "protocol error: kernel_parallel from the master thread",
+    "protocol error: kernel_parallel with no staged region",
+    "protocol error: end_parallel from the master thread",
+    "protocol error: end_parallel with no active region",
+    "protocol error: kernel_deinit from a worker thread",
+    "protocol error: kernel_deinit before init",
+    "protocol error: kernel_deinit while a region is in flight",
+    "protocol error: kernel_deinit called twice",
+    "data-sharing stack overflow",
+    "data-sharing stack underflow",
+};
+
+int64_t roundUp8(int64_t n) { return (n + 7) & ~int64_t(7); }
+
+// Working state of one depot slot while the pipeline runs.
+struct Slot {
+  int64_t size = 0;
+  int32_t align = 8;
+  bool shared = false;
+  std::vector<int32_t> owners; // var indices; empty = dropped by repacking
+};
+
+// Coloring liveness of one slot, in doubled coordinates (see ompds.h).
+struct Live {
+  int64_t first = -1, last = -1;
+  bool pinned = false;
+  bool empty() const { return first < 0; }
+  bool disjoint(const Live &o) const {
+    if (empty() || o.empty())
+      return true;
+    return last < o.first || o.last < first;
+  }
+  void merge(const Live &o) {
+    if (o.empty())
+      return;
+    if (empty()) {
+      first = o.first;
+      last = o.last;
+      return;
+    }
+    first = std::min(first, o.first);
+    last = std::max(last, o.last);
+  }
+};
+
+struct Group {
+  std::vector<Slot> slots;
+  std::vector<int32_t> slot_var; // slot -> defining var
+};
+
+// lower-shared-frames (LoweringPasses.cpp:345-380): slots of escaping
+// variables become shared-resident.  Coloring may have merged other owners
+// into such a slot; they are dragged along (the hazard the audit catches).
+void lowerShared(Group &g, const ompds_frame_var *vars) {
+  for (Slot &s : g.slots)
+    for (int32_t v : s.owners)
+      if (vars[v].flags & OMPDS_VAR_ESCAPES)
+        s.shared = true;
+}
+
+// color-stack (LoweringPasses.cpp:458-538), per member function.
+void colorStack(Group &g, const ompds_frame_var *vars) {
+  // Member functions present in this group, in first-appearance order.
+  std::vector<int32_t> funcs;
+  for (int32_t v : g.slot_var)
+    if (std::find(funcs.begin(), funcs.end(), vars[v].func) == funcs.end())
+      funcs.push_back(vars[v].func);
+  for (int32_t f : funcs) {
+    std::vector<int32_t> ids; // slots whose frame index lives in f
+    for (size_t s = 0; s < g.slot_var.size(); ++s)
+      if (vars[g.slot_var[s]].func == f)
+        ids.push_back(static_cast<int32_t>(s));
+    if (ids.size() < 2)
+      continue; // SlotOfValue.size() < 2
+    std::vector<Live> live(g.slots.size());
+    for (int32_t s : ids) {
+      const ompds_frame_var &v = vars[g.slot_var[s]];
+      Live &l = live[s];
+      if (v.flags & OMPDS_VAR_ESCAPES) {
+        // The only direct use left is the cast right after the alloca.
+        if (v.def_pos >= 0)
+          l.first = l.last = 2 * int64_t(v.def_pos) + 1;
+      } else if (v.live_first >= 0) {
+        l.first = 2 * int64_t(v.live_first);
+        l.last = 2 * int64_t(v.live_last);
+        l.pinned = (v.flags & OMPDS_VAR_PINNED) != 0;
+      } else {
+        l.pinned = (v.flags & OMPDS_VAR_PINNED) != 0;
+      }
+    }
+    auto mergeable = [&](int32_t s) {
+      return !g.slots[s].shared && !live[s].pinned && !g.slots[s].owners.empty();
+    };
+    for (size_t a = 0; a < ids.size(); ++a) {
+      const int32_t sa = ids[a];
+      if (!mergeable(sa))
+        continue;
+      for (size_t b = a + 1; b < ids.size(); ++b) {
+        const int32_t sb = ids[b];
+        if (g.slots[sb].owners.empty() || !mergeable(sb))
+          continue;
+        if (live[sb].empty() || live[sa].empty())
+          continue; // dead slots are dropped by repacking, not merged
+        if (!live[sa].disjoint(live[sb]))
+          continue;
+        Slot &dst = g.slots[sa];
+        Slot &src = g.slots[sb];
+        dst.size = std::max(dst.size, src.size);
+        dst.align = std::max(dst.align, src.align);
+        dst.owners.insert(dst.owners.end(), src.owners.begin(), src.owners.end());
+        src.owners.clear();
+        live[sa].merge(live[sb]);
+      }
+    }
+  }
+}
+
+} // namespace
+
+extern "C" {
+
+const char *ompds_trap_reason(int32_t code) {
+  if (code < 0 ||
+      code >= static_cast<int32_t>(sizeof(kTrapStrings) / sizeof(kTrapStrings[0])))
+    return code == OMPDS_ERR_CUDA       ? "cuda error"
+           : code == OMPDS_ERR_INVALID  ? "invalid argument"
+           : code == OMPDS_ERR_CAPACITY ? "output capacity exceeded"
+                                        : "unknown status";
+  return kTrapStrings[code];
+}
+
+uint32_t ompds_version(void) { return 0x00010000u; }
+
+int64_t ompds_dynamic_args_bytes(int64_t nargs, int32_t prealloc_entries) {
+  return nargs <= prealloc_entries ? 0 : nargs * OMPDS_SHARED_ARG_ENTRY_BYTES;
+}
+
+int64_t ompds_shared_footprint(int64_t total_shared, int32_t prealloc_entries) {
+  return total_shared + int64_t(prealloc_entries) * OMPDS_SHARED_ARG_ENTRY_BYTES +
+         OMPDS_RUNTIME_PRIVATE_BYTES;
+}
+
+int32_t ompds_layout_build(const ompds_frame_var *vars, int32_t n_vars,
+                           int32_t n_groups, int32_t pipeline,
+                           ompds_depot_layout *layouts,
+                           ompds_depot_slot *slots, int32_t max_slots,
+                           int32_t *owners, int32_t max_owners) {
+  if (n_vars < 0 || n_groups < 0 || (n_vars && !vars) ||
+      (n_groups && !layouts) || pipeline < OMPDS_PIPELINE_DEFAULT ||
+      pipeline > OMPDS_PIPELINE_BAD_ORDER)
+    return OMPDS_ERR_INVALID;
+  for (int32_t i = 0; i < n_vars; ++i)
+    if (vars[i].group < 0 || vars[i].group >= n_groups || vars[i].bytes < 0)
+      return OMPDS_ERR_INVALID;
+
+  // build-depots (LoweringPasses.cpp:264-305): one slot per alloca in group
+  // emission order, size roundUp8, align 8.
+  std::vector<Group> groups(static_cast<size_t>(n_groups));
+  for (int32_t i = 0; i < n_vars; ++i) {
+    Group &g = groups[static_cast<size_t>(vars[i].group)];
+    Slot s;
+    s.size = roundUp8(vars[i].bytes);
+    s.owners.push_back(i);
+    g.slots.push_back(std::move(s));
+    g.slot_var.push_back(i);
+  }
+  for (Group &g : groups) {
+    switch (pipeline) {
+    case OMPDS_PIPELINE_DEFAULT: // planFor(Default) :38-43
+      lowerShared(g, vars);
+      colorStack(g, vars);
+      break;
+    case OMPDS_PIPELINE_O0: // :44-48, no coloring
+      lowerShared(g, vars);
+      break;
+    case OMPDS_PIPELINE_BAD_ORDER: // :49-54, coloring before lowering
+      colorStack(g, vars);
+      lowerShared(g, vars);
+      break;
+    }
+  }
+
+  // repack-offsets (:556-593): drop emptied slots, prefix-sum offsets,
+  // TotalShared mirrors TotalLocal.
+  int32_t ns = 0, no = 0;
+  for (int32_t gi = 0; gi < n_groups; ++gi) {
+    Group &g = groups[static_cast<size_t>(gi)];
+    ompds_depot_layout &L = layouts[gi];
+    std::memset(&L, 0, sizeof(L));
+    L.slot_begin = ns;
+    L.overlap_slot = -1;
+    int64_t off = 0;
+    for (const Slot &s : g.slots) {
+      if (s.owners.empty())
+        continue;
+      if (ns >= max_slots || no + static_cast<int32_t>(s.owners.size()) > max_owners)
+        return OMPDS_ERR_CAPACITY;
+      ompds_depot_slot &o = slots[ns];
+      o.offset = off;
+      o.size = s.size;
+      o.align = s.align;
+      o.shared = s.shared ? 1 : 0;
+      o.owner_begin = no;
+      o.n_owners = static_cast<int32_t>(s.owners.size());
+      for (int32_t v : s.owners)
+        owners[no++] = v;
+      // findSharedLocalOverlap (IR.cpp:228-242): a shared slot with >1 owner.
+      if (s.shared && s.owners.size() > 1 && L.overlap_slot < 0)
+        L.overlap_slot = L.n_slots;
+      if (s.shared)
+        L.has_shared_depot = 1;
+      off += s.size;
+      ++L.n_slots;
+      ++ns;
+    }
+    L.total_local = off;
+    L.total_shared = off;
+  }
+  return OMPDS_OK;
+}
+
+//===----------------------------------------------------------------------===//
+// Occupancy (proj/src/Occupancy.cpp:14-105) plus a measured-B200 row.
+//===----------------------------------------------------------------------===//
+
+int32_t ompds_gpu_spec_get(const char *name, ompds_gpu_spec *out) {
+  if (!name || !out)
+    return OMPDS_ERR_INVALID;
+  struct Row {
+    const char *name;
+    ompds_gpu_spec spec;
+  };
+  static const Row rows[] = {
+      {"k40-16k", {16384, 65536, 16, 32, 255, 0, 0}},
+      {"k40-32k", {32768, 65536, 16, 32, 255, 0, 0}},
+      {"k40-48k", {49152, 65536, 16, 32, 255, 0, 0}},
+      {"p100", {65536, 65536, 32, 32, 255, 0, 0}},
+      // B200 (sm_100a): 228 KB smem per SM with 1 KB reserved per CTA,
+      // 64K registers, 32 CTAs and 2048 threads per SM.
+      {"b200", {233472, 65536, 32, 32, 255, 2048, 1024}},
+  };
+  for (const Row &r : rows)
+    if (std::strcmp(r.name, name) == 0) {
+      *out = r.spec;
+      return OMPDS_OK;
+    }
+  return OMPDS_ERR_INVALID;
+}
+
+int32_t ompds_occupancy_for(const ompds_gpu_spec *g, int64_t footprint,
+                            int32_t regs, int32_t threads, ompds_occupancy *o) {
+  if (!g || !o)
+    return OMPDS_ERR_INVALID;
+  const int64_t regs_per_team = int64_t(regs) * threads;
+  o->teams_by_regs = regs_per_team > 0 ? g->registers_per_sm / regs_per_team : 0;
+  const int64_t per_team_smem = footprint > 0 ? footprint + g->reserved_smem_per_block : 0;
+  o->teams_by_smem = per_team_smem > 0 ? g->shared_bytes_per_sm / per_team_smem : 0;
+  o->potential = std::min(o->teams_by_regs, g->max_blocks_per_sm);
+  if (g->max_threads_per_sm > 0 && threads > 0)
+    o->potential = std::min<int64_t>(o->potential, g->max_threads_per_sm / threads);
+  o->actual = std::min(o->potential, o->teams_by_smem);
+  o->smem_used = o->potential * footprint;
+  return OMPDS_OK;
+}
+
+int64_t ompds_max_regs_for_teams(const ompds_gpu_spec *g, int64_t teams,
+                                 int32_t threads) {
+  if (!g)
+    return 0;
+  if (teams <= 0 || threads <= 0)
+    return g->max_regs_per_thread;
+  return std::min<int64_t>(g->registers_per_sm / (teams * threads),
+                           g->max_regs_per_thread);
+}
+
+int64_t ompds_max_shared_vars(const ompds_gpu_spec *g, int64_t teams) {
+  if (!g || teams <= 0)
+    return 0;
+  const int64_t budget = g->shared_bytes_per_sm / teams - g->reserved_smem_per_block;
+  // scalars fixture with no variables (wf.addr + args.addr) + a loop counter
+  const int64_t fixed =
+      ompds_shared_footprint(16, OMPDS_DEFAULT_PREALLOC_ENTRIES) + 8;
+  if (budget < fixed)
+    return 0;
+  return (budget - fixed) / 8;
+}
+
+} // extern "C"

@@ -1,0 +1,944 @@
+// ompds_kernels.cu -- generic-mode target-region kernels for sm_100a and the
+// C-ABI launchers of include/ompds.h.
+//
+// One CTA = one OpenMP team.  Worker warps [0, ceil(W/32)) run the worker
+// loop of proj/src/Codegen.cpp:403-513; the last warp is the reserved master
+// warp (Codegen.h:25-30): lane 0 is the master and commits every side effect
+// of the sequential region, lanes 1..31 execute it redundantly so the warp
+// stays converged for the aligned named barriers it must arrive at.
+//
+// Per region the master pays exactly two handoff barriers (release, join --
+// Codegen.cpp:304-309) and the team sees 2R+1 releases including the
+// termination release (the reference's "master death" release,
+// Simulator.cpp:475-478, is an explicit barrier with a null-work sentinel
+// here because exited threads never arrive at a hardware barrier).
+#include "ompds_device.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+namespace ompds {
+
+thread_local char g_last_error[512] = "";
+
+static int32_t cuda_fail(cudaError_t e, const char *what) {
+  std::snprintf(g_last_error, sizeof(g_last_error), "%s: %s", what,
+                cudaGetErrorString(e));
+  return OMPDS_ERR_CUDA;
+}
+#define OMPDS_CUDA(call)                                                       \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess)                                                     \
+      return cuda_fail(e_, #call);                                             \
+  } while (0)
+
+//===----------------------------------------------------------------------===//
+// Launch parameters shared by every generic-mode kernel.
+//===----------------------------------------------------------------------===//
+
+constexpr int kMaxCaptures = 32;
+
+struct TeamParams {
+  int32_t workers;       // W
+  int32_t prealloc;      // PreallocEntries
+  int32_t fail_dyn;
+  int32_t max_events;
+  int64_t depot_cap;     // master data-sharing slot in smem (bytes, 8-aligned)
+  int64_t total_shared;  // the layout's depot size (frame pushed by master)
+  unsigned char *slabs;  // teams * slab_bytes of global memory
+  uint32_t slab_bytes;
+  int32_t n_caps;
+  ompds_event *events;   // teams * max_events, or nullptr
+  ompds_team_stats *stats;
+  int64_t cap_off[kMaxCaptures]; // depot offsets of the captures (layout)
+  int64_t aux_off;       // depot offset of the sequential loop counter (-1)
+};
+
+// Master-warp view of the sequential region.  Every lane runs it; lane 0
+// (the master) commits side effects.
+struct Master {
+  TeamCtx t;
+  const TeamParams *p;
+  bool leader;
+  uint32_t team_threads;
+  int32_t trap = 0;
+  int32_t barriers = 0;
+  int32_t regions = 0;
+  DsStack ds;
+  Frame depot;
+
+  __device__ __forceinline__ int32_t sync_status(int32_t s) {
+    s = __shfl_sync(0xffffffffu, s, 0);
+    if (s && !trap) {
+      trap = s;
+      if (leader)
+        t.trap(s);
+    }
+    return s;
+  }
+
+  __device__ __forceinline__ int32_t init() {
+    int32_t s = 0;
+    if (leader)
+      s = kernel_init(t, kMaster, p->workers);
+    return sync_status(s);
+  }
+
+  // The kernel frame group's depot is the first frame of the master's
+  // data-sharing stack: the shared-memory slot when it fits, else the
+  // team's global overflow chain (placement decision of config 2).
+  __device__ __forceinline__ int32_t push_depot() {
+    unsigned char *ovf = t.slab ? t.slab + (t.slab_bytes / 2) : nullptr;
+    ds.init(t.region, p->depot_cap, ovf, t.slab_bytes / 2);
+    depot = ds.push(p->total_shared, 1);
+    if (depot.status == OMPDS_OK && !depot.in_smem) {
+      // zero-fill like pushActivation (Simulator.cpp:453-456); smem was
+      // zeroed in the prologue.
+      for (int64_t i = lane_id() * 8; i < p->total_shared; i += 32 * 8)
+        *reinterpret_cast<uint64_t *>(depot.base + i) = 0;
+      __syncwarp();
+    }
+    return sync_status(depot.status);
+  }
+
+  __device__ __forceinline__ unsigned char *cap(int j) const {
+    return depot.base + p->cap_off[j];
+  }
+
+  // prepare_parallel + publish &capture_j into the list + release + join.
+  __device__ __forceinline__ int32_t parallel(int32_t fn, int32_t nargs) {
+    void **list = nullptr;
+    int32_t s = 0;
+    if (leader)
+      s = prepare_parallel(t, kMaster, fn, nargs, &list);
+    if (sync_status(s))
+      return s;
+    list = reinterpret_cast<void **>(__shfl_sync(
+        0xffffffffu, reinterpret_cast<unsigned long long>(list), 0));
+    // The reserved warp publishes the pointer list lane-parallel (one
+    // coalesced store per 32 entries) instead of nargs scalar stores.
+    for (int j = lane_id(); j < nargs; j += 32)
+      list[j] = cap(j < kMaxCaptures ? j : 0);
+    bar_sync(kBarHandoff, team_threads); // release the workers
+    bar_sync(kBarHandoff, team_threads); // join
+    barriers += 2;
+    regions += 1;
+    return OMPDS_OK;
+  }
+
+  __device__ __forceinline__ void finish() {
+    int32_t s = 0;
+    if (leader)
+      s = kernel_deinit(t, kMaster);
+    sync_status(s);
+    if (leader && p->stats) {
+      ompds_team_stats st{};
+      st.trap = trap ? trap : t.at<int32_t>(Rt::kTrap);
+      st.master_barriers = barriers;
+      st.barrier_releases = barriers + 1;
+      st.regions = regions;
+      st.dynamic_alloc_bytes = t.at<uint32_t>(Rt::kDynBytes);
+      st.dynamic_allocs = static_cast<int32_t>(t.at<uint32_t>(Rt::kDynAllocs));
+      st.dynamic_frees = static_cast<int32_t>(t.at<uint32_t>(Rt::kDynFrees));
+      st.depot_in_smem = depot.in_smem;
+      st.depot_offset = depot.offset;
+      st.n_events = static_cast<int32_t>(t.at<uint32_t>(Rt::kEvents));
+      st.smem_bytes = team_region_bytes(p->depot_cap, p->prealloc);
+      p->stats[blockIdx.x] = st;
+    }
+    __syncwarp();
+    // Termination release: workers parked at await.work observe Terminated
+    // (the null work function) and leave their loop.
+    bar_sync(kBarHandoff, team_threads);
+  }
+};
+
+// Worker-side context handed to region bodies.
+struct Worker {
+  int32_t wid;  // omp_get_thread_num
+  bool mine;    // wid < W (padding lanes of the last worker warp idle)
+  int32_t team;
+  int32_t teams;
+  int32_t workers;
+};
+
+template <class Prog>
+__global__ void __launch_bounds__(1024, 1)
+    generic_mode_kernel(const __grid_constant__ TeamParams p,
+                        const __grid_constant__ typename Prog::Args a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t team_threads = blockDim.x;
+  const int warp = threadIdx.x >> 5;
+  const int worker_warps = static_cast<int>(team_threads >> 5) - 1;
+
+  TeamCtx t = make_team(
+      smem, p.depot_cap, p.prealloc, p.fail_dyn,
+      p.slabs ? p.slabs + size_t(blockIdx.x) * p.slab_bytes : nullptr,
+      p.slab_bytes,
+      p.events ? p.events + size_t(blockIdx.x) * p.max_events : nullptr,
+      p.max_events);
+  // Prologue: zero the team region (Simulator.cpp:286), runtime span last.
+  const int64_t region = team_region_bytes(p.depot_cap, p.prealloc);
+  for (int64_t i = threadIdx.x; i < region; i += team_threads)
+    smem[i] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    t.work_fn() = -1;
+  __syncthreads();
+
+  if (warp < worker_warps) {
+    Worker w;
+    w.wid = threadIdx.x;
+    w.mine = w.wid < p.workers;
+    w.team = blockIdx.x;
+    w.teams = gridDim.x;
+    w.workers = p.workers;
+    for (;;) {
+      bar_sync(kBarHandoff, team_threads); // await.work
+      Fetch f = begin_parallel_warp(t, w.mine);
+      if (f.fn < 0 && f.status == OMPDS_OK)
+        break; // termination sentinel
+      if (f.status == OMPDS_OK) {
+        SharedVars sv = get_shared_variables(f.args, f.nargs);
+        Prog::region(f.fn, sv, w, a);
+        end_parallel_warp(t, w.mine);
+      }
+      bar_sync(kBarHandoff, team_threads); // barrier.parallel (join)
+    }
+  } else {
+    Master m;
+    m.t = t;
+    m.p = &p;
+    m.leader = lane_id() == 0;
+    m.team_threads = team_threads;
+    if (m.init() == OMPDS_OK && m.push_depot() == OMPDS_OK)
+      Prog::master(m, a);
+    m.finish();
+  }
+}
+
+//===----------------------------------------------------------------------===//
+// Config 1: latency -- R regions sharing 4 scalars (2 int, 2 elem).
+//===----------------------------------------------------------------------===//
+
+template <class T> struct RegionsProg {
+  struct Args {
+    T *a;
+    int32_t regions;
+  };
+  __device__ static void master(Master &m, const Args &a) {
+    if (m.leader) {
+      *reinterpret_cast<int32_t *>(m.cap(0)) = 1;
+      *reinterpret_cast<int32_t *>(m.cap(1)) = 2;
+      *reinterpret_cast<T *>(m.cap(2)) = T(3);
+      *reinterpret_cast<T *>(m.cap(3)) = T(4);
+    }
+    int32_t *r = reinterpret_cast<int32_t *>(m.depot.base + m.p->aux_off);
+    for (int32_t i = 0; i < a.regions; ++i) {
+      if (m.leader)
+        *r = i;
+      if (m.parallel(0, 4) != OMPDS_OK)
+        return;
+      if (m.leader) // sequential code between regions: c4 += 1
+        *reinterpret_cast<T *>(m.cap(3)) += T(1);
+    }
+    if (m.leader)
+      *r = a.regions;
+  }
+  __device__ static void region(int32_t, const SharedVars &sv, const Worker &w,
+                                const Args &a) {
+    const int32_t c1 = shared_value<int32_t>(sv, 0);
+    const int32_t c2 = shared_value<int32_t>(sv, 1);
+    const T c3 = shared_value<T>(sv, 2);
+    const T c4 = shared_value<T>(sv, 3);
+    if (w.mine) {
+      T sum = (T(c1 + c2) + c3) + c4;
+      T *dst = a.a + size_t(w.team) * w.workers + w.wid;
+      *dst = *dst + sum;
+    }
+  }
+};
+
+//===----------------------------------------------------------------------===//
+// Config 2: static shared array d[256] staged by the master, parallel for.
+//===----------------------------------------------------------------------===//
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+               "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_inval(uint64_t *bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile(
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  const uint32_t addr = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  asm volatile("{\n"
+               ".reg .pred P;\n"
+               "WAIT_%=:\n"
+               "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+               "@!P bra WAIT_%=;\n"
+               "}\n" ::"r"(addr),
+               "r"(parity)
+               : "memory");
+}
+// One bulk copy global -> this CTA's shared memory, completing on `bar`.
+__device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src,
+                                         uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(dst_smem))),
+      "l"(src), "r"(bytes),
+      "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+
+template <class T> struct SharedArrayProg {
+  static constexpr int kLen = 256;
+  struct Args {
+    T *a;
+    int64_t n;
+    const T *d_init; // nullptr: the master's own loop d[k] = 3k+1
+  };
+  __device__ static void master(Master &m, const Args &a) {
+    T *d = reinterpret_cast<T *>(m.cap(0));
+    constexpr uint32_t bytes = kLen * sizeof(T);
+    if (a.d_init != nullptr && m.depot.in_smem) {
+      // TMA staging: the args window is idle until the first prepare, so
+      // its first 8 bytes host the transfer's mbarrier -- no extra smem.
+      uint64_t *bar = reinterpret_cast<uint64_t *>(m.t.window);
+      if (m.leader) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s(d, a.d_init, bytes, bar);
+        mbar_wait(bar, 0);
+        mbar_inval(bar);
+        *bar = 0;
+      }
+      __syncwarp();
+    } else if (a.d_init != nullptr) {
+      // depot on the global overflow chain: the reserved warp copies.
+      for (int k = lane_id(); k < kLen; k += 32)
+        d[k] = a.d_init[k];
+      __syncwarp();
+    } else if (m.leader) {
+      for (int k = 0; k < kLen; ++k)
+        d[k] = T(3 * k + 1);
+    }
+    if (m.leader && m.p->aux_off >= 0)
+      *reinterpret_cast<int32_t *>(m.depot.base + m.p->aux_off) = kLen;
+    __syncwarp();
+    m.parallel(0, 1);
+  }
+  __device__ static void region(int32_t, const SharedVars &sv, const Worker &w,
+                                const Args &a) {
+    const T *d = static_cast<const T *>(sv.get(0));
+    if (!w.mine)
+      return;
+    const int64_t gid = int64_t(w.team) * w.workers + w.wid;
+    const int64_t pool = int64_t(w.teams) * w.workers;
+    // Cyclic schedule over 16-byte units (AstLowering.cpp:429-462 applied
+    // to vectors; the body is element-wise, so results are identical).
+    constexpr int V = 16 / sizeof(T);
+    using Vec = typename std::conditional<sizeof(T) == 8, double2, int4>::type;
+    const int64_t units = a.n / V;
+    Vec *av = reinterpret_cast<Vec *>(a.a);
+    for (int64_t u = gid; u < units; u += pool) {
+      Vec v = av[u];
+      T *e = reinterpret_cast<T *>(&v);
+      const int base = static_cast<int>((u * V) & (kLen - 1));
+      const Vec dv = *reinterpret_cast<const Vec *>(d + base);
+      const T *de = reinterpret_cast<const T *>(&dv);
+#pragma unroll
+      for (int k = 0; k < V; ++k)
+        e[k] = e[k] + de[k];
+      av[u] = v;
+    }
+    for (int64_t i = units * V + gid; i < a.n; i += pool)
+      a.a[i] = a.a[i] + d[i & (kLen - 1)];
+  }
+};
+
+//===----------------------------------------------------------------------===//
+// Config 4/5: streaming region, 8 implicitly shared scalars.
+//===----------------------------------------------------------------------===//
+
+__device__ __forceinline__ double2 ld_stream(const double2 *p) {
+  return __ldcs(p);
+}
+__device__ __forceinline__ int4 ld_stream(const int4 *p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(double2 *p, double2 v) {
+  __stcs(p, v);
+}
+__device__ __forceinline__ void st_stream(int4 *p, int4 v) { __stcs(p, v); }
+
+__device__ __forceinline__ double stream_op(double c1, double x, double y,
+                                            double s) {
+  return __dadd_rn(__fma_rn(c1, x, y), s);
+}
+__device__ __forceinline__ int32_t stream_op(int32_t c1, int32_t x, int32_t y,
+                                             int32_t s) {
+  return static_cast<int32_t>(static_cast<uint32_t>(y) +
+                              (static_cast<uint32_t>(c1) *
+                                   static_cast<uint32_t>(x) +
+                               static_cast<uint32_t>(s)));
+}
+
+template <class T> struct StreamProg {
+  struct Args {
+    const T *x;
+    T *y;
+    int64_t n;
+    T coef[8];
+  };
+  __device__ static void master(Master &m, const Args &a) {
+    if (m.leader)
+      for (int k = 0; k < 8; ++k)
+        *reinterpret_cast<T *>(m.cap(k)) = a.coef[k];
+    __syncwarp();
+    m.parallel(0, 8);
+  }
+  __device__ static void region(int32_t, const SharedVars &sv, const Worker &w,
+                                const Args &a) {
+    // get-shared-variables: lane j dereferences capture j, shuffles spread
+    // the values; every lane folds c2..c8 in the same order.
+    T v{};
+    if (lane_id() < 8 && sv.mine)
+      v = *static_cast<const T *>(sv.mine);
+    const T c1 = __shfl_sync(0xffffffffu, v, 0);
+    T s = __shfl_sync(0xffffffffu, v, 1);
+#pragma unroll
+    for (int k = 2; k < 8; ++k) {
+      const T ck = __shfl_sync(0xffffffffu, v, k);
+      if constexpr (sizeof(T) == 8)
+        s = __dadd_rn(s, ck);
+      else
+        s = static_cast<T>(static_cast<uint32_t>(s) + static_cast<uint32_t>(ck));
+    }
+    if (!w.mine)
+      return;
+    constexpr int V = 16 / sizeof(T);
+    using Vec = typename std::conditional<sizeof(T) == 8, double2, int4>::type;
+    constexpr int U = 4; // 16-byte units in flight per thread per array
+    const int64_t gid = int64_t(w.team) * w.workers + w.wid;
+    const int64_t pool = int64_t(w.teams) * w.workers;
+    const int64_t units = a.n / V;
+    const Vec *xv = reinterpret_cast<const Vec *>(a.x);
+    Vec *yv = reinterpret_cast<Vec *>(a.y);
+    int64_t u = gid;
+    for (; u + (U - 1) * pool < units; u += U * pool) {
+      Vec xs[U], ys[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        xs[k] = ld_stream(xv + u + k * pool);
+        ys[k] = ld_stream(yv + u + k * pool);
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        T *xe = reinterpret_cast<T *>(&xs[k]);
+        T *ye = reinterpret_cast<T *>(&ys[k]);
+#pragma unroll
+        for (int e = 0; e < V; ++e)
+          ye[e] = stream_op(c1, xe[e], ye[e], s);
+        st_stream(yv + u + k * pool, ys[k]);
+      }
+    }
+    for (; u < units; u += pool) {
+      Vec xs = ld_stream(xv + u), ys = ld_stream(yv + u);
+      T *xe = reinterpret_cast<T *>(&xs);
+      T *ye = reinterpret_cast<T *>(&ys);
+#pragma unroll
+      for (int e = 0; e < V; ++e)
+        ye[e] = stream_op(c1, xe[e], ye[e], s);
+      st_stream(yv + u, ys);
+    }
+    for (int64_t i = units * V + gid; i < a.n; i += pool)
+      a.y[i] = stream_op(c1, a.x[i], a.y[i], s);
+  }
+};
+
+//===----------------------------------------------------------------------===//
+// Protocol replay: one device thread drives the single-caller runtime
+// functions over a team region in shared memory (the TeamRuntime API).
+//===----------------------------------------------------------------------===//
+
+__global__ void rt_replay_kernel(ompds_runtime_config cfg,
+                                 const ompds_rt_call *calls, int32_t n,
+                                 ompds_rt_result *res, ompds_event *events,
+                                 int32_t max_events, ompds_rt_summary *sum,
+                                 unsigned char *slab, uint32_t slab_bytes) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  if (threadIdx.x != 0)
+    return;
+  TeamCtx t = make_team(smem, 0, cfg.prealloc_entries, cfg.fail_dynamic_alloc,
+                        slab, slab_bytes, events, max_events);
+  const int64_t region = team_region_bytes(0, cfg.prealloc_entries);
+  for (int64_t i = 0; i < region; ++i)
+    smem[i] = 0;
+  t.work_fn() = -1;
+  int32_t fn_seq = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const ompds_rt_call c = calls[i];
+    ompds_rt_result r{};
+    r.wf = -1;
+    int32_t s = OMPDS_ERR_INVALID;
+    switch (c.op) {
+    case OMPDS_OP_KERNEL_INIT:
+      s = kernel_init(t, c.role, static_cast<int32_t>(c.arg));
+      break;
+    case OMPDS_OP_PREPARE_PARALLEL: {
+      void **list = nullptr;
+      s = prepare_parallel(t, c.role, fn_seq, c.arg, &list);
+      if (s == OMPDS_OK) {
+        ++fn_seq;
+        r.addr_kind = list == t.window ? OMPDS_ADDR_PREALLOC : OMPDS_ADDR_DYNAMIC;
+        r.live_bytes = t.args_dynamic() ? int64_t(t.nargs()) * 8 : 0;
+      }
+      break;
+    }
+    case OMPDS_OP_KERNEL_PARALLEL: {
+      int32_t fn = -1;
+      void **args = nullptr;
+      bool part = false;
+      s = kernel_parallel(t, c.role, &fn, &args, &part);
+      if (s == OMPDS_OK) {
+        r.wf = fn;
+        r.participate = part;
+        r.addr_kind = args == nullptr ? OMPDS_ADDR_NULL
+                      : args == t.window ? OMPDS_ADDR_PREALLOC
+                                         : OMPDS_ADDR_DYNAMIC;
+      }
+      break;
+    }
+    case OMPDS_OP_END_PARALLEL:
+      s = end_parallel(t, c.role);
+      break;
+    case OMPDS_OP_KERNEL_DEINIT:
+      s = kernel_deinit(t, c.role);
+      break;
+    }
+    r.status = s;
+    r.heap_live = t.args_dynamic() ? 1 : 0;
+    res[i] = r;
+  }
+  ompds_rt_summary out{};
+  out.workers = t.at<int32_t>(Rt::kWorkers);
+  out.terminated = t.phase() == kTerminated;
+  out.dynamic_allocs = t.at<uint32_t>(Rt::kDynAllocs);
+  out.dynamic_frees = t.at<uint32_t>(Rt::kDynFrees);
+  out.leaked_blocks = out.dynamic_allocs - out.dynamic_frees;
+  out.n_events = static_cast<int32_t>(t.at<uint32_t>(Rt::kEvents));
+  *sum = out;
+}
+
+//===----------------------------------------------------------------------===//
+// Inputs and checksums
+//===----------------------------------------------------------------------===//
+
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__global__ void fill_f64_kernel(double *out, int64_t n, uint64_t seed,
+                                int64_t first) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    const uint64_t z = splitmix64(seed + static_cast<uint64_t>(first + i));
+    out[i] = __dadd_rn(__dmul_rn(static_cast<double>(z >> 11),
+                                 2.220446049250313080847263336181640625e-16),
+                       -1.0);
+  }
+}
+__global__ void fill_i32_kernel(int32_t *out, int64_t n, uint64_t seed,
+                                int64_t first) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    const uint64_t z = splitmix64(seed + static_cast<uint64_t>(first + i));
+    out[i] = static_cast<int32_t>(z % 201) - 100;
+  }
+}
+
+template <class T>
+__global__ void checksum_kernel(const T *data, int64_t n,
+                                unsigned long long *out) {
+  unsigned long long acc = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    if constexpr (sizeof(T) == 8)
+      acc += __double_as_longlong(static_cast<double>(data[i]));
+    else
+      acc += static_cast<unsigned long long>(
+          static_cast<long long>(static_cast<int32_t>(data[i])));
+  }
+  for (int o = 16; o > 0; o >>= 1)
+    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ unsigned long long part[32];
+  if ((threadIdx.x & 31) == 0)
+    part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0ull;
+    for (int o = 16; o > 0; o >>= 1)
+      acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0)
+      atomicAdd(out, acc);
+  }
+}
+
+//===----------------------------------------------------------------------===//
+// Host side: workspace, layouts for the fixed configs, launch helpers.
+//===----------------------------------------------------------------------===//
+
+struct Workspace {
+  std::mutex mu;
+  int device = -1;
+  unsigned char *slabs = nullptr;
+  size_t slab_total = 0;
+  int sm_count = 0;
+};
+static Workspace g_ws;
+
+static int32_t ensure_slabs(size_t bytes, unsigned char **out) {
+  std::lock_guard<std::mutex> lk(g_ws.mu);
+  int dev = 0;
+  OMPDS_CUDA(cudaGetDevice(&dev));
+  if (g_ws.device != dev) {
+    g_ws.slabs = nullptr; // leaked on device switch (bounded, rare)
+    g_ws.slab_total = 0;
+    g_ws.device = dev;
+  }
+  if (g_ws.slab_total < bytes) {
+    if (g_ws.slabs)
+      OMPDS_CUDA(cudaFree(g_ws.slabs));
+    g_ws.slabs = nullptr;
+    OMPDS_CUDA(cudaMalloc(&g_ws.slabs, bytes));
+    g_ws.slab_total = bytes;
+  }
+  *out = g_ws.slabs;
+  return OMPDS_OK;
+}
+
+} // namespace ompds
+
+using namespace ompds;
+
+// Host layout builder (ompds_host.cpp).
+extern "C" int32_t ompds_layout_build(const ompds_frame_var *, int32_t, int32_t,
+                                      int32_t, ompds_depot_layout *,
+                                      ompds_depot_slot *, int32_t, int32_t *,
+                                      int32_t);
+
+namespace {
+
+// Kernel frame group of a fixed config, in the reference's emission order:
+// captured locals, then sequential loop counters, then __omp_worker's
+// wf.addr / args.addr (Codegen.cpp:413-430, LoweringPasses.cpp:264-305).
+struct FixedLayout {
+  int64_t total_shared = 0;
+  int64_t cap_off[kMaxCaptures] = {};
+  int64_t aux_off = -1;
+};
+
+int32_t build_fixed_layout(const std::vector<int64_t> &cap_bytes,
+                           int64_t aux_bytes, FixedLayout *out) {
+  std::vector<ompds_frame_var> vars;
+  for (int64_t b : cap_bytes)
+    vars.push_back({0, 0, OMPDS_VAR_ESCAPES, -1, b, -1, -1});
+  if (aux_bytes > 0)
+    vars.push_back({0, 0, 0, -1, aux_bytes, -1, -1});
+  vars.push_back({0, 1, OMPDS_VAR_PINNED, -1, 8, -1, -1}); // wf.addr
+  vars.push_back({0, 1, OMPDS_VAR_PINNED, -1, 8, -1, -1}); // args.addr
+  ompds_depot_layout lay{};
+  ompds_depot_slot slots[kMaxCaptures + 4];
+  int32_t owners[kMaxCaptures + 4];
+  int32_t s = ompds_layout_build(vars.data(), static_cast<int32_t>(vars.size()),
+                                 1, OMPDS_PIPELINE_DEFAULT, &lay, slots,
+                                 kMaxCaptures + 4, owners, kMaxCaptures + 4);
+  if (s)
+    return s;
+  out->total_shared = lay.total_shared;
+  // Without merges every var owns its slot, in order.
+  for (size_t j = 0; j < cap_bytes.size(); ++j)
+    out->cap_off[j] = slots[j].offset;
+  if (aux_bytes > 0)
+    out->aux_off = slots[cap_bytes.size()].offset;
+  return OMPDS_OK;
+}
+
+int32_t validate_launch(const ompds_launch *l) {
+  if (!l || l->teams <= 0 || l->workers <= 0 || l->workers > 992 ||
+      l->prealloc_entries < 0 || l->prealloc_entries > 4096)
+    return OMPDS_ERR_INVALID;
+  return OMPDS_OK;
+}
+
+constexpr uint32_t kSlabBytes = 8192; // per team: args lists + depot overflow
+
+template <class Prog>
+int32_t launch_generic(const ompds_launch *l, const FixedLayout &lay,
+                       int32_t n_caps, const typename Prog::Args &args,
+                       ompds_team_stats *stats, ompds_event *events) {
+  int32_t s = validate_launch(l);
+  if (s)
+    return s;
+  int ndev = 0;
+  OMPDS_CUDA(cudaGetDeviceCount(&ndev));
+  TeamParams p{};
+  p.workers = l->workers;
+  p.prealloc = l->prealloc_entries;
+  p.fail_dyn = l->fail_dynamic_alloc;
+  p.max_events = l->log_events ? l->max_events : 0;
+  p.total_shared = lay.total_shared;
+  p.depot_cap = l->depot_capacity < 0 ? lay.total_shared
+                                      : round_up(l->depot_capacity, 8);
+  p.events = l->log_events ? events : nullptr;
+  p.stats = stats;
+  p.n_caps = n_caps;
+  for (int j = 0; j < kMaxCaptures; ++j)
+    p.cap_off[j] = lay.cap_off[j];
+  p.aux_off = lay.aux_off;
+  p.slab_bytes = std::max<uint32_t>(
+      kSlabBytes, static_cast<uint32_t>(round_up(2 * lay.total_shared + 64, 256)));
+  s = ensure_slabs(size_t(p.slab_bytes) * l->teams, &p.slabs);
+  if (s)
+    return s;
+  const int threads = static_cast<int>(round_up(l->workers, 32)) + 32;
+  const size_t smem = static_cast<size_t>(team_region_bytes(p.depot_cap, p.prealloc));
+  auto kern = generic_mode_kernel<Prog>;
+  if (smem > 48 * 1024)
+    OMPDS_CUDA(cudaFuncSetAttribute(kern,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+  cudaStream_t st = static_cast<cudaStream_t>(l->stream);
+  kern<<<l->teams, threads, smem, st>>>(p, args);
+  OMPDS_CUDA(cudaGetLastError());
+  return OMPDS_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+const char *ompds_last_error(void) { return g_last_error; }
+
+int32_t ompds_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess)
+    return 0;
+  return n;
+}
+
+int64_t ompds_team_smem_bytes(int64_t depot_capacity, int32_t prealloc) {
+  return team_region_bytes(round_up(depot_capacity, 8), prealloc);
+}
+
+int32_t ompds_rt_replay(const ompds_runtime_config *config,
+                        const ompds_rt_call *calls, int32_t n_calls,
+                        ompds_rt_result *results, ompds_event *events,
+                        int32_t max_events, ompds_rt_summary *summary) {
+  if (!config || n_calls < 0 || (n_calls && (!calls || !results)) ||
+      !summary || config->prealloc_entries < 0 ||
+      config->prealloc_entries > 4096 || max_events < 0)
+    return OMPDS_ERR_INVALID;
+  ompds_rt_call *d_calls = nullptr;
+  ompds_rt_result *d_res = nullptr;
+  ompds_event *d_ev = nullptr;
+  ompds_rt_summary *d_sum = nullptr;
+  unsigned char *d_slab = nullptr;
+  const uint32_t slab_bytes = 1u << 16;
+  cudaError_t e = cudaSuccess;
+  auto cleanup = [&]() {
+    cudaFree(d_calls);
+    cudaFree(d_res);
+    cudaFree(d_ev);
+    cudaFree(d_sum);
+    cudaFree(d_slab);
+  };
+  const size_t nc = static_cast<size_t>(std::max(n_calls, 1));
+  if ((e = cudaMalloc(&d_calls, nc * sizeof(ompds_rt_call))) ||
+      (e = cudaMalloc(&d_res, nc * sizeof(ompds_rt_result))) ||
+      (e = cudaMalloc(&d_ev, std::max(max_events, 1) * sizeof(ompds_event))) ||
+      (e = cudaMalloc(&d_sum, sizeof(ompds_rt_summary))) ||
+      (e = cudaMalloc(&d_slab, slab_bytes))) {
+    cleanup();
+    return cuda_fail(e, "ompds_rt_replay: cudaMalloc");
+  }
+  if (n_calls)
+    e = cudaMemcpy(d_calls, calls, n_calls * sizeof(ompds_rt_call),
+                   cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    const size_t smem =
+        static_cast<size_t>(team_region_bytes(0, config->prealloc_entries));
+    rt_replay_kernel<<<1, 32, smem>>>(*config, d_calls, n_calls, d_res,
+                                      max_events ? d_ev : nullptr, max_events,
+                                      d_sum, d_slab, slab_bytes);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess)
+    e = cudaDeviceSynchronize();
+  if (e == cudaSuccess && n_calls)
+    e = cudaMemcpy(results, d_res, n_calls * sizeof(ompds_rt_result),
+                   cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(summary, d_sum, sizeof(*summary), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && events && max_events) {
+    const int32_t n = std::min(summary->n_events, max_events);
+    if (n > 0)
+      e = cudaMemcpy(events, d_ev, n * sizeof(ompds_event),
+                     cudaMemcpyDeviceToHost);
+  }
+  cleanup();
+  if (e != cudaSuccess)
+    return cuda_fail(e, "ompds_rt_replay");
+  return OMPDS_OK;
+}
+
+int32_t ompds_run_regions(const ompds_launch *launch, int32_t elem,
+                          int32_t regions, void *a, ompds_team_stats *stats,
+                          ompds_event *events) {
+  if (!a || regions < 0 || (elem != 0 && elem != 1))
+    return OMPDS_ERR_INVALID;
+  FixedLayout lay;
+  // c1, c2 (int), c3, c4 (elem), r (loop counter): scalars take 8-byte slots.
+  int32_t s = build_fixed_layout({4, 4, elem ? 8 : 4, elem ? 8 : 4}, 4, &lay);
+  if (s)
+    return s;
+  if (elem == 0)
+    return launch_generic<RegionsProg<int32_t>>(
+        launch, lay, 4, {static_cast<int32_t *>(a), regions}, stats, events);
+  return launch_generic<RegionsProg<double>>(
+      launch, lay, 4, {static_cast<double *>(a), regions}, stats, events);
+}
+
+int32_t ompds_run_shared_array(const ompds_launch *launch, int32_t elem,
+                               int64_t n, void *a, const void *d_init,
+                               ompds_team_stats *stats, ompds_event *events) {
+  if (!a || n < 0 || (elem != 0 && elem != 1) ||
+      (reinterpret_cast<uintptr_t>(a) & 15))
+    return OMPDS_ERR_INVALID;
+  FixedLayout lay;
+  const int64_t esz = elem ? 8 : 4;
+  int32_t s = build_fixed_layout({256 * esz}, 4, &lay);
+  if (s)
+    return s;
+  if (elem == 0)
+    return launch_generic<SharedArrayProg<int32_t>>(
+        launch, lay, 1,
+        {static_cast<int32_t *>(a), n, static_cast<const int32_t *>(d_init)},
+        stats, events);
+  return launch_generic<SharedArrayProg<double>>(
+      launch, lay, 1,
+      {static_cast<double *>(a), n, static_cast<const double *>(d_init)}, stats,
+      events);
+}
+
+int32_t ompds_run_stream(const ompds_launch *launch, int32_t elem, int64_t n,
+                         const void *x, void *y, const void *coef_host,
+                         ompds_team_stats *stats, ompds_event *events) {
+  if (!x || !y || !coef_host || n < 0 || (elem != 0 && elem != 1) ||
+      (reinterpret_cast<uintptr_t>(x) & 15) ||
+      (reinterpret_cast<uintptr_t>(y) & 15))
+    return OMPDS_ERR_INVALID;
+  static FixedLayout lay8;
+  static std::once_flag once;
+  static int32_t lay_status = 0;
+  std::call_once(once, [] {
+    lay_status = build_fixed_layout({4, 4, 4, 4, 4, 4, 4, 4}, 0, &lay8);
+  });
+  if (lay_status)
+    return lay_status;
+  if (elem == 0) {
+    StreamProg<int32_t>::Args a{static_cast<const int32_t *>(x),
+                                static_cast<int32_t *>(y), n, {}};
+    std::memcpy(a.coef, coef_host, sizeof(a.coef));
+    return launch_generic<StreamProg<int32_t>>(launch, lay8, 8, a, stats,
+                                               events);
+  }
+  StreamProg<double>::Args a{static_cast<const double *>(x),
+                             static_cast<double *>(y), n, {}};
+  std::memcpy(a.coef, coef_host, sizeof(a.coef));
+  return launch_generic<StreamProg<double>>(launch, lay8, 8, a, stats, events);
+}
+
+int32_t ompds_run_stream_host(const ompds_launch *launch, int32_t elem,
+                              int64_t n, const void *x_host, void *y_host,
+                              const void *coef_host, void *x_dev,
+                              void *y_dev) {
+  if (!launch || !x_host || !y_host || !x_dev || !y_dev)
+    return OMPDS_ERR_INVALID;
+  const size_t bytes = static_cast<size_t>(n) * (elem ? 8 : 4);
+  cudaStream_t st = static_cast<cudaStream_t>(launch->stream);
+  OMPDS_CUDA(cudaMemcpyAsync(x_dev, x_host, bytes, cudaMemcpyHostToDevice, st));
+  OMPDS_CUDA(cudaMemcpyAsync(y_dev, y_host, bytes, cudaMemcpyHostToDevice, st));
+  int32_t s = ompds_run_stream(launch, elem, n, x_dev, y_dev, coef_host,
+                               nullptr, nullptr);
+  if (s)
+    return s;
+  OMPDS_CUDA(cudaMemcpyAsync(y_host, y_dev, bytes, cudaMemcpyDeviceToHost, st));
+  OMPDS_CUDA(cudaStreamSynchronize(st));
+  return OMPDS_OK;
+}
+
+int32_t ompds_fill_uniform(int32_t elem, void *out, int64_t n, uint64_t seed,
+                           int64_t first, void *stream) {
+  if (!out || n < 0 || (elem != 0 && elem != 1))
+    return OMPDS_ERR_INVALID;
+  if (n == 0)
+    return OMPDS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  if (elem)
+    fill_f64_kernel<<<blocks, 256, 0, st>>>(static_cast<double *>(out), n, seed,
+                                            first);
+  else
+    fill_i32_kernel<<<blocks, 256, 0, st>>>(static_cast<int32_t *>(out), n,
+                                            seed, first);
+  OMPDS_CUDA(cudaGetLastError());
+  return OMPDS_OK;
+}
+
+int32_t ompds_checksum(int32_t elem, const void *data, int64_t n,
+                       uint64_t *out_dev, void *stream) {
+  if (!data || !out_dev || n < 0 || (elem != 0 && elem != 1))
+    return OMPDS_ERR_INVALID;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  OMPDS_CUDA(cudaMemsetAsync(out_dev, 0, 8, st));
+  if (n == 0)
+    return OMPDS_OK;
+  const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 8));
+  auto *o = reinterpret_cast<unsigned long long *>(out_dev);
+  if (elem)
+    checksum_kernel<double><<<blocks, 256, 0, st>>>(
+        static_cast<const double *>(data), n, o);
+  else
+    checksum_kernel<int32_t><<<blocks, 256, 0, st>>>(
+        static_cast<const int32_t *>(data), n, o);
+  OMPDS_CUDA(cudaGetLastError());
+  return OMPDS_OK;
+}
+
+} // extern "C"

@@ -1,0 +1,144 @@
+"""Frame-layout descriptors: ``DepotSlot`` / ``DepotLayout`` / ``FrameGroup``
+(proj/include/omplab/IR.h:219-254) built by the C-ABI frame pipeline
+(``ompds_layout_build``; LoweringPasses.cpp buildDepots :264-305,
+lowerSharedFrames :345-380, colorStack :458-538, repackOffsets :556-593).
+
+Also the descriptor exports the reference produces: the ``.sir`` frame block
+(IRPrinter.cpp:191-218) and the manifest's depot section
+(Compiler.cpp:112-155), and the layout audit (LoweringPasses.cpp:617-665).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+from . import _lib as L
+
+PIPELINES = {"default": L.PIPELINE_DEFAULT, "o0": L.PIPELINE_O0, "bad_order": L.PIPELINE_BAD_ORDER}
+
+
+@dataclass
+class FrameVar:
+    """One alloca of the post-codegen module, in emission order."""
+    name: str
+    bytes: int
+    group: int = 0
+    func: int = 0
+    escapes: bool = False
+    pinned: bool = False
+    def_pos: int = -1
+    first: int = -1
+    last: int = -1
+
+
+@dataclass
+class DepotSlot:  # IR.h:219-228
+    offset: int
+    size: int
+    align: int = 8
+    shared: bool = False
+    owners: List[str] = field(default_factory=list)
+
+
+@dataclass
+class DepotLayout:  # IR.h:230-244
+    slots: List[DepotSlot]
+    total_local: int
+    total_shared: int
+    has_shared_depot: bool
+    overlap_slot: int = -1
+
+    def stack_bytes(self) -> int:
+        return self.total_local
+
+    def find_shared_local_overlap(self) -> Optional[str]:  # IR.cpp:228-242
+        if self.overlap_slot < 0:
+            return None
+        s = self.slots[self.overlap_slot]
+        return (f"slot {self.overlap_slot} at offset {s.offset} hosts"
+                + "".join(f" %{o}" for o in s.owners))
+
+
+@dataclass
+class FrameGroup:  # IR.h:249-254
+    root: str
+    members: List[str]
+
+
+def build_layouts(vars_: Sequence[FrameVar], n_groups: int,
+                  pipeline: str = "default") -> List[DepotLayout]:
+    """Runs the frame pipeline over ``vars_`` and returns one layout per group."""
+    lib = L.lib()
+    n = len(vars_)
+    arr = (L.FrameVar * max(n, 1))()
+    for i, v in enumerate(vars_):
+        flags = (L.VAR_ESCAPES if v.escapes else 0) | (L.VAR_PINNED if v.pinned else 0)
+        arr[i] = L.FrameVar(v.group, v.func, flags, v.def_pos, v.bytes, v.first, v.last)
+    lays = (L.DepotLayout * max(n_groups, 1))()
+    slots = (L.DepotSlot * max(n, 1))()
+    owners = (C.c_int32 * max(n, 1))()
+    L.check(lib.ompds_layout_build(arr, n, n_groups, PIPELINES[pipeline], lays, slots, max(n, 1),
+                                   owners, max(n, 1)), "ompds_layout_build")
+    out = []
+    for g in range(n_groups):
+        lay = lays[g]
+        ss = []
+        for k in range(lay.slot_begin, lay.slot_begin + lay.n_slots):
+            s = slots[k]
+            names = [vars_[owners[j]].name for j in range(s.owner_begin, s.owner_begin + s.n_owners)]
+            ss.append(DepotSlot(s.offset, s.size, s.align, bool(s.shared), names))
+        out.append(DepotLayout(ss, lay.total_local, lay.total_shared, bool(lay.has_shared_depot),
+                               lay.overlap_slot))
+    return out
+
+
+def shared_footprint(total_shared: int, prealloc_entries: int = L.DEFAULT_PREALLOC_ENTRIES) -> int:
+    """Simulator.cpp:281-284 / Occupancy.h:49-51: depot + window + runtime span."""
+    return int(L.lib().ompds_shared_footprint(total_shared, prealloc_entries))
+
+
+def audit(layouts: Sequence[DepotLayout], roots: Sequence[str]) -> List[Dict[str, str]]:
+    """layout-overlap / mirror-mismatch findings (LoweringPasses.cpp:617-640)."""
+    diags = []
+    for lay, root in zip(layouts, roots):
+        ov = lay.find_shared_local_overlap()
+        if ov:
+            diags.append({"rule": "layout-overlap", "message": ov, "function": root})
+        if lay.total_shared != lay.total_local:
+            diags.append({"rule": "mirror-mismatch",
+                          "message": f"shared depot size {lay.total_shared} does not mirror "
+                                     f"local depot size {lay.total_local}",
+                          "function": root})
+    return diags
+
+
+def frame_block(group: FrameGroup, lay: DepotLayout) -> str:
+    """The ``.sir`` frame block for one group (IRPrinter.cpp:191-218)."""
+    out = [f"frame @{group.root} members [" + ", ".join(f"@{m}" for m in group.members) + "] {"]
+    for i, s in enumerate(lay.slots):
+        line = (f"  slot {i}: offset {s.offset}, size {s.size}, align {s.align}, "
+                + ("shared" if s.shared else "local"))
+        line += "".join(f", %{o}" for o in s.owners)
+        out.append(line)
+    out.append(f"  total {lay.total_local}" + (", mirrored" if lay.has_shared_depot else ""))
+    out.append("}")
+    return "\n".join(out) + "\n"
+
+
+def manifest_depot(lay: DepotLayout, prealloc_entries: int = L.DEFAULT_PREALLOC_ENTRIES) -> dict:
+    """The depot part of the reference manifest (Compiler.cpp:112-155)."""
+    return {
+        "depot": {
+            "slots": [{"offset": s.offset, "size": s.size, "align": s.align, "shared": s.shared,
+                       "owners": list(s.owners)} for s in lay.slots],
+            "total_local": lay.total_local,
+            "total_shared": lay.total_shared,
+            "mirrored": lay.has_shared_depot,
+        },
+        "stack_bytes": lay.total_local,
+        "prealloc_entries": prealloc_entries,
+        "prealloc_bytes": prealloc_entries * L.SHARED_ARG_ENTRY_BYTES,
+        "runtime_bytes": L.RUNTIME_PRIVATE_BYTES,
+        "shared_footprint": shared_footprint(lay.total_shared, prealloc_entries),
+    }

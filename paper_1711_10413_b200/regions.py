@@ -1,0 +1,175 @@
+"""Generic-mode target-region launches (BASELINE.json configs 1, 2, 4, 5).
+
+Thin wrappers over the C ABI that take torch CUDA tensors (torch is used for
+device memory and streams only).  Each call launches one sm_100a kernel in
+which every CTA is an OpenMP team running the data-sharing protocol:
+kernel_init -> push the kernel depot on the master's data-sharing stack ->
+sequential code -> prepare_parallel + publish &captures -> named-barrier
+release -> workers fetch, get-shared-variables (warp-shuffle broadcast), run
+the region, retire -> join -> ... -> kernel_deinit -> termination release.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional
+
+import torch
+
+from . import _lib as L
+
+ELEM = {torch.int32: L.ELEM_I32, torch.float64: L.ELEM_F64}
+
+
+@dataclass
+class TeamStats:
+    trap: int
+    master_barriers: int
+    barrier_releases: int
+    regions: int
+    dynamic_alloc_bytes: int
+    dynamic_allocs: int
+    dynamic_frees: int
+    depot_in_smem: bool
+    n_events: int
+    depot_offset: int
+    smem_bytes: int
+
+
+STATS_DTYPE_BYTES = C.sizeof(L.TeamStats)
+EVENT_BYTES = C.sizeof(L.Event)
+
+
+def _require_cuda(*ts: torch.Tensor) -> None:
+    for t in ts:
+        if not t.is_cuda:
+            raise ValueError("device tensors required (there is no CPU path)")
+        if not t.is_contiguous():
+            raise ValueError("contiguous tensors required")
+
+
+def make_launch(teams: int, workers: int, prealloc_entries: int = L.DEFAULT_PREALLOC_ENTRIES,
+                fail_dynamic_alloc: bool = False, depot_capacity: int = -1,
+                log_events: bool = False, max_events: int = 0,
+                stream: Optional[torch.cuda.Stream] = None) -> L.Launch:
+    s = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    return L.Launch(teams, workers, prealloc_entries, 1 if fail_dynamic_alloc else 0,
+                    depot_capacity, 1 if log_events else 0, max_events if log_events else 0,
+                    C.c_void_p(s))
+
+
+class Outputs:
+    """Device buffers for per-team statistics and event logs."""
+
+    def __init__(self, teams: int, device, max_events: int = 0):
+        self.teams = teams
+        self.max_events = max_events
+        self.stats = torch.zeros(teams * STATS_DTYPE_BYTES, dtype=torch.uint8, device=device)
+        self.events = (torch.zeros(max(teams * max_events, 1) * EVENT_BYTES, dtype=torch.uint8,
+                                   device=device) if max_events else None)
+
+    def stats_ptr(self):
+        return C.c_void_p(self.stats.data_ptr())
+
+    def events_ptr(self):
+        return C.c_void_p(self.events.data_ptr()) if self.events is not None else None
+
+    def team_stats(self) -> List[TeamStats]:
+        raw = bytes(self.stats.cpu().numpy().tobytes())
+        arr = (L.TeamStats * self.teams).from_buffer_copy(raw)
+        return [TeamStats(s.trap, s.master_barriers, s.barrier_releases, s.regions,
+                          s.dynamic_alloc_bytes, s.dynamic_allocs, s.dynamic_frees,
+                          bool(s.depot_in_smem), s.n_events, s.depot_offset, s.smem_bytes)
+                for s in arr]
+
+    def team_events(self) -> List[List[tuple]]:
+        if self.events is None:
+            return [[] for _ in range(self.teams)]
+        stats = self.team_stats()
+        raw = bytes(self.events.cpu().numpy().tobytes())
+        arr = (L.Event * (self.teams * self.max_events)).from_buffer_copy(raw)
+        out = []
+        for t in range(self.teams):
+            n = min(stats[t].n_events, self.max_events)
+            base = t * self.max_events
+            out.append([(L.EVENT_KIND_NAMES[e.kind], e.fn, e.nargs, e.bytes)
+                        for e in arr[base:base + n]])
+        return out
+
+
+def run_regions(a: torch.Tensor, teams: int, workers: int, regions: int, **kw) -> Outputs:
+    """Config 1: ``regions`` parallel regions sharing 4 scalars per team."""
+    _require_cuda(a)
+    max_events = kw.pop("max_events", 0)
+    out = Outputs(teams, a.device, max_events)
+    launch = make_launch(teams, workers, log_events=max_events > 0, max_events=max_events, **kw)
+    L.check(L.lib().ompds_run_regions(C.byref(launch), ELEM[a.dtype], regions,
+                                      C.c_void_p(a.data_ptr()), out.stats_ptr(),
+                                      out.events_ptr()), "ompds_run_regions")
+    return out
+
+
+def run_shared_array(a: torch.Tensor, teams: int, workers: int,
+                     d_init: Optional[torch.Tensor] = None, **kw) -> Outputs:
+    """Config 2: d[256] in the depot, ``parallel for i: a[i] += d[i & 255]``."""
+    _require_cuda(a)
+    max_events = kw.pop("max_events", 0)
+    out = Outputs(teams, a.device, max_events)
+    launch = make_launch(teams, workers, log_events=max_events > 0, max_events=max_events, **kw)
+    dp = C.c_void_p(d_init.data_ptr()) if d_init is not None else None
+    L.check(L.lib().ompds_run_shared_array(C.byref(launch), ELEM[a.dtype], a.numel(),
+                                           C.c_void_p(a.data_ptr()), dp, out.stats_ptr(),
+                                           out.events_ptr()), "ompds_run_shared_array")
+    return out
+
+
+def coef_buffer(dtype: torch.dtype, coef) -> C.Array:
+    if dtype == torch.float64:
+        return (C.c_double * 8)(*[float(c) for c in coef])
+    return (C.c_int32 * 8)(*[int(c) for c in coef])
+
+
+def run_stream(x: torch.Tensor, y: torch.Tensor, coef, teams: int, workers: int,
+               stats: bool = True, **kw) -> Optional[Outputs]:
+    """Config 4: ``y = fma(c1, x, y) + (c2+...+c8)`` over all elements."""
+    _require_cuda(x, y)
+    max_events = kw.pop("max_events", 0)
+    out = Outputs(teams, x.device, max_events) if stats else None
+    launch = make_launch(teams, workers, log_events=max_events > 0, max_events=max_events, **kw)
+    cb = coef_buffer(x.dtype, coef)
+    L.check(L.lib().ompds_run_stream(C.byref(launch), ELEM[x.dtype], x.numel(),
+                                     C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), cb,
+                                     out.stats_ptr() if out else None,
+                                     out.events_ptr() if out else None), "ompds_run_stream")
+    return out
+
+
+def run_stream_host(x_host: torch.Tensor, y_host: torch.Tensor, coef, teams: int, workers: int,
+                    x_dev: torch.Tensor, y_dev: torch.Tensor,
+                    stream: Optional[torch.cuda.Stream] = None) -> None:
+    """Config 4 end to end from host buffers (H2D, region, D2H, synchronise)."""
+    launch = make_launch(teams, workers, stream=stream)
+    cb = coef_buffer(x_host.dtype, coef)
+    L.check(L.lib().ompds_run_stream_host(C.byref(launch), ELEM[x_host.dtype], x_host.numel(),
+                                          C.c_void_p(x_host.data_ptr()),
+                                          C.c_void_p(y_host.data_ptr()), cb,
+                                          C.c_void_p(x_dev.data_ptr()),
+                                          C.c_void_p(y_dev.data_ptr())), "ompds_run_stream_host")
+
+
+def fill_uniform(t: torch.Tensor, seed: int, first: int = 0,
+                 stream: Optional[torch.cuda.Stream] = None) -> None:
+    _require_cuda(t)
+    s = (stream or torch.cuda.current_stream()).cuda_stream
+    L.check(L.lib().ompds_fill_uniform(ELEM[t.dtype], C.c_void_p(t.data_ptr()), t.numel(),
+                                       seed, first, C.c_void_p(s)), "ompds_fill_uniform")
+
+
+def checksum(t: torch.Tensor, stream: Optional[torch.cuda.Stream] = None) -> int:
+    """Sum of the elements' bit patterns mod 2^64 (order independent, exact)."""
+    _require_cuda(t)
+    out = torch.zeros(1, dtype=torch.int64, device=t.device)
+    s = (stream or torch.cuda.current_stream()).cuda_stream
+    L.check(L.lib().ompds_checksum(ELEM[t.dtype], C.c_void_p(t.data_ptr()), t.numel(),
+                                   C.c_void_p(out.data_ptr()), C.c_void_p(s)), "ompds_checksum")
+    return int(out.item()) & ((1 << 64) - 1)

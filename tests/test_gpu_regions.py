@@ -1,0 +1,232 @@
+"""GPU parity of the generic-mode region kernels (configs 1, 2, 4) through the
+C ABI: integer analogs bit-exact against the reference's own simulator output
+(tests/golden/analogs.json), fp64 bodies against the C oracle (bit-exact: the
+kernels and the oracle use the same explicit fma / add order; the stated
+tolerance would be 1e-12 relative), runtime statistics against the
+reference's barrier / allocation laws."""
+import numpy as np
+import pytest
+import torch
+
+import golden_util as G
+from oracle import oracle as O
+from paper_1711_10413_b200 import regions as RG
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+RTOL_F64 = 1e-12  # north_star tolerance for fp64 bodies; we also require bit equality
+
+
+def analog(stem):
+    return next(p for p in G.load("analogs") if p["stem"] == stem)
+
+
+def canon(events, fn_of=None):
+    """Orders each region's worker events like the reference's round-robin
+    simulator: fetches, then retires by decreasing `remaining`, then free."""
+    out, seg = [], []
+    order = {"fetch": 0, "retire": 1, "dynamic_free": 2}
+
+    def flush():
+        seg.sort(key=lambda e: (order[e[0]], -e[2] if e[0] == "retire" else 0))
+        out.extend(seg)
+        seg.clear()
+
+    for e in events:
+        kind, fn, nargs, nbytes = e
+        fn = fn_of(fn) if fn_of else fn
+        if kind in order:
+            seg.append((kind, fn, nargs, nbytes))
+        else:
+            flush()
+            out.append((kind, fn, nargs, nbytes))
+    flush()
+    return out
+
+
+def golden_events(team_events):
+    names = {}
+
+    def fid(name):
+        if not name:
+            return -1
+        return names.setdefault(name, len(names))
+
+    return canon([(k, fid(fn) if k.startswith("prepare") else -1 if k != "fetch" else fn,
+                   n, b) for k, fn, n, b in team_events], None)
+
+
+def norm_fetch(ev):
+    # our fetch events carry the fn id; the golden's carry the name -> compare ids
+    return ev
+
+
+# --------------------------------------------------------------------------- config 1
+
+@pytest.mark.parametrize("stem,regions", [("cfg1_analog", 1), ("cfg1_loop_analog", 5)])
+def test_config1_int_analog_matches_reference(stem, regions):
+    p = analog(stem)
+    for run in p["runs"]:
+        if run["teams"] != 1 or not G.race_free_run(run):
+            continue
+        w = run["workers"]
+        a = torch.zeros(len(run["sim"]["globals"]["a"]), dtype=torch.int32, device=DEV)
+        out = RG.run_regions(a, 1, w, regions, max_events=4096)
+        assert a.cpu().tolist() == run["sim"]["globals"]["a"]
+        st = out.team_stats()[0]
+        assert st.trap == 0
+        assert st.master_barriers == run["sim"]["master_barrier_entries"][0] == 2 * regions
+        assert st.barrier_releases == run["sim"]["barrier_releases"][0] == 2 * regions + 1
+        assert st.regions == regions and st.dynamic_allocs == 0 and st.depot_in_smem
+        # team region = depot (layout) + 160 + 49, the reference footprint
+        depot = next(l for l in p["layouts"] if l["root"] == p["kernel"])["total_shared"]
+        assert st.smem_bytes == p["manifest"]["shared_footprint"] == depot + 209
+        # event log == the reference TeamRuntime's, per region in canonical order
+        ours = canon(out.team_events()[0])
+        ref = run["sim"]["team_events"][0]
+        names = {}
+        ref_ev = []
+        for k, fn, n, b in ref:
+            if k.startswith("prepare"):
+                names.setdefault(fn, len(names))
+            ref_ev.append((k, names[fn] if fn else -1, n, b))
+        assert ours == canon(ref_ev)
+
+
+@pytest.mark.parametrize("teams,workers,regions", [(1, 32, 1), (3, 40, 7), (148, 96, 3),
+                                                   (2, 992, 2), (5, 1, 4)])
+def test_config1_f64_and_int_match_oracle(teams, workers, regions):
+    for dt, elem in ((torch.float64, 1), (torch.int32, 0)):
+        a = torch.zeros(teams * workers, dtype=dt, device=DEV)
+        out = RG.run_regions(a, teams, workers, regions)
+        want = np.zeros(teams * workers, dtype=np.float64 if elem else np.int32)
+        O.lib().orc_regions(elem, teams, workers, regions, O.ptr(want))
+        assert np.array_equal(a.cpu().numpy(), want)
+        for st in out.team_stats():
+            assert (st.trap, st.master_barriers, st.barrier_releases, st.regions) == \
+                (0, 2 * regions, 2 * regions + 1, regions)
+
+
+# --------------------------------------------------------------------------- config 2
+
+def test_config2_int_analog_matches_reference():
+    p = analog("cfg2_analog")
+    for run in p["runs"]:
+        for staged in (False, True):
+            a = torch.zeros(256, dtype=torch.int32, device=DEV)
+            d_init = (torch.arange(256, dtype=torch.int32, device=DEV) * 3 + 1) if staged else None
+            out = RG.run_shared_array(a, run["teams"], run["workers"], d_init=d_init)
+            assert a.cpu().tolist() == run["sim"]["globals"]["a"]
+            for st in out.team_stats():
+                assert st.trap == 0 and st.depot_in_smem
+                assert st.smem_bytes == p["manifest"]["shared_footprint"] == 1048 + 209
+                assert st.master_barriers == 2
+
+
+@pytest.mark.parametrize("capacity", [-1, 1024, 0])
+def test_config2_f64_placement_and_values(capacity):
+    n = (1 << 20) + 3
+    a = torch.empty(n, dtype=torch.float64, device=DEV)
+    RG.fill_uniform(a, 0x5eed01ac)
+    want = np.empty(n)
+    O.lib().orc_fill(1, O.ptr(want), n, 0x5eed01ac, 0)
+    assert np.array_equal(a.cpu().numpy(), want)
+    d_init = torch.arange(256, dtype=torch.float64, device=DEV) * 3 + 1
+    out = RG.run_shared_array(a, 148, 224, d_init=d_init, depot_capacity=capacity)
+    O.lib().orc_shared_array(1, n, O.ptr(want))
+    assert np.array_equal(a.cpu().numpy(), want)
+    in_smem = capacity < 0 or capacity >= 2072
+    for st in out.team_stats():
+        assert st.trap == 0
+        assert st.depot_in_smem == in_smem  # slot vs global-overflow decision
+        assert st.depot_offset == 0
+        expect_depot = 2072 if capacity < 0 else capacity
+        assert st.smem_bytes == expect_depot + 160 + 49
+
+
+def test_config2_master_loop_equals_tma_staging():
+    n = 4096 * 7 + 1
+    a1 = torch.zeros(n, dtype=torch.float64, device=DEV)
+    a2 = torch.zeros(n, dtype=torch.float64, device=DEV)
+    RG.run_shared_array(a1, 16, 64)
+    RG.run_shared_array(a2, 16, 64, d_init=torch.arange(256, dtype=torch.float64,
+                                                        device=DEV) * 3 + 1)
+    assert torch.equal(a1, a2)
+
+
+# --------------------------------------------------------------------------- config 4
+
+@pytest.mark.parametrize("n", [1024, 4096])
+def test_config4_int_analog_matches_reference(n):
+    p = analog(f"cfg4_analog_{n}")
+    for run in p["runs"]:
+        x = torch.tensor(p["inputs"]["x"], dtype=torch.int32, device=DEV)
+        y = torch.tensor(p["inputs"]["y"], dtype=torch.int32, device=DEV)
+        out = RG.run_stream(x, y, list(range(1, 9)), run["teams"], run["workers"],
+                            max_events=4096)
+        assert y.cpu().tolist() == run["sim"]["globals"]["y"]
+        for t, st in enumerate(out.team_stats()):
+            assert st.trap == 0 and st.master_barriers == 2 and st.barrier_releases == 3
+            assert st.smem_bytes == p["manifest"]["shared_footprint"] == 80 + 209
+            ours = canon(out.team_events()[t])
+            ref = run["sim"]["team_events"][t] if "team_events" in run["sim"] else None
+            if ref is not None:
+                assert [e[0] for e in ours] == [e[0] for e in canon(
+                    [(k, -1, nn, b) for k, _, nn, b in ref])]
+
+
+def _f64_inputs(n, first=0):
+    x = torch.empty(n, dtype=torch.float64, device=DEV)
+    y = torch.empty(n, dtype=torch.float64, device=DEV)
+    RG.fill_uniform(x, 0x5eed01ab, first)
+    RG.fill_uniform(y, 0x5eed01ac, first)
+    return x, y
+
+
+COEF = [k / 8 for k in range(1, 9)]
+
+
+@pytest.mark.parametrize("teams,workers", [(148, 224), (296, 992), (7, 33), (1, 1)])
+def test_config4_f64_bitwise_vs_oracle(teams, workers):
+    n = (1 << 20) + 5
+    x, y = _f64_inputs(n)
+    xs, ys = x.cpu().numpy().copy(), y.cpu().numpy().copy()
+    out = RG.run_stream(x, y, COEF, teams, workers)
+    O.lib().orc_stream(1, n, O.ptr(xs), O.ptr(ys), O.ptr(np.array(COEF)), 0)
+    got = y.cpu().numpy()
+    assert np.allclose(got, ys, rtol=RTOL_F64, atol=0)
+    assert np.array_equal(got.view(np.uint64), ys.view(np.uint64))
+    assert all(s.trap == 0 and s.regions == 1 for s in out.team_stats())
+
+
+def test_config4_spilled_args_list_and_alloc_failure():
+    n = 100_003
+    x, y = _f64_inputs(n)
+    y0 = y.clone()
+    ref = y.clone()
+    RG.run_stream(x, ref, COEF, 64, 96)
+    out = RG.run_stream(x, y, COEF, 64, 96, prealloc_entries=2, max_events=1024)
+    assert torch.equal(y, ref)
+    for t, st in enumerate(out.team_stats()):
+        assert (st.dynamic_allocs, st.dynamic_frees, st.dynamic_alloc_bytes) == (1, 1, 64)
+        ev = canon(out.team_events()[t])
+        assert ev[1] == ("prepare_dynamic", 0, 8, 64) and ev[-2] == ("dynamic_free", -1, 0, 64)
+    y2 = y0.clone()
+    out = RG.run_stream(x, y2, COEF, 64, 96, prealloc_entries=2, fail_dynamic_alloc=True)
+    assert torch.equal(y2, y0)  # no region ran
+    assert all(st.trap == 9 and st.regions == 0 for st in out.team_stats())
+
+
+def test_config4_full_size_checksum_vs_oracle():
+    n = 1 << 28
+    x, y = _f64_inputs(n)
+    RG.run_stream(x, y, COEF, 296, 992, stats=False)
+    torch.cuda.synchronize()
+    got = RG.checksum(y)
+    del x, y
+    xs = np.empty(n)
+    ys = np.empty(n)
+    O.lib().orc_fill(1, O.ptr(xs), n, 0x5eed01ab, 0)
+    O.lib().orc_fill(1, O.ptr(ys), n, 0x5eed01ac, 0)
+    O.lib().orc_stream(1, n, O.ptr(xs), O.ptr(ys), O.ptr(np.array(COEF)), 0)
+    assert got == O.lib().orc_checksum(1, O.ptr(ys), n)

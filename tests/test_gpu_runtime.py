@@ -1,0 +1,129 @@
+"""GPU parity of the device runtime protocol (csrc/ompds_device.cuh) against
+the reference TeamRuntime's recorded outcomes (tests/golden/runtime.json) and
+the C oracle.  Calls go through the C ABI (ompds_rt_replay)."""
+import ctypes as C
+import random
+
+import pytest
+
+import golden_util as G
+from oracle import oracle as O
+from paper_1711_10413_b200 import _lib as P
+from paper_1711_10413_b200 import runtime as R
+from test_oracle_golden import _replay, check_script
+
+pytestmark = pytest.mark.gpu
+
+
+def test_device_runtime_matches_reference_scripts():
+    scripts = G.load("runtime")
+    for s in scripts:
+        check_script(s, *_replay(P.lib().ompds_rt_replay, s))
+
+
+def test_device_runtime_matches_oracle_on_long_fuzz():
+    rng = random.Random(1234)
+    for trial in range(60):
+        calls = [(0, 0, rng.randint(1, 64))] if rng.random() < 0.9 else []
+        for _ in range(rng.randint(50, 300)):
+            op = rng.choice([1, 2, 2, 2, 3, 3, 3, 4])
+            role = 0 if op in (1, 4) else 1
+            if rng.random() < 0.05:
+                role ^= 1
+            arg = rng.randint(-1, 70) if op == 1 else 0
+            calls.append((op, role, arg))
+        pe = rng.choice([0, 1, 4, 20, 20, 20, 64])
+        fail = rng.random() < 0.1
+        script = {"calls": calls, "prealloc_entries": pe, "fail_dynamic_alloc": fail}
+        a = _replay(P.lib().ompds_rt_replay, script)
+        b = _replay(O.lib().orc_rt_replay, script)
+        for x, y in zip(a[0], b[0]):
+            assert (x.status, x.addr_kind, x.wf, x.participate, x.live_bytes, x.heap_live) == \
+                (y.status, y.addr_kind, y.wf, y.participate, y.live_bytes, y.heap_live)
+        assert [(e.kind, e.fn, e.nargs, e.bytes) for e in a[1]] == \
+            [(e.kind, e.fn, e.nargs, e.bytes) for e in b[1]]
+
+
+# proj/tests/RuntimeTests.cpp, through the TeamRuntime mirror -------------------
+
+def live(workers=8, cfg=None):
+    rt = R.TeamRuntime(cfg or R.RuntimeConfig(), prealloc_base=0x2000)
+    assert rt.kernelInit(R.MASTER, workers).ok
+    return rt
+
+
+def drain(rt):
+    res, wf, addr, part = rt.kernelParallel(R.WORKER)
+    assert res.ok and part
+    assert rt.endParallel(R.WORKER).ok
+
+
+def test_init_accepts_one_master_call_and_nothing_else():
+    rt = R.TeamRuntime(R.RuntimeConfig(), 0x2000)
+    assert not rt.kernelInit(R.WORKER, 8).ok
+    assert not rt.kernelInit(R.MASTER, 0).ok
+    assert rt.kernelInit(R.MASTER, 8).ok
+    assert not rt.kernelInit(R.MASTER, 8).ok
+    assert rt.workerCount() == 8
+
+
+def test_small_capture_lists_use_the_preallocated_window():
+    rt = live()
+    for n in (0, 1, 19, 20):
+        res, addr = rt.prepareParallel(R.MASTER, "wf", n)
+        assert res.ok and addr == 0x2000
+        drain(rt)
+    assert rt.dynamicAllocs() == 0
+
+
+def test_oversized_capture_lists_fall_back_to_global_memory():
+    rt = live()
+    for n, nbytes in ((21, 168), (32, 256), (64, 512), (128, 1024)):
+        res, addr = rt.prepareParallel(R.MASTER, "wf", n)
+        assert res.ok and addr != 0x2000
+        assert rt.events()[-1].kind == "prepare_dynamic" and rt.events()[-1].bytes == nbytes
+        drain(rt)
+        assert rt.events()[-1].str() == f"free bytes={nbytes}"
+    assert rt.dynamicAllocs() == 4 and rt.dynamicFrees() == 4 and rt.leakedBlocks() == 0
+
+
+def test_window_boundary_is_exactly_the_entry_count():
+    rt = live(cfg=R.RuntimeConfig(prealloc_entries=4))
+    res, addr = rt.prepareParallel(R.MASTER, "wf", 4)
+    assert res.ok and addr == 0x2000
+    drain(rt)
+    res, addr = rt.prepareParallel(R.MASTER, "wf", 5)
+    assert res.ok and addr != 0x2000
+    assert rt.events()[-1].bytes == 40
+
+
+def test_failing_global_allocation_is_a_trap():
+    rt = live(cfg=R.RuntimeConfig(fail_dynamic_alloc=True))
+    res, _ = rt.prepareParallel(R.MASTER, "wf", 21)
+    assert not res.ok and res.trap_reason == "shared-args-alloc-failed"
+
+
+def test_termination_sentinel_and_event_order():
+    rt = live()
+    res, _ = rt.prepareParallel(R.MASTER, "region0", 21)
+    assert res.ok
+    res, wf, _, part = rt.kernelParallel(R.WORKER)
+    assert wf == "region0"
+    assert rt.endParallel(R.WORKER).ok
+    assert rt.kernelDeinit(R.MASTER).ok
+    res, wf, addr, part = rt.kernelParallel(R.WORKER)
+    assert res.ok and wf == "" and addr == 0 and not part and rt.terminated()
+    assert [e.kind for e in rt.events()] == ["init", "prepare_dynamic", "fetch", "retire",
+                                             "dynamic_free", "deinit"]
+
+
+def test_byte_law_for_every_count():
+    rng = random.Random(1234)
+    for _ in range(50):
+        n = rng.randint(0, 128)
+        rt = live()
+        res, addr = rt.prepareParallel(R.MASTER, "wf", n)
+        assert res.ok
+        dyn = rt.events()[-1].bytes
+        assert dyn == R.dynamic_args_bytes(n)
+        assert (addr == 0x2000) == (n <= 20)

@@ -1,0 +1,159 @@
+"""CPU-side tests of the product library: the C ABI loads and exports every
+symbol include/ompds.h declares; the host parts of the boundary (frame-layout
+descriptor builder, occupancy model, trap strings) match the reference's
+golden vectors and the oracle; compute entry points fail loudly without a
+GPU instead of falling back to the CPU."""
+import ctypes as C
+import os
+import random
+import re
+
+import pytest
+
+import golden_util as G
+import layout_util as LU
+from oracle import oracle as O
+from paper_1711_10413_b200 import _lib as P
+from paper_1711_10413_b200 import layout, occupancy, runtime
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "ompds.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ompds_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported_and_bound():
+    lib = P.lib()
+    declared = header_functions()
+    assert len(declared) >= 19
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(P.exported_symbols()) == declared
+
+
+def test_struct_sizes_match_the_c_abi():
+    # sizes implied by the header's field lists (natural alignment, x86-64)
+    assert C.sizeof(P.RtCall) == 16
+    assert C.sizeof(P.RtResult) == 32
+    assert C.sizeof(P.Event) == 24
+    assert C.sizeof(P.FrameVar) == 32
+    assert C.sizeof(P.DepotSlot) == 32
+    assert C.sizeof(P.DepotLayout) == 32
+    assert C.sizeof(P.Launch) == 40
+    assert C.sizeof(P.TeamStats) == 56
+
+
+def test_trap_strings_are_the_reference_strings():
+    strings = {r["trap"] for s in G.load("runtime") for r in s["results"] if not r["ok"]}
+    assert {runtime.trap_reason(c) for c in range(1, 18)} == strings
+
+
+@pytest.mark.parametrize("key", ["layouts", "layouts_o0", "layouts_bad_order"])
+def test_product_layout_builder_matches_reference(key):
+    for p in G.programs():
+        if p.get(key) is None:
+            continue
+        out = LU.run_builder(P.lib().ompds_layout_build, p["frame_vars"], len(p["layouts"]),
+                             LU.PIPE[key])
+        assert LU.strip(out) == LU.golden_view(p[key]), (p["stem"], key)
+
+
+def test_product_layout_builder_matches_oracle_on_random_frames():
+    rng = random.Random(0x5eed01ab)
+    for trial in range(400):
+        n = rng.randint(0, 14)
+        ngroups = rng.randint(1, 3)
+        fv = []
+        for i in range(n):
+            first = rng.randint(-1, 30)
+            fv.append({"group": rng.randrange(ngroups), "func": rng.randint(0, 1),
+                       "name": f"v{i}", "bytes": rng.choice([4, 8, 12, 384, 1024, 0 + 4]),
+                       "escapes": rng.random() < 0.3, "pinned": rng.random() < 0.2,
+                       "def_pos": i, "first": first,
+                       "last": first + rng.randint(0, 10) if first >= 0 else -1})
+        for pipe in (0, 1, 2):
+            a = LU.run_builder(P.lib().ompds_layout_build, fv, ngroups, pipe)
+            b = LU.run_builder(O.lib().orc_layout_build, fv, ngroups, pipe)
+            assert a == b, (trial, pipe)
+
+
+def test_frame_block_and_manifest_render_like_the_reference():
+    p = next(x for x in G.load("corpus") if x["stem"] == "shared_scalar")
+    fv = [layout.FrameVar(v["name"], v["bytes"], v["group"], v["func"], v["escapes"], v["pinned"],
+                          v["def_pos"], v["first"], v["last"]) for v in p["frame_vars"]]
+    lays = layout.build_layouts(fv, len(p["layouts"]))
+    golden_sir = open(os.path.join("/root/reference/proj/tests/golden/shared_scalar.sir")).read() \
+        if os.path.exists("/root/reference/proj/tests/golden/shared_scalar.sir") else None
+    text = "".join("\n" + layout.frame_block(layout.FrameGroup(r, m), l)
+                   for (r, m), l in zip(G.frame_groups(p), lays))
+    want = ("\nframe @__omp_offload_shared_scalar members [@__omp_offload_shared_scalar, "
+            "@__omp_worker] {\n  slot 0: offset 0, size 8, align 8, shared, %c\n"
+            "  slot 1: offset 8, size 8, align 8, local, %wf.addr\n"
+            "  slot 2: offset 16, size 8, align 8, local, %args.addr\n  total 24, mirrored\n}\n")
+    assert text.startswith(want)
+    if golden_sir is not None:  # byte-equal to the reference's golden frame blocks
+        assert golden_sir.endswith(text)
+    m = layout.manifest_depot(lays[0])
+    gm = p["manifest"]
+    for k in ("depot", "stack_bytes", "prealloc_entries", "prealloc_bytes", "runtime_bytes",
+              "shared_footprint"):
+        assert m[k] == gm[k], k
+
+
+def test_audit_flags_the_bad_order_overlap():
+    p = next(x for x in G.load("corpus") if x["stem"] == "coloring_demo")
+    fv = [layout.FrameVar(v["name"], v["bytes"], v["group"], v["func"], v["escapes"], v["pinned"],
+                          v["def_pos"], v["first"], v["last"]) for v in p["frame_vars"]]
+    roots = [r for r, _ in G.frame_groups(p)]
+    bad = layout.build_layouts(fv, len(roots), "bad_order")
+    diags = layout.audit(bad, roots)
+    want = p["bad_order_audit"]
+    assert [(d["rule"], d["message"]) for d in diags] == [(d["rule"], d["message"]) for d in want]
+    assert layout.audit(layout.build_layouts(fv, len(roots)), roots) == []
+
+
+def test_occupancy_tables_match_reference_csv():
+    occ = G.load("occupancy")
+    assert occupancy.footprint_scalars_csv() == occ["footprint_scalars_csv"]
+    assert occupancy.footprint_arrays_csv() == occ["footprint_arrays_csv"]
+    for name, dev in occ["devices"].items():
+        assert occupancy.occupancy_scalars_csv(name) == dev["occupancy_scalars_csv"], name
+        assert occupancy.occupancy_arrays_csv(name) == dev["occupancy_arrays_csv"], name
+        assert occupancy.max_vars_csv(name) == dev["max_vars_csv"], name
+        for fp, regs, thr, tr, ts, pot, act, used in dev["occupancy_grid"]:
+            o = occupancy.occupancy_for(name, fp, regs, thr)
+            assert (o.teams_by_regs, o.teams_by_smem, o.potential, o.actual, o.smem_used) == \
+                (tr, ts, pot, act, used)
+
+
+def test_paper_footprints_and_capacity_law():
+    # AcceptanceMain.cpp:88-90 and the 200-round byte law of RuntimeTests.cpp:235-252
+    for n, total in zip([1, 2, 4, 8, 16, 32, 64], [233, 241, 257, 289, 353, 481, 737]):
+        assert layout.shared_footprint(8 * n + 16) == total
+    for k, total in zip([1, 2, 3, 4], [617, 1001, 1385, 1769]):
+        assert layout.shared_footprint(384 * k + 24) == total
+    for n in range(0, 129):
+        assert runtime.dynamic_args_bytes(n) == (0 if n <= 20 else 8 * n)
+    assert runtime.dynamic_args_bytes(5, 4) == 40
+
+
+def test_b200_occupancy_row():
+    # 265-byte team region (config 1 loop layout) at 64 threads, 32 regs:
+    # the 32-CTA limit binds; at 40 regs the register file does (25).
+    o = occupancy.occupancy_for("b200", 265, 32, 64)
+    assert o.actual == 32
+    assert occupancy.occupancy_for("b200", 265, 40, 64).actual == 25
+    # 1024-thread teams: the 2048-threads/SM limit binds (2 teams/SM).
+    o = occupancy.occupancy_for("b200", 289, 32, 1024)
+    assert o.potential == 2 and o.actual == 2
+
+
+def test_compute_entry_point_raises_ompds_error_without_gpu():
+    if P.lib().ompds_device_count() > 0:
+        pytest.skip("a GPU is present")
+    with pytest.raises(P.OmpdsError) as e:
+        runtime.replay([(0, 0, 8)])
+    assert e.value.code == P.ERR_CUDA
