@@ -239,16 +239,18 @@ template <class T> struct RegionsProg {
       *reinterpret_cast<T *>(m.cap(2)) = T(3);
       *reinterpret_cast<T *>(m.cap(3)) = T(4);
     }
-    int32_t *r = reinterpret_cast<int32_t *>(m.depot.base + m.p->aux_off);
+    int32_t *r = m.p->aux_off >= 0
+                     ? reinterpret_cast<int32_t *>(m.depot.base + m.p->aux_off)
+                     : nullptr;
     for (int32_t i = 0; i < a.regions; ++i) {
-      if (m.leader)
+      if (m.leader && r)
         *r = i;
       if (m.parallel(0, 4) != OMPDS_OK)
         return;
       if (m.leader) // sequential code between regions: c4 += 1
         *reinterpret_cast<T *>(m.cap(3)) += T(1);
     }
-    if (m.leader)
+    if (m.leader && r)
       *r = a.regions;
   }
   __device__ static void region(int32_t, const SharedVars &sv, const Worker &w,
@@ -823,8 +825,11 @@ int32_t ompds_run_regions(const ompds_launch *launch, int32_t elem,
   if (!a || regions < 0 || (elem != 0 && elem != 1))
     return OMPDS_ERR_INVALID;
   FixedLayout lay;
-  // c1, c2 (int), c3, c4 (elem), r (loop counter): scalars take 8-byte slots.
-  int32_t s = build_fixed_layout({4, 4, elem ? 8 : 4, elem ? 8 : 4}, 4, &lay);
+  // c1, c2 (int), c3, c4 (elem) and -- when the region sits in a sequential
+  // loop -- the loop counter r: the kernel frame group of the reference's
+  // cfg1 analog (48 B, footprint 257) or its loop variant (56 B, 265).
+  int32_t s = build_fixed_layout({4, 4, elem ? 8 : 4, elem ? 8 : 4},
+                                 regions > 1 ? 4 : 0, &lay);
   if (s)
     return s;
   if (elem == 0)

@@ -172,4 +172,5 @@ def checksum(t: torch.Tensor, stream: Optional[torch.cuda.Stream] = None) -> int
     s = (stream or torch.cuda.current_stream()).cuda_stream
     L.check(L.lib().ompds_checksum(ELEM[t.dtype], C.c_void_p(t.data_ptr()), t.numel(),
                                    C.c_void_p(out.data_ptr()), C.c_void_p(s)), "ompds_checksum")
+    (stream or torch.cuda.current_stream()).synchronize()
     return int(out.item()) & ((1 << 64) - 1)

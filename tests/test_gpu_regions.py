@@ -44,23 +44,6 @@ def canon(events, fn_of=None):
     return out
 
 
-def golden_events(team_events):
-    names = {}
-
-    def fid(name):
-        if not name:
-            return -1
-        return names.setdefault(name, len(names))
-
-    return canon([(k, fid(fn) if k.startswith("prepare") else -1 if k != "fetch" else fn,
-                   n, b) for k, fn, n, b in team_events], None)
-
-
-def norm_fetch(ev):
-    # our fetch events carry the fn id; the golden's carry the name -> compare ids
-    return ev
-
-
 # --------------------------------------------------------------------------- config 1
 
 @pytest.mark.parametrize("stem,regions", [("cfg1_analog", 1), ("cfg1_loop_analog", 5)])
