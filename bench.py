@@ -227,9 +227,9 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    from paper_1711_10413_b200 import sharding
     n_total = args.n * world if args.scaling == "weak" else args.n
-    lo = rank * n_total // world
-    hi = (rank + 1) * n_total // world
+    lo, hi = sharding.shard_range(n_total, rank, world)
     n = hi - lo
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     workers = args.workers or 992
@@ -281,11 +281,7 @@ def main():
     value = BYTES_PER_ELEM * n_total / (ms_per_step * 1e-3) / 1e9
 
     # checksum gather (once, outside the timed region)
-    c = RG.checksum(y, stream=stream)
-    cks = torch.tensor([c - (1 << 64) if c >= 1 << 63 else c], dtype=torch.int64, device=dev)
-    if world > 1:
-        dist.all_reduce(cks)
-    checksum = int(cks.item()) & ((1 << 64) - 1)
+    checksum = sharding.allreduce_checksum(RG.checksum(y, stream=stream), device=dev)
 
     # config-1 latency: 1 team x 32 workers, R regions in a loop, 4 shared scalars
     R = 10_000

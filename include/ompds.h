@@ -310,6 +310,28 @@ int32_t ompds_run_stream(const ompds_launch *launch, int32_t elem, int64_t n,
                          const void *x, void *y, const void *coef_host,
                          ompds_team_stats *stats_dev, ompds_event *events_dev);
 
+/* Config 3: nested parallel regions, depth 3, serialized inner levels whose
+ * captured locals live on per-warp data-sharing stacks: a statically sized
+ * shared-memory slot of `warp_slot_bytes` per worker warp plus a
+ * global-memory overflow chain (__kmpc_data_sharing_push_stack /
+ * _pop_stack).  Program and semantics: DESIGN.md "config 3"; the reference
+ * rejects nesting (DslParser.cpp:846-849), so the oracle restates it.
+ * `warp_stats_dev` receives teams * ceil(W/32) records (may be NULL). */
+typedef struct ompds_warp_stack_stats {
+  int32_t frame_in_smem[2]; /* level-1 / level-2 frame: 1 smem slot, 0 chain */
+  int64_t frame_offset[2];  /* offset inside that segment                  */
+  int32_t status;           /* 0 or OMPDS_TRAP_STACK_*                       */
+  int32_t max_depth;        /* deepest stack (frames)                         */
+  int64_t high_water;       /* max bytes in use (slot + chain)               */
+} ompds_warp_stack_stats;
+
+int32_t ompds_run_nested(const ompds_launch *launch, int32_t elem,
+                         int32_t regions, int64_t warp_slot_bytes,
+                         int64_t warp_overflow_bytes, void *a,
+                         ompds_team_stats *stats_dev,
+                         ompds_warp_stack_stats *warp_stats_dev,
+                         ompds_event *events_dev);
+
 /* The same region end to end from HOST buffers (pinned recommended): copies
  * x,y in, runs, copies y out, on `launch->stream`; synchronises. */
 int32_t ompds_run_stream_host(const ompds_launch *launch, int32_t elem,

@@ -473,6 +473,41 @@ void orc_stream(int32_t elem, int64_t n, const void *x, void *y, const void *coe
   }
 }
 
+void orc_nested(int32_t elem, int32_t teams, int32_t workers, int32_t regions, void *a) {
+  for (int32_t t = 0; t < teams; ++t) {
+    int32_t c = 1;
+    for (int32_t r = 0; r < regions; ++r) {
+      for (int32_t w = 0; w < workers; ++w) {
+        int32_t e = wrap_add(w, c);
+        if (elem) {
+          double *p = (double *)a + (int64_t)t * workers + w;
+          double v[4];
+          double s = (double)(w % 8 + 1);
+          for (int j = 0; j < 4; ++j) v[j] = s * (double)(j + 1);
+          double f = (double)e + v[3];      /* L2 */
+          *p = *p + (f + (double)c);        /* L3 */
+          f = f * 2.0;
+          v[0] = f;
+          e = wrap_add(e, 1);
+          *p = *p + (v[0] + (double)e);     /* back in L1 */
+        } else {
+          int32_t *p = (int32_t *)a + (int64_t)t * workers + w;
+          int32_t v[4];
+          int32_t s = w % 8 + 1;
+          for (int j = 0; j < 4; ++j) v[j] = wrap_mul(s, j + 1);
+          int32_t f = wrap_add(e, v[3]);
+          *p = wrap_add(*p, wrap_add(f, c));
+          f = wrap_mul(f, 2);
+          v[0] = f;
+          e = wrap_add(e, 1);
+          *p = wrap_add(*p, wrap_add(v[0], e));
+        }
+      }
+      c = wrap_add(c, 1);
+    }
+  }
+}
+
 int32_t orc_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

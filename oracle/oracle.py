@@ -53,6 +53,7 @@ def lib():
         L.orc_stream.argtypes = [C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_int32]
         L.orc_max_threads.restype = C.c_int32
+        L.orc_nested.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]
         L.orc_ds_stack.argtypes = [C.c_int64, C.c_int64, C.POINTER(C.c_int64),
                                    C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32),
                                    C.POINTER(C.c_int64), C.POINTER(C.c_int32),

@@ -103,6 +103,11 @@ class TeamStats(C.Structure):
                 ("n_events", C.c_int32), ("depot_offset", C.c_int64), ("smem_bytes", C.c_int64)]
 
 
+class WarpStackStats(C.Structure):
+    _fields_ = [("frame_in_smem", C.c_int32 * 2), ("frame_offset", C.c_int64 * 2),
+                ("status", C.c_int32), ("max_depth", C.c_int32), ("high_water", C.c_int64)]
+
+
 # Every symbol include/ompds.h declares, with its signature.
 _P = C.c_void_p
 _SIGS = {
@@ -128,7 +133,9 @@ _SIGS = {
                                             _P, _P]),
     "ompds_run_stream": (C.c_int32, [C.POINTER(Launch), C.c_int32, C.c_int64, _P, _P, _P, _P,
                                       _P]),
-    "ompds_run_stream_host": (C.c_int32, [C.POINTER(Launch), C.c_int32, C.c_int64, _P, _P, _P,
+    "ompds_run_nested": (C.c_int32, [C.POINTER(Launch), C.c_int32, C.c_int32, C.c_int64,
+                                      C.c_int64, _P, _P, _P, _P]),
+    "ompds_run_stream_host":(C.c_int32, [C.POINTER(Launch), C.c_int32, C.c_int64, _P, _P, _P,
                                            _P, _P]),
     "ompds_fill_uniform": (C.c_int32, [C.c_int32, _P, C.c_int64, C.c_uint64, C.c_int64, _P]),
     "ompds_checksum": (C.c_int32, [C.c_int32, _P, C.c_int64, _P, _P]),

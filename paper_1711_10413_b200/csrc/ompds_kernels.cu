@@ -58,6 +58,9 @@ struct TeamParams {
   ompds_team_stats *stats;
   int64_t cap_off[kMaxCaptures]; // depot offsets of the captures (layout)
   int64_t aux_off;       // depot offset of the sequential loop counter (-1)
+  int64_t warp_slot_bytes;       // per-warp data-sharing slot in smem
+  unsigned char *warp_ovf;       // teams * worker_warps * warp_ovf_bytes
+  int64_t warp_ovf_bytes;
 };
 
 // Master-warp view of the sequential region.  Every lane runs it; lane 0
@@ -150,6 +153,9 @@ struct Master {
       st.depot_offset = depot.offset;
       st.n_events = static_cast<int32_t>(t.at<uint32_t>(Rt::kEvents));
       st.smem_bytes = team_region_bytes(p->depot_cap, p->prealloc);
+      if (p->warp_slot_bytes > 0)
+        st.smem_bytes = round_up(st.smem_bytes, 16) +
+                        int64_t(team_threads / 32 - 1) * p->warp_slot_bytes;
       p->stats[blockIdx.x] = st;
     }
     __syncwarp();
@@ -166,6 +172,8 @@ struct Worker {
   int32_t team;
   int32_t teams;
   int32_t workers;
+  int32_t warp;
+  DsStack ds;   // this warp's data-sharing stack (nested regions)
 };
 
 template <class Prog>
@@ -199,6 +207,14 @@ __global__ void __launch_bounds__(1024, 1)
     w.team = blockIdx.x;
     w.teams = gridDim.x;
     w.workers = p.workers;
+    w.warp = warp;
+    // Per-warp data-sharing stack: a statically sized slot after the team
+    // region, then this warp's slice of the global overflow chain.
+    unsigned char *slot = smem + round_up(region, 16) + int64_t(warp) * p.warp_slot_bytes;
+    unsigned char *ovf =
+        p.warp_ovf ? p.warp_ovf + (size_t(blockIdx.x) * worker_warps + warp) * p.warp_ovf_bytes
+                   : nullptr;
+    w.ds.init(slot, p.warp_slot_bytes, ovf, p.warp_ovf ? p.warp_ovf_bytes : 0);
     for (;;) {
       bar_sync(kBarHandoff, team_threads); // await.work
       Fetch f = begin_parallel_warp(t, w.mine);
@@ -478,6 +494,105 @@ template <class T> struct StreamProg {
 };
 
 //===----------------------------------------------------------------------===//
+// Config 3: nested parallel regions (depth 3) with per-warp data-sharing
+// stacks.  The reference rejects nesting (DslParser.cpp:846-849); the
+// semantics here are the LLVM NVPTX runtime's the paper builds on: a nested
+// region is serialized on the encountering thread (team of one), and the
+// encountering level's locals it captures are globalized on the warp's
+// data-sharing stack (one lane-strided frame per warp).  Program:
+//
+//   master:  int c = 1; T s[8] = {1..8};
+//            for r < R: parallel { L1 } ; c += 1
+//   L1(w):   int e = w + c; T v[4] = {s[w%8]*(j+1)};
+//            parallel { L2 } ; a[t*W+w] += v[0] + e
+//   L2:      T f = e + v[3]; parallel { L3 } ; v[0] = f; e += 1
+//   L3:      a[t*W+w] += f + c; f = f * 2
+//===----------------------------------------------------------------------===//
+
+template <class T> struct NestedProg {
+  struct Args {
+    T *a;
+    int32_t regions;
+    int32_t l1_bytes; // level-1 frame per lane (layout of e, v)
+    int32_t e_off, v_off;
+    int32_t l2_bytes; // level-2 frame per lane (layout of f)
+    int32_t f_off;
+    ompds_warp_stack_stats *wstats; // teams * worker_warps
+  };
+  __device__ static void master(Master &m, const Args &a) {
+    if (m.leader) {
+      *reinterpret_cast<int32_t *>(m.cap(0)) = 1;
+      T *s = reinterpret_cast<T *>(m.cap(1));
+      for (int k = 0; k < 8; ++k)
+        s[k] = T(k + 1);
+    }
+    __syncwarp();
+    for (int32_t r = 0; r < a.regions; ++r) {
+      if (m.parallel(0, 2) != OMPDS_OK)
+        return;
+      if (m.leader)
+        *reinterpret_cast<int32_t *>(m.cap(0)) += 1;
+    }
+  }
+  __device__ static void region(int32_t, const SharedVars &sv, Worker &w,
+                                const Args &a) {
+    const int32_t *cp = static_cast<const int32_t *>(sv.get(0));
+    const T *sp = static_cast<const T *>(sv.get(1));
+    const uint32_t lane = lane_id();
+    // L1: its captured locals live in this warp's stack frame.
+    Frame f1 = w.ds.push(a.l1_bytes, kWarp);
+    Frame f2{};
+    int32_t s1 = OMPDS_OK, s2 = OMPDS_OK;
+    if (f1.status != OMPDS_OK)
+      goto done; // overflow chain exhausted: recorded, region skipped
+    {
+    unsigned char *my1 = f1.base + int64_t(lane) * a.l1_bytes;
+    int32_t *e = reinterpret_cast<int32_t *>(my1 + a.e_off);
+    T *v = reinterpret_cast<T *>(my1 + a.v_off);
+    *e = w.wid + *cp;
+    const T sw = sp[w.wid % 8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      v[j] = sw * T(j + 1);
+    // L2 (serialized nested region): globalizes f.
+    f2 = w.ds.push(a.l2_bytes, kWarp);
+    if (f2.status != OMPDS_OK) {
+      s1 = w.ds.pop(f1);
+      goto done;
+    }
+    {
+    T *f = reinterpret_cast<T *>(f2.base + int64_t(lane) * a.l2_bytes + a.f_off);
+    *f = T(*e) + v[3];
+    // L3 (serialized nested region)
+    T *dst = a.a + size_t(w.team) * w.workers + w.wid;
+    if (w.mine)
+      *dst = *dst + (*f + T(*cp));
+    *f = *f * T(2);
+    v[0] = *f;
+    *e = *e + 1;
+    s2 = w.ds.pop(f2);
+    if (w.mine)
+      *dst = *dst + (v[0] + T(*e));
+    s1 = w.ds.pop(f1);
+    }
+    }
+  done:
+    __syncwarp();
+    if (lane == 0 && a.wstats) {
+      ompds_warp_stack_stats st;
+      st.frame_in_smem[0] = f1.in_smem;
+      st.frame_in_smem[1] = f2.in_smem;
+      st.frame_offset[0] = f1.offset;
+      st.frame_offset[1] = f2.offset;
+      st.status = f1.status ? f1.status : f2.status ? f2.status : s2 ? s2 : s1;
+      st.max_depth = w.ds.max_depth;
+      st.high_water = w.ds.high_water;
+      a.wstats[size_t(w.team) * (blockDim.x / 32 - 1) + w.warp] = st;
+    }
+  }
+};
+
+//===----------------------------------------------------------------------===//
 // Protocol replay: one device thread drives the single-caller runtime
 // functions over a team region in shared memory (the TeamRuntime API).
 //===----------------------------------------------------------------------===//
@@ -615,32 +730,39 @@ __global__ void checksum_kernel(const T *data, int64_t n,
 // Host side: workspace, layouts for the fixed configs, launch helpers.
 //===----------------------------------------------------------------------===//
 
+// Library-owned global memory reused across launches on a device: buffer 0
+// holds the teams' overflow slabs (args lists, master depot overflow),
+// buffer 1 the worker warps' data-sharing overflow chains.  Launches that
+// run concurrently on different streams must not share a device.
 struct Workspace {
   std::mutex mu;
   int device = -1;
-  unsigned char *slabs = nullptr;
-  size_t slab_total = 0;
-  int sm_count = 0;
+  unsigned char *buf[2] = {nullptr, nullptr};
+  size_t bytes[2] = {0, 0};
 };
 static Workspace g_ws;
 
-static int32_t ensure_slabs(size_t bytes, unsigned char **out) {
+static int32_t ensure_buffer(int which, size_t bytes, unsigned char **out) {
   std::lock_guard<std::mutex> lk(g_ws.mu);
   int dev = 0;
   OMPDS_CUDA(cudaGetDevice(&dev));
   if (g_ws.device != dev) {
-    g_ws.slabs = nullptr; // leaked on device switch (bounded, rare)
-    g_ws.slab_total = 0;
+    for (int i = 0; i < 2; ++i) { // leaked on device switch (bounded, rare)
+      g_ws.buf[i] = nullptr;
+      g_ws.bytes[i] = 0;
+    }
     g_ws.device = dev;
   }
-  if (g_ws.slab_total < bytes) {
-    if (g_ws.slabs)
-      OMPDS_CUDA(cudaFree(g_ws.slabs));
-    g_ws.slabs = nullptr;
-    OMPDS_CUDA(cudaMalloc(&g_ws.slabs, bytes));
-    g_ws.slab_total = bytes;
+  if (g_ws.bytes[which] < bytes) {
+    if (g_ws.buf[which]) {
+      OMPDS_CUDA(cudaDeviceSynchronize());
+      OMPDS_CUDA(cudaFree(g_ws.buf[which]));
+    }
+    g_ws.buf[which] = nullptr;
+    OMPDS_CUDA(cudaMalloc(&g_ws.buf[which], bytes));
+    g_ws.bytes[which] = bytes;
   }
-  *out = g_ws.slabs;
+  *out = g_ws.buf[which];
   return OMPDS_OK;
 }
 
@@ -703,7 +825,8 @@ constexpr uint32_t kSlabBytes = 8192; // per team: args lists + depot overflow
 template <class Prog>
 int32_t launch_generic(const ompds_launch *l, const FixedLayout &lay,
                        int32_t n_caps, const typename Prog::Args &args,
-                       ompds_team_stats *stats, ompds_event *events) {
+                       ompds_team_stats *stats, ompds_event *events,
+                       int64_t warp_slot_bytes = 0, int64_t warp_ovf_bytes = 0) {
   int32_t s = validate_launch(l);
   if (s)
     return s;
@@ -725,11 +848,23 @@ int32_t launch_generic(const ompds_launch *l, const FixedLayout &lay,
   p.aux_off = lay.aux_off;
   p.slab_bytes = std::max<uint32_t>(
       kSlabBytes, static_cast<uint32_t>(round_up(2 * lay.total_shared + 64, 256)));
-  s = ensure_slabs(size_t(p.slab_bytes) * l->teams, &p.slabs);
+  s = ensure_buffer(0, size_t(p.slab_bytes) * l->teams, &p.slabs);
   if (s)
     return s;
   const int threads = static_cast<int>(round_up(l->workers, 32)) + 32;
-  const size_t smem = static_cast<size_t>(team_region_bytes(p.depot_cap, p.prealloc));
+  const int worker_warps = threads / 32 - 1;
+  p.warp_slot_bytes = round_up(warp_slot_bytes, 16);
+  p.warp_ovf_bytes = round_up(warp_ovf_bytes, 256);
+  if (p.warp_ovf_bytes > 0) {
+    s = ensure_buffer(1, size_t(p.warp_ovf_bytes) * worker_warps * l->teams, &p.warp_ovf);
+    if (s)
+      return s;
+  }
+  size_t smem = static_cast<size_t>(team_region_bytes(p.depot_cap, p.prealloc));
+  if (p.warp_slot_bytes > 0)
+    smem = static_cast<size_t>(round_up(int64_t(smem), 16) + worker_warps * p.warp_slot_bytes);
+  if (smem > 227 * 1024)
+    return OMPDS_ERR_INVALID;
   auto kern = generic_mode_kernel<Prog>;
   if (smem > 48 * 1024)
     OMPDS_CUDA(cudaFuncSetAttribute(kern,
@@ -887,6 +1022,58 @@ int32_t ompds_run_stream(const ompds_launch *launch, int32_t elem, int64_t n,
                              static_cast<double *>(y), n, {}};
   std::memcpy(a.coef, coef_host, sizeof(a.coef));
   return launch_generic<StreamProg<double>>(launch, lay8, 8, a, stats, events);
+}
+
+int32_t ompds_run_nested(const ompds_launch *launch, int32_t elem,
+                         int32_t regions, int64_t warp_slot_bytes,
+                         int64_t warp_overflow_bytes, void *a,
+                         ompds_team_stats *stats,
+                         ompds_warp_stack_stats *warp_stats,
+                         ompds_event *events) {
+  if (!a || regions < 0 || (elem != 0 && elem != 1) || warp_slot_bytes < 0 ||
+      warp_overflow_bytes < 0)
+    return OMPDS_ERR_INVALID;
+  const int64_t esz = elem ? 8 : 4;
+  // Kernel group: c (int), s[8] (elem) captured; wf.addr, args.addr.
+  FixedLayout lay;
+  int32_t s = build_fixed_layout({4, 8 * esz}, 0, &lay);
+  if (s)
+    return s;
+  // Frame groups of the outlined level-1 and level-2 functions: their
+  // escaping locals (e, v[4]) and (f), laid out by the same frame pipeline.
+  ompds_frame_var vars[3] = {{0, 0, OMPDS_VAR_ESCAPES, -1, 4, -1, -1},
+                             {0, 0, OMPDS_VAR_ESCAPES, -1, 4 * esz, -1, -1},
+                             {1, 0, OMPDS_VAR_ESCAPES, -1, esz, -1, -1}};
+  ompds_depot_layout lays[2];
+  ompds_depot_slot slots[3];
+  int32_t owners[3];
+  s = ompds_layout_build(vars, 3, 2, OMPDS_PIPELINE_DEFAULT, lays, slots, 3,
+                         owners, 3);
+  if (s)
+    return s;
+  if (elem == 0) {
+    NestedProg<int32_t>::Args args{static_cast<int32_t *>(a),
+                                   regions,
+                                   static_cast<int32_t>(lays[0].total_shared),
+                                   static_cast<int32_t>(slots[0].offset),
+                                   static_cast<int32_t>(slots[1].offset),
+                                   static_cast<int32_t>(lays[1].total_shared),
+                                   static_cast<int32_t>(slots[2].offset),
+                                   warp_stats};
+    return launch_generic<NestedProg<int32_t>>(launch, lay, 2, args, stats,
+                                               events, warp_slot_bytes,
+                                               warp_overflow_bytes);
+  }
+  NestedProg<double>::Args args{static_cast<double *>(a),
+                                regions,
+                                static_cast<int32_t>(lays[0].total_shared),
+                                static_cast<int32_t>(slots[0].offset),
+                                static_cast<int32_t>(slots[1].offset),
+                                static_cast<int32_t>(lays[1].total_shared),
+                                static_cast<int32_t>(slots[2].offset),
+                                warp_stats};
+  return launch_generic<NestedProg<double>>(launch, lay, 2, args, stats, events,
+                                            warp_slot_bytes, warp_overflow_bytes);
 }
 
 int32_t ompds_run_stream_host(const ompds_launch *launch, int32_t elem,

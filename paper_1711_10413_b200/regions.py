@@ -123,6 +123,39 @@ def run_shared_array(a: torch.Tensor, teams: int, workers: int,
     return out
 
 
+@dataclass
+class WarpStack:
+    frame_in_smem: List[bool]
+    frame_offset: List[int]
+    status: int
+    max_depth: int
+    high_water: int
+
+
+def run_nested(a: torch.Tensor, teams: int, workers: int, regions: int,
+               warp_slot_bytes: int = 2048, warp_overflow_bytes: int = 4096, **kw):
+    """Config 3: nested regions (depth 3) on per-warp data-sharing stacks.
+
+    Returns (Outputs, per-team list of per-warp :class:`WarpStack`)."""
+    _require_cuda(a)
+    max_events = kw.pop("max_events", 0)
+    out = Outputs(teams, a.device, max_events)
+    warps = (workers + 31) // 32
+    ws = torch.zeros(teams * warps * C.sizeof(L.WarpStackStats), dtype=torch.uint8,
+                     device=a.device)
+    launch = make_launch(teams, workers, log_events=max_events > 0, max_events=max_events, **kw)
+    L.check(L.lib().ompds_run_nested(C.byref(launch), ELEM[a.dtype], regions, warp_slot_bytes,
+                                     warp_overflow_bytes, C.c_void_p(a.data_ptr()),
+                                     out.stats_ptr(), C.c_void_p(ws.data_ptr()),
+                                     out.events_ptr()), "ompds_run_nested")
+    raw = bytes(ws.cpu().numpy().tobytes())
+    arr = (L.WarpStackStats * (teams * warps)).from_buffer_copy(raw)
+    stacks = [[WarpStack([bool(x) for x in s.frame_in_smem], list(s.frame_offset), s.status,
+                         s.max_depth, s.high_water) for s in arr[t * warps:(t + 1) * warps]]
+              for t in range(teams)]
+    return out, stacks
+
+
 def coef_buffer(dtype: torch.dtype, coef) -> C.Array:
     if dtype == torch.float64:
         return (C.c_double * 8)(*[float(c) for c in coef])
