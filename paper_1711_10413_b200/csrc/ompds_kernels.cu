@@ -1082,17 +1082,52 @@ int32_t ompds_run_stream_host(const ompds_launch *launch, int32_t elem,
                               void *y_dev) {
   if (!launch || !x_host || !y_host || !x_dev || !y_dev)
     return OMPDS_ERR_INVALID;
-  const size_t bytes = static_cast<size_t>(n) * (elem ? 8 : 4);
+  // Pipelined over element chunks: H2D of chunk k+1 and D2H of chunk k-1
+  // overlap the region on chunk k (copy engines in both directions plus the
+  // SMs).  Each chunk is one target-region launch over its element range;
+  // the body is element-wise, so results equal one launch over [0, n).
+  const int64_t esz = elem ? 8 : 4;
+  const int64_t chunk = std::max<int64_t>(int64_t(1) << 23, round_up((n + 31) / 32, 1024));
   cudaStream_t st = static_cast<cudaStream_t>(launch->stream);
-  OMPDS_CUDA(cudaMemcpyAsync(x_dev, x_host, bytes, cudaMemcpyHostToDevice, st));
-  OMPDS_CUDA(cudaMemcpyAsync(y_dev, y_host, bytes, cudaMemcpyHostToDevice, st));
-  int32_t s = ompds_run_stream(launch, elem, n, x_dev, y_dev, coef_host,
-                               nullptr, nullptr);
-  if (s)
-    return s;
-  OMPDS_CUDA(cudaMemcpyAsync(y_host, y_dev, bytes, cudaMemcpyDeviceToHost, st));
+  static thread_local cudaStream_t h2d = nullptr, d2h = nullptr;
+  static thread_local int dev_of = -1;
+  int dev = 0;
+  OMPDS_CUDA(cudaGetDevice(&dev));
+  if (h2d == nullptr || dev_of != dev) {
+    OMPDS_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+    OMPDS_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+    dev_of = dev;
+  }
+  const int64_t nchunks = n == 0 ? 0 : (n + chunk - 1) / chunk;
+  std::vector<cudaEvent_t> ev(static_cast<size_t>(2 * nchunks + 1));
+  for (auto &e : ev)
+    OMPDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // copies must not start before the caller's prior work on `st`
+  OMPDS_CUDA(cudaEventRecord(ev[2 * nchunks], st));
+  OMPDS_CUDA(cudaStreamWaitEvent(h2d, ev[2 * nchunks], 0));
+  int32_t s = OMPDS_OK;
+  for (int64_t k = 0; k < nchunks && s == OMPDS_OK; ++k) {
+    const int64_t lo = k * chunk, len = std::min(chunk, n - lo);
+    const size_t off = static_cast<size_t>(lo * esz), bytes = static_cast<size_t>(len * esz);
+    auto *xd = static_cast<unsigned char *>(x_dev) + off;
+    auto *yd = static_cast<unsigned char *>(y_dev) + off;
+    OMPDS_CUDA(cudaMemcpyAsync(xd, static_cast<const unsigned char *>(x_host) + off, bytes,
+                               cudaMemcpyHostToDevice, h2d));
+    OMPDS_CUDA(cudaMemcpyAsync(yd, static_cast<unsigned char *>(y_host) + off, bytes,
+                               cudaMemcpyHostToDevice, h2d));
+    OMPDS_CUDA(cudaEventRecord(ev[2 * k], h2d));
+    OMPDS_CUDA(cudaStreamWaitEvent(st, ev[2 * k], 0));
+    s = ompds_run_stream(launch, elem, len, xd, yd, coef_host, nullptr, nullptr);
+    OMPDS_CUDA(cudaEventRecord(ev[2 * k + 1], st));
+    OMPDS_CUDA(cudaStreamWaitEvent(d2h, ev[2 * k + 1], 0));
+    OMPDS_CUDA(cudaMemcpyAsync(static_cast<unsigned char *>(y_host) + off, yd, bytes,
+                               cudaMemcpyDeviceToHost, d2h));
+  }
+  OMPDS_CUDA(cudaStreamSynchronize(d2h));
   OMPDS_CUDA(cudaStreamSynchronize(st));
-  return OMPDS_OK;
+  for (auto &e : ev)
+    cudaEventDestroy(e);
+  return s;
 }
 
 int32_t ompds_fill_uniform(int32_t elem, void *out, int64_t n, uint64_t seed,

@@ -200,6 +200,19 @@ def test_config4_spilled_args_list_and_alloc_failure():
     assert all(st.trap == 9 and st.regions == 0 for st in out.team_stats())
 
 
+def test_config4_host_buffer_entry_point_matches_oracle():
+    n = (1 << 24) + 5  # three pipelined chunks
+    x, y = _f64_inputs(n)
+    xh = x.cpu().pin_memory()
+    yh = y.cpu().pin_memory()
+    xs, ys = xh.numpy().copy(), yh.numpy().copy()
+    xd = torch.empty_like(x)
+    yd = torch.empty_like(y)
+    RG.run_stream_host(xh, yh, COEF, 148, 992, xd, yd)
+    O.lib().orc_stream(1, n, O.ptr(xs), O.ptr(ys), O.ptr(np.array(COEF)), 0)
+    assert np.array_equal(yh.numpy().view(np.uint64), ys.view(np.uint64))
+
+
 def test_config4_full_size_checksum_vs_oracle():
     n = 1 << 28
     x, y = _f64_inputs(n)

@@ -75,7 +75,10 @@ def test_gpu_nested_values_and_stack_placement(elem, slot):
     for s in out.team_stats():
         assert s.trap == 0 and s.regions == regions and s.master_barriers == 2 * regions
         depot = 8 + 8 * (8 if elem else 4) + 16
-        assert s.smem_bytes == ((depot + 209 + 15) // 16) * 16 + 3 * ((slot + 15) // 16) * 16
+        region = depot + 209
+        if slot:
+            region = (region + 15) // 16 * 16 + 3 * ((slot + 15) // 16) * 16
+        assert s.smem_bytes == region
 
 
 @pytest.mark.gpu
