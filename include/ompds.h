@@ -56,6 +56,8 @@ typedef enum ompds_status {
   /* data-sharing stack (new; no reference counterpart) */
   OMPDS_TRAP_STACK_OVERFLOW = 18,  /* global overflow chain exhausted */
   OMPDS_TRAP_STACK_UNDERFLOW = 19, /* pop of a frame that is not the top */
+  OMPDS_TRAP_OUT_OF_BOUNDS = 20,   /* region program: index outside its object
+                                      (Simulator.cpp:313-377 "out-of-bounds") */
   /* host-side errors */
   OMPDS_ERR_CUDA = 100,    /* no usable CUDA device / launch or copy failed */
   OMPDS_ERR_INVALID = 101, /* invalid argument */
@@ -331,6 +333,45 @@ int32_t ompds_run_nested(const ompds_launch *launch, int32_t elem,
                          ompds_team_stats *stats_dev,
                          ompds_warp_stack_stats *warp_stats_dev,
                          ompds_event *events_dev);
+
+/* Region programs: the reference's kernel language (int32 scalars/arrays,
+ * `parallel` / `parallel for`) lowered by paper_1711_10413_b200/program.py
+ * to a stack bytecode that the generic-mode kernel interprets inside the
+ * real protocol (master lane: sequential code; workers: region bodies).
+ * Variables live where the frame layout puts them (space): 0 team depot
+ * (shared slot), 1 the master's local depot mirror, 2 the worker's private
+ * frame, 3 capture j of the current region (via get-shared-variables),
+ * 4 mapped buffer.  All host arrays below are copied per launch. */
+typedef struct ompds_prog_var {
+  int32_t space;  /* 0..4 as above                           */
+  int32_t index;  /* byte offset (0..2), capture j, buffer k */
+  int32_t count;  /* elements (int32) for bounds checks       */
+  int32_t _pad;
+} ompds_prog_var;
+typedef struct ompds_prog_region {
+  int32_t entry;      /* pc of the region body            */
+  int32_t n_captures; /* nargs of its prepare_parallel    */
+  int32_t cap_begin;  /* into `captures` (var indices)    */
+  int32_t _pad;
+} ompds_prog_region;
+typedef struct ompds_program {
+  const int32_t *code;
+  int64_t n_code;
+  const ompds_prog_var *vars;
+  int32_t n_vars;
+  int32_t n_regions;
+  const ompds_prog_region *regions;
+  const int32_t *captures;
+  int32_t n_captures;
+  int32_t n_buffers;
+  void *const *buffers; /* host array of DEVICE int32 buffer pointers */
+  int64_t total_shared; /* kernel frame group depot (TotalShared)     */
+  int64_t total_local;  /* its local mirror                            */
+  int64_t priv_bytes;   /* largest outlined-function frame             */
+} ompds_program;
+
+int32_t ompds_run_program(const ompds_launch *launch, const ompds_program *prog,
+                          ompds_team_stats *stats_dev, ompds_event *events_dev);
 
 /* The same region end to end from HOST buffers (pinned recommended): copies
  * x,y in, runs, copies y out, on `launch->stream`; synchronises. */

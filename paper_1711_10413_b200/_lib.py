@@ -108,6 +108,25 @@ class WarpStackStats(C.Structure):
                 ("status", C.c_int32), ("max_depth", C.c_int32), ("high_water", C.c_int64)]
 
 
+class ProgVar(C.Structure):
+    _fields_ = [("space", C.c_int32), ("index", C.c_int32), ("count", C.c_int32),
+                ("_pad", C.c_int32)]
+
+
+class ProgRegion(C.Structure):
+    _fields_ = [("entry", C.c_int32), ("n_captures", C.c_int32), ("cap_begin", C.c_int32),
+                ("_pad", C.c_int32)]
+
+
+class Program(C.Structure):
+    _fields_ = [("code", C.POINTER(C.c_int32)), ("n_code", C.c_int64),
+                ("vars", C.POINTER(ProgVar)), ("n_vars", C.c_int32), ("n_regions", C.c_int32),
+                ("regions", C.POINTER(ProgRegion)), ("captures", C.POINTER(C.c_int32)),
+                ("n_captures", C.c_int32), ("n_buffers", C.c_int32),
+                ("buffers", C.POINTER(C.c_void_p)), ("total_shared", C.c_int64),
+                ("total_local", C.c_int64), ("priv_bytes", C.c_int64)]
+
+
 # Every symbol include/ompds.h declares, with its signature.
 _P = C.c_void_p
 _SIGS = {
@@ -135,6 +154,7 @@ _SIGS = {
                                       _P]),
     "ompds_run_nested": (C.c_int32, [C.POINTER(Launch), C.c_int32, C.c_int32, C.c_int64,
                                       C.c_int64, _P, _P, _P, _P]),
+    "ompds_run_program": (C.c_int32, [C.POINTER(Launch), C.POINTER(Program), _P, _P]),
     "ompds_run_stream_host":(C.c_int32, [C.POINTER(Launch), C.c_int32, C.c_int64, _P, _P, _P,
                                            _P, _P]),
     "ompds_fill_uniform": (C.c_int32, [C.c_int32, _P, C.c_int64, C.c_uint64, C.c_int64, _P]),

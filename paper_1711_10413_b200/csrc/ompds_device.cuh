@@ -408,18 +408,29 @@ __device__ __forceinline__ SharedVars get_shared_variables(void **args,
                                                            int32_t nargs) {
   SharedVars v;
   const uint32_t lane = lane_id();
-  v.mine = (args != nullptr && static_cast<int32_t>(lane) < nargs) ? args[lane]
-                                                                   : nullptr;
+  v.mine = nullptr;
+  if (args != nullptr && static_cast<int32_t>(lane) < nargs) {
+    if (__isShared(args)) { // the preallocated window: a plain LDS
+      const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(args));
+      unsigned long long p;
+      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(p) : "r"(sa + 8u * lane));
+      v.mine = reinterpret_cast<void *>(p);
+    } else { // a global overflow block
+      v.mine = args[lane];
+    }
+  }
   return v;
 }
 
 // Loads capture j's value through its pointer: lane j dereferences, then a
-// shuffle broadcasts the value (T is 4 or 8 bytes).
+// shuffle broadcasts the value (T is 4 or 8 bytes).  A weak load suffices:
+// the master's stores precede the release barrier, and bar.sync orders
+// shared and global memory among the CTA's participating threads.
 template <class T>
 __device__ __forceinline__ T shared_value(const SharedVars &v, int j) {
   T x{};
   if (static_cast<int>(lane_id()) == j && v.mine)
-    x = *static_cast<const volatile T *>(v.mine);
+    x = *static_cast<const T *>(v.mine);
   return __shfl_sync(0xffffffffu, x, j);
 }
 

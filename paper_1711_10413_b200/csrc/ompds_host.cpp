@@ -33,6 +33,7 @@ const char *const kTrapStrings[] = {
     "protocol error: kernel_deinit called twice",
     "data-sharing stack overflow",
     "data-sharing stack underflow",
+    "out-of-bounds access",
 };
 
 int64_t roundUp8(int64_t n) { return (n + 7) & ~int64_t(7); }

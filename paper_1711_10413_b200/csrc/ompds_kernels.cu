@@ -116,6 +116,14 @@ struct Master {
 
   // prepare_parallel + publish &capture_j into the list + release + join.
   __device__ __forceinline__ int32_t parallel(int32_t fn, int32_t nargs) {
+    return parallel_with(fn, nargs, [this](int j) -> void * {
+      return cap(j < kMaxCaptures ? j : 0);
+    });
+  }
+
+  template <class AddrOf>
+  __device__ __forceinline__ int32_t parallel_with(int32_t fn, int32_t nargs,
+                                                   AddrOf addr_of) {
     void **list = nullptr;
     int32_t s = 0;
     if (leader)
@@ -127,7 +135,7 @@ struct Master {
     // The reserved warp publishes the pointer list lane-parallel (one
     // coalesced store per 32 entries) instead of nargs scalar stores.
     for (int j = lane_id(); j < nargs; j += 32)
-      list[j] = cap(j < kMaxCaptures ? j : 0);
+      list[j] = addr_of(j);
     bar_sync(kBarHandoff, team_threads); // release the workers
     bar_sync(kBarHandoff, team_threads); // join
     barriers += 2;
@@ -174,6 +182,9 @@ struct Worker {
   int32_t workers;
   int32_t warp;
   DsStack ds;   // this warp's data-sharing stack (nested regions)
+  const TeamCtx *t;
+  void **args;  // the fetched shared-args list
+  int32_t nargs;
 };
 
 template <class Prog>
@@ -208,6 +219,9 @@ __global__ void __launch_bounds__(1024, 1)
     w.teams = gridDim.x;
     w.workers = p.workers;
     w.warp = warp;
+    w.t = &t;
+    w.args = nullptr;
+    w.nargs = 0;
     // Per-warp data-sharing stack: a statically sized slot after the team
     // region, then this warp's slice of the global overflow chain.
     unsigned char *slot = smem + round_up(region, 16) + int64_t(warp) * p.warp_slot_bytes;
@@ -221,6 +235,8 @@ __global__ void __launch_bounds__(1024, 1)
       if (f.fn < 0 && f.status == OMPDS_OK)
         break; // termination sentinel
       if (f.status == OMPDS_OK) {
+        w.args = f.args;
+        w.nargs = f.nargs;
         SharedVars sv = get_shared_variables(f.args, f.nargs);
         Prog::region(f.fn, sv, w, a);
         end_parallel_warp(t, w.mine);
@@ -258,10 +274,12 @@ template <class T> struct RegionsProg {
     int32_t *r = m.p->aux_off >= 0
                      ? reinterpret_cast<int32_t *>(m.depot.base + m.p->aux_off)
                      : nullptr;
+    // lane j < 4 keeps &c_{j+1}: publishing the list is one store per lane
+    void *mine = lane_id() < 4 ? static_cast<void *>(m.cap(lane_id())) : nullptr;
     for (int32_t i = 0; i < a.regions; ++i) {
       if (m.leader && r)
         *r = i;
-      if (m.parallel(0, 4) != OMPDS_OK)
+      if (m.parallel_with(0, 4, [mine](int) { return mine; }) != OMPDS_OK)
         return;
       if (m.leader) // sequential code between regions: c4 += 1
         *reinterpret_cast<T *>(m.cap(3)) += T(1);
@@ -271,14 +289,17 @@ template <class T> struct RegionsProg {
   }
   __device__ static void region(int32_t, const SharedVars &sv, const Worker &w,
                                 const Args &a) {
+    // The body's global load does not depend on the captures: issue it
+    // first so its latency overlaps get-shared-variables.
+    T *dst = a.a + size_t(w.team) * w.workers + w.wid;
+    const T old = w.mine ? *dst : T(0);
     const int32_t c1 = shared_value<int32_t>(sv, 0);
     const int32_t c2 = shared_value<int32_t>(sv, 1);
     const T c3 = shared_value<T>(sv, 2);
     const T c4 = shared_value<T>(sv, 3);
     if (w.mine) {
       T sum = (T(c1 + c2) + c3) + c4;
-      T *dst = a.a + size_t(w.team) * w.workers + w.wid;
-      *dst = *dst + sum;
+      *dst = old + sum;
     }
   }
 };
@@ -593,6 +614,177 @@ template <class T> struct NestedProg {
 };
 
 //===----------------------------------------------------------------------===//
+// Region programs (paper_1711_10413_b200/program.py): the reference's kernel
+// language as stack bytecode, interpreted inside the real protocol.  i32
+// storage and wrap-around after every operation (Simulator.cpp:29-42).
+//===----------------------------------------------------------------------===//
+
+enum : int32_t {
+  OP_END, OP_PUSH, OP_LOAD, OP_STORE, OP_LOADX, OP_STOREX, OP_ADD, OP_SUB,
+  OP_MUL, OP_TID, OP_TEAM, OP_NTHREADS, OP_NTEAMS, OP_JMP, OP_JNLT,
+  OP_PARALLEL, OP_ZERO_PRIV
+};
+enum : int32_t { SP_DEPOT, SP_MLOCAL, SP_PRIV, SP_CAPTURE, SP_GLOBAL };
+
+constexpr int kVmStack = 32;
+constexpr int kVmPriv = 256;    // bytes of a worker's private frame
+constexpr int kVmCaps = 128;    // captures per region
+
+struct VmCtx {
+  const int32_t *code;
+  const ompds_prog_var *vars;
+  void *const *bufs;
+  unsigned char *depot;
+  unsigned char *mlocal;
+  unsigned char *priv;
+  void *const *caps;
+  int32_t tid, team, nthreads, nteams;
+};
+
+// Resolves element `idx` of variable `v`; nullptr when out of bounds.
+__device__ __forceinline__ int32_t *vm_addr(const VmCtx &c, int32_t v,
+                                            int32_t idx) {
+  const ompds_prog_var d = c.vars[v];
+  if (idx < 0 || idx >= d.count)
+    return nullptr;
+  unsigned char *base;
+  switch (d.space) {
+  case SP_DEPOT: base = c.depot + d.index; break;
+  case SP_MLOCAL: base = c.mlocal + d.index; break;
+  case SP_PRIV: base = c.priv + d.index; break;
+  case SP_CAPTURE: base = static_cast<unsigned char *>(c.caps[d.index]); break;
+  default: base = static_cast<unsigned char *>(c.bufs[d.index]); break;
+  }
+  return reinterpret_cast<int32_t *>(base) + idx;
+}
+
+// Runs from *pc until END (returns 0), PARALLEL (returns 1, region in *r)
+// or a trap (returns the trap code, negated).
+__device__ int32_t vm_run(const VmCtx &c, int32_t *pc_io, int32_t *r) {
+  int32_t st[kVmStack];
+  int sp = 0;
+  int32_t pc = *pc_io;
+  for (;;) {
+    const int32_t op = c.code[pc++];
+    switch (op) {
+    case OP_END:
+      *pc_io = pc;
+      return 0;
+    case OP_PUSH: st[sp++] = c.code[pc++]; break;
+    case OP_LOAD: {
+      int32_t *p = vm_addr(c, c.code[pc++], 0);
+      if (!p) return -OMPDS_TRAP_OUT_OF_BOUNDS;
+      st[sp++] = *p;
+      break;
+    }
+    case OP_STORE: {
+      int32_t *p = vm_addr(c, c.code[pc++], 0);
+      if (!p) return -OMPDS_TRAP_OUT_OF_BOUNDS;
+      *p = st[--sp];
+      break;
+    }
+    case OP_LOADX: {
+      int32_t *p = vm_addr(c, c.code[pc++], st[sp - 1]);
+      if (!p) return -OMPDS_TRAP_OUT_OF_BOUNDS;
+      st[sp - 1] = *p;
+      break;
+    }
+    case OP_STOREX: {
+      const int32_t val = st[--sp];
+      const int32_t idx = st[--sp];
+      int32_t *p = vm_addr(c, c.code[pc++], idx);
+      if (!p) return -OMPDS_TRAP_OUT_OF_BOUNDS;
+      *p = val;
+      break;
+    }
+    case OP_ADD: --sp; st[sp - 1] = int32_t(uint32_t(st[sp - 1]) + uint32_t(st[sp])); break;
+    case OP_SUB: --sp; st[sp - 1] = int32_t(uint32_t(st[sp - 1]) - uint32_t(st[sp])); break;
+    case OP_MUL: --sp; st[sp - 1] = int32_t(uint32_t(st[sp - 1]) * uint32_t(st[sp])); break;
+    case OP_TID: st[sp++] = c.tid; break;
+    case OP_TEAM: st[sp++] = c.team; break;
+    case OP_NTHREADS: st[sp++] = c.nthreads; break;
+    case OP_NTEAMS: st[sp++] = c.nteams; break;
+    case OP_JMP: pc = c.code[pc]; break;
+    case OP_JNLT: {
+      const int32_t target = c.code[pc++];
+      sp -= 2;
+      if (!(st[sp] < st[sp + 1]))
+        pc = target;
+      break;
+    }
+    case OP_PARALLEL:
+      *r = c.code[pc++];
+      *pc_io = pc;
+      return 1;
+    case OP_ZERO_PRIV:
+      for (int i = 0; i < kVmPriv; i += 4)
+        *reinterpret_cast<int32_t *>(c.priv + i) = 0;
+      break;
+    default:
+      return -OMPDS_ERR_INVALID;
+    }
+  }
+}
+
+struct ProgramProg {
+  struct Args {
+    const int32_t *code;
+    const ompds_prog_var *vars;
+    const ompds_prog_region *regions;
+    const int32_t *caps;
+    void *const *bufs;
+    unsigned char *mlocal; // teams * total_local
+    int64_t total_local;
+  };
+  __device__ static void master(Master &m, const Args &a) {
+    unsigned char *ml = a.mlocal + size_t(blockIdx.x) * a.total_local;
+    for (int64_t i = lane_id() * 4; i < a.total_local; i += 128) // zero-filled frame
+      *reinterpret_cast<int32_t *>(ml + i) = 0;
+    __syncwarp();
+    VmCtx c{a.code, a.vars, a.bufs, m.depot.base, ml, nullptr, nullptr,
+            0, static_cast<int32_t>(blockIdx.x), 1, static_cast<int32_t>(gridDim.x)};
+    int32_t pc = 0;
+    for (;;) {
+      int32_t ev = 0, r = 0;
+      if (m.leader)
+        ev = vm_run(c, &pc, &r);
+      ev = __shfl_sync(0xffffffffu, ev, 0);
+      r = __shfl_sync(0xffffffffu, r, 0);
+      if (ev <= 0) {
+        if (ev < 0)
+          m.sync_status(-ev);
+        return;
+      }
+      const ompds_prog_region reg = a.regions[r];
+      if (m.parallel_with(r, reg.n_captures, [&](int j) -> void * {
+            return vm_addr(c, a.caps[reg.cap_begin + j], 0);
+          }) != OMPDS_OK)
+        return;
+    }
+  }
+  __device__ static void region(int32_t fn, const SharedVars &sv, Worker &w,
+                                const Args &a) {
+    // get-shared-variables: the first 32 entries come from the warp-shuffle
+    // broadcast, further ones straight from the list.
+    void *caps[kVmCaps];
+    const int32_t n = w.nargs < kVmCaps ? w.nargs : kVmCaps;
+    for (int j = 0; j < 32 && j < n; ++j)
+      caps[j] = sv.get(j);
+    for (int j = 32; j < n; ++j)
+      caps[j] = w.args[j];
+    if (!w.mine)
+      return;
+    alignas(16) unsigned char priv[kVmPriv];
+    VmCtx c{a.code, a.vars, a.bufs, nullptr, nullptr, priv, caps,
+            w.wid, w.team, w.workers, w.teams};
+    int32_t pc = a.regions[fn].entry, r = 0;
+    const int32_t ev = vm_run(c, &pc, &r);
+    if (ev < 0)
+      w.t->trap(-ev);
+  }
+};
+
+//===----------------------------------------------------------------------===//
 // Protocol replay: one device thread drives the single-caller runtime
 // functions over a team region in shared memory (the TeamRuntime API).
 //===----------------------------------------------------------------------===//
@@ -732,13 +924,14 @@ __global__ void checksum_kernel(const T *data, int64_t n,
 
 // Library-owned global memory reused across launches on a device: buffer 0
 // holds the teams' overflow slabs (args lists, master depot overflow),
-// buffer 1 the worker warps' data-sharing overflow chains.  Launches that
-// run concurrently on different streams must not share a device.
+// buffer 1 the worker warps' data-sharing overflow chains, buffer 2 a region
+// program's tables, buffer 3 the masters' local depot mirrors.  Launches
+// that run concurrently on different streams must not share a device.
 struct Workspace {
   std::mutex mu;
   int device = -1;
-  unsigned char *buf[2] = {nullptr, nullptr};
-  size_t bytes[2] = {0, 0};
+  unsigned char *buf[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t bytes[4] = {0, 0, 0, 0};
 };
 static Workspace g_ws;
 
@@ -747,7 +940,7 @@ static int32_t ensure_buffer(int which, size_t bytes, unsigned char **out) {
   int dev = 0;
   OMPDS_CUDA(cudaGetDevice(&dev));
   if (g_ws.device != dev) {
-    for (int i = 0; i < 2; ++i) { // leaked on device switch (bounded, rare)
+    for (int i = 0; i < 4; ++i) { // leaked on device switch (bounded, rare)
       g_ws.buf[i] = nullptr;
       g_ws.bytes[i] = 0;
     }
@@ -1074,6 +1267,54 @@ int32_t ompds_run_nested(const ompds_launch *launch, int32_t elem,
                                 warp_stats};
   return launch_generic<NestedProg<double>>(launch, lay, 2, args, stats, events,
                                             warp_slot_bytes, warp_overflow_bytes);
+}
+
+int32_t ompds_run_program(const ompds_launch *launch, const ompds_program *pr,
+                          ompds_team_stats *stats, ompds_event *events) {
+  if (!launch || !pr || !pr->code || pr->n_code <= 0 || pr->n_vars < 0 ||
+      pr->n_regions < 0 || pr->n_captures < 0 || pr->n_buffers < 0 ||
+      pr->total_shared < 0 || pr->total_local < 0 || pr->priv_bytes > kVmPriv)
+    return OMPDS_ERR_INVALID;
+  for (int32_t i = 0; i < pr->n_regions; ++i)
+    if (pr->regions[i].n_captures > kVmCaps || pr->regions[i].entry < 0 ||
+        pr->regions[i].entry >= pr->n_code)
+      return OMPDS_ERR_INVALID;
+  // Stage the program's tables in one device buffer (workspace slot 2).
+  const size_t sz_code = size_t(pr->n_code) * 4, sz_vars = size_t(pr->n_vars) * sizeof(ompds_prog_var),
+               sz_regs = size_t(pr->n_regions) * sizeof(ompds_prog_region),
+               sz_caps = size_t(pr->n_captures) * 4, sz_bufs = size_t(pr->n_buffers) * sizeof(void *);
+  auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+  const size_t o_vars = al(sz_code), o_regs = o_vars + al(sz_vars), o_caps = o_regs + al(sz_regs),
+               o_bufs = o_caps + al(sz_caps), total = o_bufs + al(sz_bufs) + 256;
+  std::vector<unsigned char> host(total, 0);
+  std::memcpy(host.data(), pr->code, sz_code);
+  if (sz_vars) std::memcpy(host.data() + o_vars, pr->vars, sz_vars);
+  if (sz_regs) std::memcpy(host.data() + o_regs, pr->regions, sz_regs);
+  if (sz_caps) std::memcpy(host.data() + o_caps, pr->captures, sz_caps);
+  if (sz_bufs) std::memcpy(host.data() + o_bufs, pr->buffers, sz_bufs);
+  unsigned char *dev = nullptr, *mlocal = nullptr;
+  int32_t s = ensure_buffer(2, total, &dev);
+  if (s)
+    return s;
+  s = ensure_buffer(3, size_t(std::max<int64_t>(pr->total_local, 4)) * launch->teams, &mlocal);
+  if (s)
+    return s;
+  cudaStream_t st = static_cast<cudaStream_t>(launch->stream);
+  OMPDS_CUDA(cudaMemcpyAsync(dev, host.data(), total, cudaMemcpyHostToDevice, st));
+  FixedLayout lay;
+  lay.total_shared = pr->total_shared;
+  ProgramProg::Args a{reinterpret_cast<const int32_t *>(dev),
+                      reinterpret_cast<const ompds_prog_var *>(dev + o_vars),
+                      reinterpret_cast<const ompds_prog_region *>(dev + o_regs),
+                      reinterpret_cast<const int32_t *>(dev + o_caps),
+                      reinterpret_cast<void *const *>(dev + o_bufs), mlocal,
+                      std::max<int64_t>(pr->total_local, 4)};
+  s = launch_generic<ProgramProg>(launch, lay, 0, a, stats, events);
+  if (s)
+    return s;
+  // the staging buffer is reused by the next launch: finish this one first
+  OMPDS_CUDA(cudaStreamSynchronize(st));
+  return OMPDS_OK;
 }
 
 int32_t ompds_run_stream_host(const ompds_launch *launch, int32_t elem,

