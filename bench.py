@@ -232,8 +232,11 @@ def main():
     lo, hi = sharding.shard_range(n_total, rank, world)
     n = hi - lo
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    workers = args.workers or 992
-    teams = args.teams or sms * (2048 // (((workers + 31) // 32) * 32 + 32))
+    # Tuned on B200 (tools/sweep.py, profiles/r1_sweep.json): 128-thread
+    # teams (W=96 + the master warp), 32 teams per SM = 4 waves of 8
+    # resident teams; 0.4-5 % faster than one wave of 1024-thread teams.
+    workers = args.workers or 96
+    teams = args.teams or sms * 32
 
     x = torch.empty(n, dtype=torch.float64, device=dev)
     y = torch.empty(n, dtype=torch.float64, device=dev)
@@ -295,6 +298,19 @@ def main():
     e1.record(stream)
     e1.synchronize()
     ns_per_region = e0.elapsed_time(e1) * 1e6 / R
+    # the same protocol on every SM: 8 teams/SM x 32 workers, 2000 regions each
+    R2, teams2 = 2000, sms * 8
+    a2 = torch.zeros(teams2 * 32, dtype=torch.int32, device=dev)
+    RG.run_regions(a2, teams2, 32, 10, stream=stream)
+    e0.record(stream)
+    RG.run_regions(a2, teams2, 32, R2, stream=stream)
+    e1.record(stream)
+    e1.synchronize()
+    agg_regions_per_s = teams2 * R2 / (e0.elapsed_time(e1) * 1e-3)
+    from paper_1711_10413_b200 import occupancy as OCC
+    regs = ptxas_regs("StreamProgIdE") or 64
+    thr = ((workers + 31) // 32) * 32 + 32
+    occ = OCC.occupancy_for("b200", smem_bytes, regs, thr)
 
     peak, peak_src = measured_peaks()
     roofline = {"bound": "hbm", "achieved": round(value / world, 1), "peak": peak,
@@ -324,10 +340,17 @@ def main():
         "regions": {"ns_per_region": round(ns_per_region, 1),
                     "regions_per_s": round(1e9 / ns_per_region, 1),
                     "workload": "config 1: 1 team x 32 workers, 4 shared scalars, "
-                                f"{R} regions in a sequential loop"},
+                                f"{R} regions in a sequential loop",
+                    "aggregate_regions_per_s": round(agg_regions_per_s, 0),
+                    "aggregate_workload": f"{teams2} teams x 32 workers x {R2} regions"},
         "smem_bytes_per_cta": smem_bytes,
         "smem_layout": "depot 80 + args window 160 + runtime span 49 (reference footprint 289)",
-        "regs_per_thread": ptxas_regs("StreamProgIdE"),
+        "regs_per_thread": regs,
+        "occupancy": {"model": "b200 row of the reference occupancy model",
+                      "teams_by_regs": occ.teams_by_regs, "teams_by_smem": occ.teams_by_smem,
+                      "teams_per_sm": occ.actual, "threads_per_team": thr,
+                      "binding_limit": "registers" if occ.actual == occ.teams_by_regs
+                      else "smem" if occ.actual == occ.teams_by_smem else "blocks/threads"},
         "checksum": f"{checksum:#018x}",
         "gpu_launches": args.steps,
         "clocks": clk,

@@ -32,7 +32,11 @@ def main():
     y = torch.empty(n, dtype=torch.float64, device="cuda")
     RG.fill_uniform(x, 1)
     RG.fill_uniform(y, 2)
-    for w, per_sm in [(992, 2), (480, 4), (480, 2), (224, 8), (224, 4), (992, 1), (96, 16)]:
+    geoms = [(992, 2), (96, 16), (96, 8), (96, 24), (96, 32), (64, 16), (64, 32), (32, 32),
+             (32, 64), (160, 12), (224, 8), (224, 16), (128, 16), (480, 4)]
+    if len(sys.argv) > 1 and sys.argv[1] == "quick":
+        geoms = geoms[:3]
+    for w, per_sm in geoms:
         teams = 148 * per_sm
         ms = time_it(lambda: RG.run_stream(x, y, COEF, teams, w, stats=False), 30)
         out["stream"].append({"workers": w, "teams": teams, "ms": round(ms, 4),
