@@ -356,6 +356,11 @@ __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
   const uint32_t n = __popc(ballot);
   if (n) {
     const uint32_t leader = __ffs(ballot) - 1;
+    if (t.events == nullptr) { // fast path: one fire-and-forget shared atomic
+      if (lane == leader)
+        atomicAdd(&t.active(), static_cast<int32_t>(n));
+      return f;
+    }
     int64_t ev = -1;
     if (lane == leader) {
       atomicAdd(&t.active(), static_cast<int32_t>(n));
@@ -387,7 +392,8 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t, bool mine) {
     if (old == static_cast<int32_t>(n))
       retire_last(t); // this warp retired the region's last participant
   }
-  __syncwarp();
+  // no __syncwarp: the join barrier that follows orders the leader's
+  // shared-memory updates for every participant
 }
 
 //===----------------------------------------------------------------------===//

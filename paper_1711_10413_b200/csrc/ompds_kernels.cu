@@ -125,13 +125,24 @@ struct Master {
   __device__ __forceinline__ int32_t parallel_with(int32_t fn, int32_t nargs,
                                                    AddrOf addr_of) {
     void **list = nullptr;
-    int32_t s = 0;
-    if (leader)
-      s = prepare_parallel(t, kMaster, fn, nargs, &list);
-    if (sync_status(s))
+    unsigned long long packed = 0;
+    if (leader) {
+      const int32_t s = prepare_parallel(t, kMaster, fn, nargs, &list);
+      // one shuffle carries the list, or the trap code with bit 63 set
+      packed = s ? (static_cast<unsigned long long>(s) | (1ull << 63))
+                 : reinterpret_cast<unsigned long long>(list);
+    }
+    packed = __shfl_sync(0xffffffffu, packed, 0);
+    if (packed >> 63) {
+      const int32_t s = static_cast<int32_t>(packed & 0xffffffffu);
+      if (!trap) {
+        trap = s;
+        if (leader)
+          t.trap(s);
+      }
       return s;
-    list = reinterpret_cast<void **>(__shfl_sync(
-        0xffffffffu, reinterpret_cast<unsigned long long>(list), 0));
+    }
+    list = reinterpret_cast<void **>(packed);
     // The reserved warp publishes the pointer list lane-parallel (one
     // coalesced store per 32 entries) instead of nargs scalar stores.
     for (int j = lane_id(); j < nargs; j += 32)

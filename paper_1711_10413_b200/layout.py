@@ -126,6 +126,48 @@ def frame_block(group: FrameGroup, lay: DepotLayout) -> str:
     return "\n".join(out) + "\n"
 
 
+def parse_frame_blocks(text: str):
+    """Parses every ``frame @root members [...] { ... }`` block of a ``.sir``
+    module (IRParser.cpp:689-795) into (FrameGroup, DepotLayout) pairs."""
+    import re
+    out = []
+    lines = text.splitlines()
+    i = 0
+    head = re.compile(r"^frame @(\S+) members \[(.*)\] \{$")
+    slot = re.compile(r"^  slot (\d+): offset (\d+), size (\d+), align (\d+), (shared|local)(.*)$")
+    tot = re.compile(r"^  total (\d+)(, mirrored)?$")
+    while i < len(lines):
+        m = head.match(lines[i])
+        if not m:
+            i += 1
+            continue
+        members = [x.strip().lstrip("@") for x in m.group(2).split(",") if x.strip()]
+        slots = []
+        i += 1
+        while True:
+            sm = slot.match(lines[i])
+            if sm:
+                if int(sm.group(1)) != len(slots):
+                    raise ValueError(f"frame @{m.group(1)}: slot {sm.group(1)} out of order")
+                owners = [o.strip().lstrip("%") for o in sm.group(6).split(",") if o.strip()]
+                slots.append(DepotSlot(int(sm.group(2)), int(sm.group(3)), int(sm.group(4)),
+                                       sm.group(5) == "shared", owners))
+                i += 1
+                continue
+            tm = tot.match(lines[i])
+            if not tm:
+                raise ValueError(f"frame @{m.group(1)}: malformed line {lines[i]!r}")
+            total = int(tm.group(1))
+            if lines[i + 1] != "}":
+                raise ValueError(f"frame @{m.group(1)}: missing closing brace")
+            i += 2
+            break
+        ov = next((k for k, s in enumerate(slots) if s.shared and len(s.owners) > 1), -1)
+        out.append((FrameGroup(m.group(1), members),
+                    DepotLayout(slots, total, total, bool(tm.group(2)), ov)))
+    return out
+
+
 def manifest_depot(lay: DepotLayout, prealloc_entries: int = L.DEFAULT_PREALLOC_ENTRIES) -> dict:
     """The depot part of the reference manifest (Compiler.cpp:112-155)."""
     return {

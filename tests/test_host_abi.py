@@ -103,6 +103,42 @@ def test_frame_block_and_manifest_render_like_the_reference():
         assert m[k] == gm[k], k
 
 
+@pytest.mark.parametrize("stem", ["shared_scalar", "two_regions", "seq_only"])
+def test_frame_blocks_byte_equal_reference_golden_sir(stem):
+    """All frame blocks of the reference's golden .sir modules
+    (proj/tests/golden/*.sir, IRTests.cpp:169-178) rendered from our layouts."""
+    path = f"/root/reference/proj/tests/golden/{stem}.sir"
+    if not os.path.exists(path):
+        pytest.skip("reference not mounted")
+    p = next(x for x in G.load("corpus") if x["stem"] == stem)
+    fv = [layout.FrameVar(v["name"], v["bytes"], v["group"], v["func"], v["escapes"], v["pinned"],
+                          v["def_pos"], v["first"], v["last"]) for v in p["frame_vars"]]
+    lays = layout.build_layouts(fv, len(p["layouts"]))
+    text = "".join("\n" + layout.frame_block(layout.FrameGroup(r, m), l)
+                   for (r, m), l in zip(G.frame_groups(p), lays))
+    golden = open(path).read()
+    assert golden.endswith(text)
+    assert golden[: len(golden) - len(text)].rstrip().endswith("}")  # last function body
+    # and the parser reads the reference's text back into the same layouts
+    parsed = layout.parse_frame_blocks(golden)
+    assert [(g.root, g.members) for g, _ in parsed] == [(r, m) for r, m in G.frame_groups(p)]
+    assert [l for _, l in parsed] == lays
+
+
+def test_frame_block_round_trip_over_all_programs():
+    for p in G.programs():
+        fv = [layout.FrameVar(v["name"], v["bytes"], v["group"], v["func"], v["escapes"],
+                              v["pinned"], v["def_pos"], v["first"], v["last"])
+              for v in p["frame_vars"]]
+        for pipe in ("default", "bad_order"):
+            lays = layout.build_layouts(fv, len(p["layouts"]), pipe)
+            groups = [layout.FrameGroup(r, m) for r, m in G.frame_groups(p)]
+            text = "".join(layout.frame_block(g, l) for g, l in zip(groups, lays))
+            back = layout.parse_frame_blocks(text)
+            assert [g for g, _ in back] == groups
+            assert [l for _, l in back] == lays, p["stem"]
+
+
 def test_audit_flags_the_bad_order_overlap():
     p = next(x for x in G.load("corpus") if x["stem"] == "coloring_demo")
     fv = [layout.FrameVar(v["name"], v["bytes"], v["group"], v["func"], v["escapes"], v["pinned"],

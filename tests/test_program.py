@@ -163,6 +163,21 @@ def test_lowering_reproduces_reference_outputs_on_cpu():
     assert n > 150
 
 
+def test_sharing_analysis_matches_reference_detection():
+    """The captures the lowering derives from the AST are exactly the kernel
+    allocas the reference's escape detection marks shared
+    (LoweringPasses.cpp:107-139 on the post-codegen module)."""
+    n = 0
+    for p in programs():
+        t, w, _ = launches(p)[0] if launches(p) else (1, 8, None)
+        prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], t, w)
+        caps = {prog.var_names[v] for r in prog.regions for v in r.captures}
+        want = set(p["detected_shared"].get(p["kernel"], []))
+        assert caps == want, p["stem"]
+        n += 1
+    assert n > 100
+
+
 def test_captures_follow_the_reference_order():
     p = next(x for x in G.load("corpus") if x["stem"] == "mixed_captures")
     prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], 4, 96)

@@ -36,6 +36,8 @@ def main():
              (32, 64), (160, 12), (224, 8), (224, 16), (128, 16), (480, 4)]
     if len(sys.argv) > 1 and sys.argv[1] == "quick":
         geoms = geoms[:3]
+    if len(sys.argv) > 1 and sys.argv[1] == "regions":
+        geoms = []
     for w, per_sm in geoms:
         teams = 148 * per_sm
         ms = time_it(lambda: RG.run_stream(x, y, COEF, teams, w, stats=False), 30)
