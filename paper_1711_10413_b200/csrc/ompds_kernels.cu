@@ -42,6 +42,10 @@ static int32_t cuda_fail(cudaError_t e, const char *what) {
 // Launch parameters shared by every generic-mode kernel.
 //===----------------------------------------------------------------------===//
 
+#ifndef OMPDS_GENERIC_LB
+#define OMPDS_GENERIC_LB __launch_bounds__(1024, 1)
+#endif
+
 constexpr int kMaxCaptures = 32;
 
 struct TeamParams {
@@ -61,6 +65,43 @@ struct TeamParams {
   int64_t warp_slot_bytes;       // per-warp data-sharing slot in smem
   unsigned char *warp_ovf;       // teams * worker_warps * warp_ovf_bytes
   int64_t warp_ovf_bytes;
+};
+
+// Depot accessors for the master's sequential code (see Master::with_depot).
+struct SmemDepot {
+  uint32_t base;        // shared-window address of the depot frame
+  unsigned char *gbase; // the same frame as a generic pointer
+  __device__ __forceinline__ void *ptr(int64_t off) const { return gbase + off; }
+  template <class T> __device__ __forceinline__ T ld(int64_t off) const {
+    static_assert(sizeof(T) == 4 || sizeof(T) == 8, "4/8-byte slots");
+    if constexpr (sizeof(T) == 4) {
+      uint32_t v;
+      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(base + uint32_t(off)) : "memory");
+      return __builtin_bit_cast(T, v);
+    } else {
+      unsigned long long v;
+      asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(base + uint32_t(off)) : "memory");
+      return __builtin_bit_cast(T, v);
+    }
+  }
+  template <class T> __device__ __forceinline__ void st(int64_t off, T x) const {
+    if constexpr (sizeof(T) == 4)
+      asm volatile("st.shared.b32 [%0], %1;" ::"r"(base + uint32_t(off)),
+                   "r"(__builtin_bit_cast(uint32_t, x)) : "memory");
+    else
+      asm volatile("st.shared.b64 [%0], %1;" ::"r"(base + uint32_t(off)),
+                   "l"(__builtin_bit_cast(unsigned long long, x)) : "memory");
+  }
+};
+struct GlobalDepot {
+  unsigned char *gbase;
+  __device__ __forceinline__ void *ptr(int64_t off) const { return gbase + off; }
+  template <class T> __device__ __forceinline__ T ld(int64_t off) const {
+    return *reinterpret_cast<const volatile T *>(gbase + off);
+  }
+  template <class T> __device__ __forceinline__ void st(int64_t off, T x) const {
+    *reinterpret_cast<volatile T *>(gbase + off) = x;
+  }
 };
 
 // Master-warp view of the sequential region.  Every lane runs it; lane 0
@@ -112,6 +153,17 @@ struct Master {
 
   __device__ __forceinline__ unsigned char *cap(int j) const {
     return depot.base + p->cap_off[j];
+  }
+
+  // Runs the sequential code `f(depot)` with a depot accessor that issues
+  // shared-memory instructions (LDS/STS, 32-bit addresses) when the depot
+  // frame is in the smem slot, generic ones when it is on the global chain.
+  template <class F> __device__ __forceinline__ void with_depot(F &&f) {
+    if (depot.in_smem)
+      f(SmemDepot{static_cast<uint32_t>(__cvta_generic_to_shared(depot.base)),
+                  depot.base});
+    else
+      f(GlobalDepot{depot.base});
   }
 
   // prepare_parallel + publish &capture_j into the list + release + join.
@@ -199,7 +251,7 @@ struct Worker {
 };
 
 template <class Prog>
-__global__ void __launch_bounds__(1024, 1)
+__global__ void OMPDS_GENERIC_LB
     generic_mode_kernel(const __grid_constant__ TeamParams p,
                         const __grid_constant__ typename Prog::Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -243,15 +295,17 @@ __global__ void __launch_bounds__(1024, 1)
     for (;;) {
       bar_sync(kBarHandoff, team_threads); // await.work
       Fetch f = begin_parallel_warp(t, w.mine);
-      if (f.fn < 0 && f.status == OMPDS_OK)
-        break; // termination sentinel
-      if (f.status == OMPDS_OK) {
-        w.args = f.args;
-        w.nargs = f.nargs;
-        SharedVars sv = get_shared_variables(f.args, f.nargs);
-        Prog::region(f.fn, sv, w, a);
-        end_parallel_warp(t, w.mine);
+      if (f.fn < 0) {
+        if (f.status == OMPDS_OK)
+          break; // termination sentinel (wf == null)
+        bar_sync(kBarHandoff, team_threads); // trapped fetch: skip the region
+        continue;
       }
+      w.args = f.args;
+      w.nargs = f.nargs;
+      SharedVars sv = get_shared_variables(f.args, f.nargs);
+      Prog::region(f.fn, sv, w, a);
+      end_parallel_warp(t, w.mine);
       bar_sync(kBarHandoff, team_threads); // barrier.parallel (join)
     }
   } else {
@@ -276,27 +330,31 @@ template <class T> struct RegionsProg {
     int32_t regions;
   };
   __device__ static void master(Master &m, const Args &a) {
-    if (m.leader) {
-      *reinterpret_cast<int32_t *>(m.cap(0)) = 1;
-      *reinterpret_cast<int32_t *>(m.cap(1)) = 2;
-      *reinterpret_cast<T *>(m.cap(2)) = T(3);
-      *reinterpret_cast<T *>(m.cap(3)) = T(4);
-    }
-    int32_t *r = m.p->aux_off >= 0
-                     ? reinterpret_cast<int32_t *>(m.depot.base + m.p->aux_off)
-                     : nullptr;
-    // lane j < 4 keeps &c_{j+1}: publishing the list is one store per lane
-    void *mine = lane_id() < 4 ? static_cast<void *>(m.cap(lane_id())) : nullptr;
-    for (int32_t i = 0; i < a.regions; ++i) {
-      if (m.leader && r)
-        *r = i;
-      if (m.parallel_with(0, 4, [mine](int) { return mine; }) != OMPDS_OK)
-        return;
-      if (m.leader) // sequential code between regions: c4 += 1
-        *reinterpret_cast<T *>(m.cap(3)) += T(1);
-    }
-    if (m.leader && r)
-      *r = a.regions;
+    m.with_depot([&](const auto &d) {
+      int64_t off[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        off[j] = m.p->cap_off[j];
+      const int64_t roff = m.p->aux_off;
+      if (m.leader) {
+        d.template st<int32_t>(off[0], 1);
+        d.template st<int32_t>(off[1], 2);
+        d.template st<T>(off[2], T(3));
+        d.template st<T>(off[3], T(4));
+      }
+      // lane j < 4 keeps &c_{j+1}: publishing the list is one store per lane
+      void *mine = lane_id() < 4 ? d.ptr(m.p->cap_off[lane_id()]) : nullptr;
+      for (int32_t i = 0; i < a.regions; ++i) {
+        if (m.leader && roff >= 0)
+          d.template st<int32_t>(roff, i);
+        if (m.parallel_with(0, 4, [mine](int) { return mine; }) != OMPDS_OK)
+          return;
+        if (m.leader) // sequential code between regions: c4 += 1
+          d.template st<T>(off[3], d.template ld<T>(off[3]) + T(1));
+      }
+      if (m.leader && roff >= 0)
+        d.template st<int32_t>(roff, a.regions);
+    });
   }
   __device__ static void region(int32_t, const SharedVars &sv, const Worker &w,
                                 const Args &a) {
