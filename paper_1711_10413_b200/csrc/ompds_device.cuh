@@ -82,9 +82,11 @@ __device__ __forceinline__ void bar_sync(uint32_t id, uint32_t count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+// Not volatile: the lane id is invariant, so the compiler may hoist the
+// (long-latency) S2R out of the region loops.
 __device__ __forceinline__ uint32_t lane_id() {
   uint32_t l;
-  asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+  asm("mov.u32 %0, %%laneid;" : "=r"(l));
   return l;
 }
 

@@ -183,9 +183,104 @@ struct ProbeProg {
     RegionsProg<int32_t>::region(fn, sv, w, ra);
   }
 };
+// worker side replaced by the ladder's body
+struct ProbeProgW {
+  using Args = ProbeProg::Args;
+  __device__ static void master(Master &m, const Args &a) { ProbeProg::master(m, a); }
+  __device__ static void region(int32_t, const SharedVars &sv, Worker &w, const Args &a) {
+    int32_t sum = shared_value<int32_t>(sv, 0) + shared_value<int32_t>(sv, 1) +
+                  shared_value<int32_t>(sv, 2) + shared_value<int32_t>(sv, 3);
+    a.a[threadIdx.x] += sum;
+  }
+};
+// master side replaced by the ladder's loop
+struct ProbeProgM {
+  using Args = ProbeProg::Args;
+  __device__ static void loop(Master &m, int R) {
+    const bool leader = m.leader;
+    unsigned char *d = m.t.region;
+    void *mine = (threadIdx.x & 31) < 4 ? d + 8 * (threadIdx.x & 31) : nullptr;
+    for (int r = 0; r < R; ++r) {
+      void **list = nullptr;
+      unsigned long long packed = 0;
+      if (leader) {
+        int32_t s = prepare_parallel(m.t, kMaster, 0, 4, &list);
+        packed = s ? (1ull << 63) : reinterpret_cast<unsigned long long>(list);
+      }
+      packed = __shfl_sync(0xffffffffu, packed, 0);
+      list = reinterpret_cast<void **>(packed);
+      if ((threadIdx.x & 31) < 4)
+        list[threadIdx.x & 31] = mine;
+      bar_sync(kBarHandoff, m.team_threads);
+      bar_sync(kBarHandoff, m.team_threads);
+      if (leader) {
+        *reinterpret_cast<int32_t *>(d + 24) += 1;
+        *reinterpret_cast<int32_t *>(d + 32) = r;
+      }
+    }
+  }
+  __device__ static void master(Master &m, const Args &a) {
+    loop(m, 64);
+    long long t0 = clock64();
+    loop(m, a.regions);
+    long long t1 = clock64();
+    if (m.leader)
+      *a.cycles = t1 - t0;
+  }
+  __device__ static void region(int32_t fn, const SharedVars &sv, Worker &w, const Args &a) {
+    ProbeProg::region(fn, sv, w, a);
+  }
+};
+// ladder loop, but the handoff through Master::parallel_with
+struct ProbeProgPW {
+  using Args = ProbeProg::Args;
+  __device__ static void loop(Master &m, int R) {
+    const bool leader = m.leader;
+    unsigned char *d = m.t.region;
+    void *mine = (threadIdx.x & 31) < 4 ? d + 8 * (threadIdx.x & 31) : nullptr;
+    for (int r = 0; r < R; ++r) {
+      if (m.parallel_with(0, 4, [mine](int) { return mine; }) != OMPDS_OK)
+        return;
+      if (leader) {
+        *reinterpret_cast<int32_t *>(d + 24) += 1;
+        *reinterpret_cast<int32_t *>(d + 32) = r;
+      }
+    }
+  }
+  __device__ static void master(Master &m, const Args &a) {
+    loop(m, 64);
+    long long t0 = clock64();
+    loop(m, a.regions);
+    long long t1 = clock64();
+    if (m.leader)
+      *a.cycles = t1 - t0;
+  }
+  __device__ static void region(int32_t fn, const SharedVars &sv, Worker &w, const Args &a) {
+    ProbeProg::region(fn, sv, w, a);
+  }
+};
 } // namespace ompds
 
+template <class P> void product_variant(const char *name) {
+  int32_t *a;
+  long long *c;
+  cudaMalloc(&a, 128);
+  cudaMalloc(&c, 8);
+  const int R = 20000;
+  ompds_launch l{1, 32, 20, 0, -1, 0, 0, nullptr};
+  FixedLayout lay;
+  build_fixed_layout({4, 4, 4, 4}, 4, &lay);
+  launch_generic<P>(&l, lay, 4, typename P::Args{a, R, c}, nullptr, nullptr);
+  cudaDeviceSynchronize();
+  long long h = 0;
+  cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+  printf("%s: %7.1f cycles/region\n", name, double(h) / R);
+}
+
 int main_product() {
+  product_variant<ProbeProgW>("product master + ladder worker body");
+  product_variant<ProbeProgM>("ladder master loop + product worker");
+  product_variant<ProbeProgPW>("ladder master loop via Master::parallel_with");
   int32_t *a;
   long long *c;
   cudaMalloc(&a, 128);
