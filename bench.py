@@ -307,12 +307,16 @@ def main():
     e1.record(stream)
     e1.synchronize()
     agg_regions_per_s = teams2 * R2 / (e0.elapsed_time(e1) * 1e-3)
+    configs = other_configs(RG, dev, stream, sms) if rank == 0 else {}
     from paper_1711_10413_b200 import occupancy as OCC
     regs = ptxas_regs("StreamProgIdE") or 64
     thr = ((workers + 31) // 32) * 32 + 32
     occ = OCC.occupancy_for("b200", smem_bytes, regs, thr)
 
     peak, peak_src = measured_peaks()
+    if "config2_shared_array" in configs:
+        c2 = configs["config2_shared_array"]
+        c2["roofline_frac"] = round(c2["GBps"] / peak, 4)
     roofline = {"bound": "hbm", "achieved": round(value / world, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(value / world / peak, 4), "traffic": None,
                 "peak_source": peak_src,
@@ -352,6 +356,7 @@ def main():
                       "binding_limit": "registers" if occ.actual == occ.teams_by_regs
                       else "smem" if occ.actual == occ.teams_by_smem else "blocks/threads"},
         "checksum": f"{checksum:#018x}",
+        "configs": configs,
         "gpu_launches": args.steps,
         "clocks": clk,
     }
@@ -364,6 +369,60 @@ def main():
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line))
+
+
+def other_configs(RG, dev, stream, sms):
+    """BASELINE configs 2 and 3 beside the headline (each timed with CUDA
+    events on the launching stream; config 2 flushes L2 between launches)."""
+    import torch
+    out = {}
+    # config 2: d[256] fp64 staged by TMA into the depot, parallel-for a[i] += d[i & 255]
+    n2 = 1 << 24
+    a = torch.zeros(n2, dtype=torch.float64, device=dev)
+    d_init = torch.arange(256, dtype=torch.float64, device=dev) * 3 + 1
+    # L2 "flush" by READING 256 MB: evicts a[] without leaving dirty lines
+    # whose write-back would be charged to the timed kernel
+    flush = torch.ones(64 << 20, dtype=torch.int32, device=dev)
+    t2, w2 = sms * 2, 480  # tools/sweep.py config2: one wave of 512-thread teams
+    times = []
+    st = RG.run_shared_array(a, t2, w2, d_init=d_init, stream=stream).team_stats()[0]
+    for _ in range(10):
+        flush.sum()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            stream.wait_stream(torch.cuda.current_stream())
+            e0.record(stream)
+            RG.run_shared_array(a, t2, w2, d_init=d_init, stream=stream)
+            e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = statistics.median(times)
+    out["config2_shared_array"] = {
+        "elements": n2, "teams": t2, "workers": w2, "ms": round(ms, 4),
+        "GBps": round(16 * n2 / ms / 1e6, 1), "bytes_per_element": 16,
+        "smem_bytes_per_cta": st.smem_bytes, "depot_in_smem": st.depot_in_smem,
+        "staging": "cp.async.bulk (TMA) of d[256] into the depot slot",
+        "roofline_frac": None,
+        "l2": "evicted before every launch by reading a 256 MB buffer"}
+    del a, flush
+    # config 3: nested regions (depth 3) on per-warp data-sharing stacks
+    R = 2000
+    for teams in (1, sms * 8):
+        a3 = torch.zeros(teams * 96, dtype=torch.float64, device=dev)
+        RG.run_nested(a3, teams, 96, 10, stream=stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, stacks = RG.run_nested(a3, teams, 96, R, stream=stream)
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        key = "config3_nested_1team" if teams == 1 else "config3_nested_full"
+        out[key] = {"teams": teams, "workers": 96, "regions": R,
+                    "ns_per_region": round(ms * 1e6 / R, 1),
+                    "aggregate_regions_per_s": round(teams * R / (ms * 1e-3), 0),
+                    "stack_depth": stacks[0][0].max_depth,
+                    "frames_in_smem": stacks[0][0].frame_in_smem}
+    return out
 
 
 def e2e(args, teams, workers, n, dev):

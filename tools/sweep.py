@@ -25,7 +25,32 @@ def time_it(fn, reps):
     return e0.elapsed_time(e1) / reps
 
 
+def config2():
+    n2 = 1 << 24
+    a = torch.zeros(n2, dtype=torch.float64, device="cuda")
+    d = torch.arange(256, dtype=torch.float64, device="cuda") * 3 + 1
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for w, per_sm in [(96, 32), (96, 8), (96, 4), (224, 4), (480, 2), (992, 1), (992, 2),
+                      (224, 8)]:
+        teams = 148 * per_sm
+        ts = []
+        for _ in range(8):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            RG.run_shared_array(a, teams, w, d_init=d, stats=False) if False else \
+                RG.run_shared_array(a, teams, w, d_init=d)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = sorted(ts)[len(ts) // 2]
+        print({"config2_workers": w, "teams": teams, "ms": round(ms, 4),
+               "GBps": round(16 * n2 / ms / 1e6, 1)}, flush=True)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "config2":
+        return config2()
     out = {"stream": [], "regions": []}
     n = 1 << 28
     x = torch.empty(n, dtype=torch.float64, device="cuda")
