@@ -78,8 +78,12 @@ __host__ __device__ constexpr int64_t team_region_bytes(int64_t depot,
 // Low-level primitives
 //===----------------------------------------------------------------------===//
 
+// Named barrier.  The non-.aligned form: each thread arrives individually,
+// so a warp whose lanes diverged just before (the master lane's sequential
+// code, lane-parallel list stores) is still correct (compute-sanitizer
+// synccheck flags the .aligned `bar.sync` there).
 __device__ __forceinline__ void bar_sync(uint32_t id, uint32_t count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 // Not volatile: the lane id is invariant, so the compiler may hoist the
@@ -114,7 +118,12 @@ struct TeamCtx {
     return *reinterpret_cast<T *>(rt + off);
   }
   __device__ __forceinline__ uint8_t &phase() const { return at<uint8_t>(Rt::kPhase); }
-  __device__ __forceinline__ int32_t &active() const { return at<int32_t>(Rt::kActive); }
+  // The 32-bit word at kActive: low 16 bits = Active (fetched - retired),
+  // high 16 bits = participants retired from the staged region (warp path).
+  __device__ __forceinline__ uint32_t &active_word() const { return at<uint32_t>(Rt::kActive); }
+  __device__ __forceinline__ int32_t active() const {
+    return static_cast<int32_t>(active_word() & 0xffffu);
+  }
   __device__ __forceinline__ void *&args() const { return at<void *>(Rt::kArgs); }
   __device__ __forceinline__ int32_t &work_fn() const { return at<int32_t>(Rt::kWorkFn); }
   __device__ __forceinline__ int32_t &nargs() const { return at<int32_t>(Rt::kNArgs); }
@@ -272,7 +281,7 @@ __device__ inline int32_t kernel_parallel(const TeamCtx &t, int role,
   *fn = t.work_fn();
   *args = static_cast<void **>(t.args());
   *participate = true;
-  t.active() += 1;
+  t.active_word() += 1;
   t.log(OMPDS_EV_FETCH, *fn, 0, 0);
   return OMPDS_OK;
 }
@@ -287,6 +296,7 @@ __device__ __forceinline__ void retire_last(const TeamCtx &t) {
   t.work_fn() = -1;
   t.args() = nullptr;
   t.nargs() = 0;
+  t.active_word() = 0;
   t.phase() = kIdle;
 }
 
@@ -297,7 +307,8 @@ __device__ inline int32_t end_parallel(const TeamCtx &t, int role) {
     return OMPDS_TRAP_END_FROM_MASTER;
   if (t.phase() != kStaged || t.active() <= 0)
     return OMPDS_TRAP_END_NOT_ACTIVE;
-  int32_t rem = --t.active();
+  t.active_word() -= 1;
+  const int32_t rem = t.active();
   t.log(OMPDS_EV_RETIRE, -1, rem, 0);
   if (rem == 0)
     retire_last(t);
@@ -360,12 +371,12 @@ __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
     const uint32_t leader = __ffs(ballot) - 1;
     if (t.events == nullptr) { // fast path: one fire-and-forget shared atomic
       if (lane == leader)
-        atomicAdd(&t.active(), static_cast<int32_t>(n));
+        atomicAdd(&t.active_word(), n);
       return f;
     }
     int64_t ev = -1;
     if (lane == leader) {
-      atomicAdd(&t.active(), static_cast<int32_t>(n));
+      atomicAdd(&t.active_word(), n);
       ev = t.log_reserve(n);
     }
     ev = __shfl_sync(0xffffffffu, ev, leader);
@@ -377,6 +388,11 @@ __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
 }
 
 // All 32 lanes of a worker warp call this when the region body is done.
+// On the GPU a fast warp can retire before a slow warp has fetched, so
+// "Active dropped to 0" would be premature; the last participant is instead
+// the one whose retirement brings the region's retired count to W (every
+// worker participates in every staged region, Codegen.cpp:403-513).  Under
+// the reference's schedule (all fetches before any retire) both rules agree.
 __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t, bool mine) {
   const uint32_t ballot = __ballot_sync(0xffffffffu, mine);
   const uint32_t n = __popc(ballot);
@@ -385,13 +401,24 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t, bool mine) {
   const uint32_t lane = lane_id();
   const uint32_t leader = __ffs(ballot) - 1;
   if (lane == leader) {
-    int32_t old = atomicSub(&t.active(), static_cast<int32_t>(n));
+    // retired += n (high half), Active -= n (low half; >= n: our own fetch).
+    // acq_rel at CTA scope: every participant's reads of the staged region
+    // happen-before the last retiree's bookkeeping writes (retire_last).
+    uint32_t old;
+    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
+                 : "=r"(old)
+                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(&t.active_word()))),
+                   "r"((n << 16) - n)
+                 : "memory");
+    const uint32_t retired = (old >> 16) + n;
+    const uint32_t w = static_cast<uint32_t>(t.at<int32_t>(Rt::kWorkers));
     if (t.events) {
       int64_t ev = t.log_reserve(n);
       for (uint32_t k = 0; k < n; ++k)
-        t.log_at(ev + k, OMPDS_EV_RETIRE, -1, old - 1 - int32_t(k), 0);
+        t.log_at(ev + k, OMPDS_EV_RETIRE, -1,
+                 int64_t(w) - int64_t((old >> 16) + k + 1), 0);
     }
-    if (old == static_cast<int32_t>(n))
+    if (retired == w)
       retire_last(t); // this warp retired the region's last participant
   }
   // no __syncwarp: the join barrier that follows orders the leader's

@@ -98,7 +98,7 @@ __global__ void ladder(int32_t *a, int R, long long *cycles, const __grid_consta
       bar_sync(kBarHandoff, nthr);
       bar_sync(kBarHandoff, nthr);
       if (V < 4 && V >= 1 && leader) // no end_parallel: reset by hand
-        retire_last(t), t.active() = 0;
+        retire_last(t);
       if (V >= 5 && leader) {
         *reinterpret_cast<int32_t *>(d + 24) += 1;
         *reinterpret_cast<int32_t *>(d + 32) = r;

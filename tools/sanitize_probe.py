@@ -1,0 +1,49 @@
+#!/usr/bin/env python
+"""Small invocation of every generic-mode kernel, for compute-sanitizer
+(memcheck / racecheck / synccheck / initcheck) runs on the GPU box:
+
+    compute-sanitizer --tool racecheck python tools/sanitize_probe.py
+"""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+sys.path.insert(0, "tests")
+from paper_1711_10413_b200 import regions as RG  # noqa: E402
+
+
+def main():
+    dev = "cuda"
+    a = torch.zeros(3 * 40, dtype=torch.int32, device=dev)
+    RG.run_regions(a, 3, 40, 3, max_events=256)
+    a = torch.zeros(2 * 40, dtype=torch.float64, device=dev)
+    RG.run_regions(a, 2, 40, 1)
+    for cap in (-1, 0):
+        s = torch.zeros(4099, dtype=torch.float64, device=dev)
+        RG.run_shared_array(s, 4, 64, d_init=torch.arange(256, dtype=torch.float64,
+                                                          device=dev), depot_capacity=cap)
+    RG.run_shared_array(torch.zeros(1000, dtype=torch.int32, device=dev), 2, 33)
+    x = torch.ones(5003, dtype=torch.float64, device=dev)
+    y = torch.ones(5003, dtype=torch.float64, device=dev)
+    RG.run_stream(x, y, [k / 8 for k in range(1, 9)], 4, 96, max_events=512)
+    RG.run_stream(x, y, [k / 8 for k in range(1, 9)], 4, 96, prealloc_entries=2)
+    for slot in (2048, 0):
+        n = torch.zeros(2 * 72, dtype=torch.float64, device=dev)
+        RG.run_nested(n, 2, 72, 2, warp_slot_bytes=slot)
+    import golden_util as G
+    from paper_1711_10413_b200 import program as PG
+    from test_program import our_layouts, launches
+    for stem in ("shared_scalar", "scalars_32", "two_regions", "private_inner"):
+        p = next(x for x in G.load("corpus") if x["stem"] == stem)
+        t, w, _ = launches(p)[0]
+        prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], t, w)
+        bufs = [torch.full((sz,), init, dtype=torch.int32, device=dev)
+                for _, sz, init in prog.buffers]
+        PG.run_program(prog, bufs)
+    torch.cuda.synchronize()
+    print("sanitize probe done")
+
+
+if __name__ == "__main__":
+    main()
