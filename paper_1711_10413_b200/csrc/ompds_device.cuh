@@ -78,12 +78,35 @@ __host__ __device__ constexpr int64_t team_region_bytes(int64_t depot,
 // Low-level primitives
 //===----------------------------------------------------------------------===//
 
-// Named barrier.  The non-.aligned form: each thread arrives individually,
-// so a warp whose lanes diverged just before (the master lane's sequential
-// code, lane-parallel list stores) is still correct (compute-sanitizer
-// synccheck flags the .aligned `bar.sync` there).
+// Named barrier.  Default (0): the non-.aligned `barrier.sync` -- each
+// thread arrives individually, so master and worker warps may reach the
+// handoff barrier from different instructions and after divergent code.
+// `.aligned` (`bar.sync`) requires every participating thread of the CTA to
+// execute the same instruction; inlined at the master's and the workers'
+// different call sites that is undefined behaviour, and compute-sanitizer
+// synccheck reports it (mode 1, measured ~50 cycles/region faster).  Mode 2
+// keeps `.aligned` legal with one out-of-line barrier instruction, but the
+// call costs more than the non-aligned form saves (tools/latency_ladder.cu).
+#ifndef OMPDS_BAR_ALIGNED
+#define OMPDS_BAR_ALIGNED 0
+#endif
+#if OMPDS_BAR_ALIGNED == 2
+// One out-of-line copy: master and worker warps execute the SAME barrier
+// instruction, as .aligned requires of every participating thread.
+__device__ __noinline__ void bar_sync_aligned(uint32_t id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+#endif
 __device__ __forceinline__ void bar_sync(uint32_t id, uint32_t count) {
+#if OMPDS_BAR_ALIGNED == 2
+  __syncwarp();
+  bar_sync_aligned(id, count);
+#elif OMPDS_BAR_ALIGNED
+  __syncwarp();
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+#else
   asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+#endif
 }
 
 // Not volatile: the lane id is invariant, so the compiler may hoist the
@@ -405,11 +428,15 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t, bool mine) {
     // acq_rel at CTA scope: every participant's reads of the staged region
     // happen-before the last retiree's bookkeeping writes (retire_last).
     uint32_t old;
+#if defined(OMPDS_RETIRE_RELAXED) && OMPDS_RETIRE_RELAXED
+    old = atomicAdd(&t.active_word(), (n << 16) - n);
+#else
     asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
                  : "=r"(old)
                  : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(&t.active_word()))),
                    "r"((n << 16) - n)
                  : "memory");
+#endif
     const uint32_t retired = (old >> 16) + n;
     const uint32_t w = static_cast<uint32_t>(t.at<int32_t>(Rt::kWorkers));
     if (t.events) {

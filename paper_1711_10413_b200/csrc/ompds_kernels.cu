@@ -185,25 +185,30 @@ struct Master {
                  : reinterpret_cast<unsigned long long>(list);
     }
     packed = __shfl_sync(0xffffffffu, packed, 0);
-    if (packed >> 63) {
-      const int32_t s = static_cast<int32_t>(packed & 0xffffffffu);
-      if (!trap) {
-        trap = s;
-        if (leader)
-          t.trap(s);
-      }
-      return s;
-    }
+    if (__builtin_expect(packed >> 63, 0))
+      return prepare_failed(static_cast<int32_t>(packed & 0xffffffffu));
     list = reinterpret_cast<void **>(packed);
     // The reserved warp publishes the pointer list lane-parallel (one
     // coalesced store per 32 entries) instead of nargs scalar stores.
-    for (int j = lane_id(); j < nargs; j += 32)
+    const int lane = static_cast<int>(lane_id());
+    if (lane < nargs)
+      list[lane] = addr_of(lane);
+    for (int j = lane + 32; j < nargs; j += 32) // lists longer than a warp
       list[j] = addr_of(j);
     bar_sync(kBarHandoff, team_threads); // release the workers
     bar_sync(kBarHandoff, team_threads); // join
     barriers += 2;
     regions += 1;
     return OMPDS_OK;
+  }
+
+  __device__ __forceinline__ int32_t prepare_failed(int32_t s) {
+    if (!trap) {
+      trap = s;
+      if (leader)
+        t.trap(s);
+    }
+    return s;
   }
 
   __device__ __forceinline__ void finish() {
