@@ -423,6 +423,17 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src,
       : "memory");
 }
 
+// Streaming 16-byte accesses for bodies that touch each element once
+// (evict-first: `ld.global.cs` / `st.global.cs`).
+__device__ __forceinline__ double2 ld_stream(const double2 *p) {
+  return __ldcs(p);
+}
+__device__ __forceinline__ int4 ld_stream(const int4 *p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(double2 *p, double2 v) {
+  __stcs(p, v);
+}
+__device__ __forceinline__ void st_stream(int4 *p, int4 v) { __stcs(p, v); }
+
 template <class T> struct SharedArrayProg {
   static constexpr int kLen = 256;
   struct Args {
@@ -474,8 +485,7 @@ template <class T> struct SharedArrayProg {
     using Vec = typename std::conditional<sizeof(T) == 8, double2, int4>::type;
     const int64_t units = a.n / V;
     Vec *av = reinterpret_cast<Vec *>(a.a);
-    for (int64_t u = gid; u < units; u += pool) {
-      Vec v = av[u];
+    auto body = [&](Vec &v, int64_t u) {
       T *e = reinterpret_cast<T *>(&v);
       const int base = static_cast<int>((u * V) & (kLen - 1));
       const Vec dv = *reinterpret_cast<const Vec *>(d + base);
@@ -483,6 +493,23 @@ template <class T> struct SharedArrayProg {
 #pragma unroll
       for (int k = 0; k < V; ++k)
         e[k] = e[k] + de[k];
+    };
+    constexpr int U = 4; // 16-byte units of a[] in flight per thread
+    int64_t u = gid;
+    for (; u + (U - 1) * pool < units; u += U * pool) {
+      Vec v[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        v[k] = ld_stream(av + u + k * pool);
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        body(v[k], u + k * pool);
+        st_stream(av + u + k * pool, v[k]);
+      }
+    }
+    for (; u < units; u += pool) {
+      Vec v = av[u];
+      body(v, u);
       av[u] = v;
     }
     for (int64_t i = units * V + gid; i < a.n; i += pool)
@@ -493,15 +520,6 @@ template <class T> struct SharedArrayProg {
 //===----------------------------------------------------------------------===//
 // Config 4/5: streaming region, 8 implicitly shared scalars.
 //===----------------------------------------------------------------------===//
-
-__device__ __forceinline__ double2 ld_stream(const double2 *p) {
-  return __ldcs(p);
-}
-__device__ __forceinline__ int4 ld_stream(const int4 *p) { return __ldcs(p); }
-__device__ __forceinline__ void st_stream(double2 *p, double2 v) {
-  __stcs(p, v);
-}
-__device__ __forceinline__ void st_stream(int4 *p, int4 v) { __stcs(p, v); }
 
 __device__ __forceinline__ double stream_op(double c1, double x, double y,
                                             double s) {

@@ -228,9 +228,14 @@ def test_gpu_reproduces_the_pass_order_miscompile():
 def test_gpu_program_events_match_reference():
     import torch
     from test_gpu_regions import canon
-    for stem in ("two_regions", "scalars_32", "shared_scalar"):
-        p = next(x for x in G.load("corpus") if x["stem"] == stem)
-        t, w, run = launches(p)[0]
+    checked = 0
+    for p in programs():
+        runs = [r for r in launches(p) if "team_events" in r[2]["sim"]]
+        if not runs:
+            continue
+        t, w, run = runs[0]
+        stem = p["stem"]
+        checked += 1
         prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], t, w)
         bufs = [torch.full((sz,), init, dtype=torch.int32, device="cuda")
                 for _, sz, init in prog.buffers]
@@ -243,6 +248,7 @@ def test_gpu_program_events_match_reference():
                     names.setdefault(fn, len(names))
                 ref.append((k, names[fn] if fn else -1, nn, b))
             assert canon(out.team_events()[team]) == canon(ref), (stem, team)
+    assert checked > 100
 
 
 @pytest.mark.gpu
