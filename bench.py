@@ -155,7 +155,7 @@ def cpu_baseline(n_sample, threads):
         L.orc_stream(1, n_sample, O.ptr(x), O.ptr(y), O.ptr(coef), threads)
         reps += 1
         el = time.perf_counter() - t0
-        if el > 3.0 or reps >= 20:
+        if el > 10.0 or reps >= 60:  # ~10 s of CPU work
             break
     gbs = BYTES_PER_ELEM * n_sample * reps / el / 1e9
     return {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
@@ -360,8 +360,10 @@ def main():
         "gpu_launches": args.steps,
         "clocks": clk,
     }
-    if rank == 0 and world == 1 and not args.no_e2e:
-        line["e2e"] = e2e(args, teams, workers, n, dev)
+    if not args.no_e2e:
+        e = e2e(args, teams, workers, n, dev, world)
+        if rank == 0:
+            line["e2e"] = e
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(1 << 26, os.cpu_count() or 1)
     if world > 1:
@@ -425,10 +427,12 @@ def other_configs(RG, dev, stream, sms):
     return out
 
 
-def e2e(args, teams, workers, n, dev):
+def e2e(args, teams, workers, n, dev, world=1):
     """Same region through the C ABI's host-buffer entry point: H2D x,y from
-    pinned memory, region, D2H y -- all inside the timed region."""
+    pinned memory, region, D2H y -- all inside the timed region.  With N
+    ranks every rank moves its own shard; the time is the max over ranks."""
     import torch
+    import torch.distributed as dist
     from paper_1711_10413_b200 import regions as RG
     xh = torch.empty(n, dtype=torch.float64).pin_memory()
     yh = torch.empty(n, dtype=torch.float64).pin_memory()
@@ -440,6 +444,9 @@ def e2e(args, teams, workers, n, dev):
     yh.copy_(yd)
     stream = torch.cuda.Stream(device=dev)
     RG.run_stream_host(xh, yh, COEF, teams, workers, xd, yd, stream=stream)  # warm
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -450,8 +457,12 @@ def e2e(args, teams, workers, n, dev):
     ev1.synchronize()
     wall = time.perf_counter() - t0
     ms = ev0.elapsed_time(ev1) / args.e2e_steps
-    return {"value": round(BYTES_PER_ELEM * n / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
-            "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 8 * n,
+    if world > 1:
+        t = torch.tensor([ms, wall], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, wall = float(t[0]), float(t[1])
+    return {"value": round(BYTES_PER_ELEM * n * world / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": 16 * n * world, "d2h_bytes_per_step": 8 * n * world,
             "ms_per_step": round(ms, 3), "wall_ms_per_step": round(wall / args.e2e_steps * 1e3, 3),
             "path": "ompds_run_stream_host (C ABI, pinned host buffers)"}
 
