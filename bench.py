@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=1 << 28, help="elements per GPU")
+    ap.add_argument("--elements", type=int, default=1 << 28, help="elements per GPU (weak) or in total (strong)")
     ap.add_argument("--teams", type=int, default=0, help="0: 148 x teams-per-SM")
     ap.add_argument("--workers", type=int, default=0, help="W (0: tuned default)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
@@ -223,12 +223,20 @@ def main():
     from paper_1711_10413_b200 import regions as RG
 
     rank, world, local = dist_env()
+    # OMPDS_BENCH_SHARE_GPU=1 + OMPDS_BENCH_BACKEND=gloo: exercise the N>1 code
+    # path with every rank on cuda:0 (a 1-GPU box); never used for numbers.
+    if os.environ.get("OMPDS_BENCH_SHARE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("OMPDS_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     from paper_1711_10413_b200 import sharding
-    n_total = args.n * world if args.scaling == "weak" else args.n
+    n_total = args.elements * world if args.scaling == "weak" else args.elements
     lo, hi = sharding.shard_range(n_total, rank, world)
     n = hi - lo
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
