@@ -122,6 +122,48 @@ def occupancy_arrays_csv(gpu: str) -> str:  # Occupancy.cpp:149-162
     return s.replace("vars,regs", "arrays,regs", 1)
 
 
+def ptxas_registers(log_path: str) -> dict:
+    """Registers per thread of every kernel in a ``ptxas -v`` log (the
+    in-tree build writes ``_build/ptxas.log``), keyed by mangled name."""
+    out = {}
+    name = None
+    for line in open(log_path).read().splitlines():
+        if "Compiling entry function" in line:
+            name = line.split("'")[1]
+        elif name and "Used" in line and "registers" in line:
+            out[name] = int(line.split("Used")[1].split("registers")[0])
+            name = None
+    return out
+
+
+# (kernel key substring, config, threads per team, team footprint bytes)
+B200_KERNELS = [
+    ("RegionsProgIiE", "config1 int (loop layout)", 64, 56 + 160 + 49),
+    ("SharedArrayProgIdE", "config2 f64", 512, 2072 + 160 + 49),
+    ("NestedProgIdE", "config3 f64 (2 KB warp slots x 3)", 128, 96 * 0 + 304 + 3 * 2048),
+    ("StreamProgIdE", "config4 f64", 128, 80 + 160 + 49),
+    ("ProgramProgE", "reference programs (scalars_4 footprint)", 128, 48 + 160 + 49),
+]
+
+
+def b200_kernel_occupancy_csv(log_path: str) -> str:
+    """The paper's occupancy table for our own sm_100a kernels on B200:
+    registers from ptxas, footprint = the team region each launch requests."""
+    regs = ptxas_registers(log_path)
+    rows = ["kernel,config,regs,threads,footprint,teams_by_regs,teams_by_smem,potential,actual,"
+            "smem_used,binding"]
+    for key, cfg, thr, fp in B200_KERNELS:
+        r = next((v for k, v in regs.items() if key in k), None)
+        if r is None:
+            continue
+        o = occupancy_for("b200", fp, r, thr)
+        binding = ("registers" if o.actual == o.teams_by_regs else
+                   "shared memory" if o.actual == o.teams_by_smem else "threads/blocks")
+        rows.append(f"{key},{cfg},{r},{thr},{fp},{o.teams_by_regs},{o.teams_by_smem},"
+                    f"{o.potential},{o.actual},{o.smem_used},{binding}")
+    return "\n".join(rows) + "\n"
+
+
 def max_vars_csv(gpu: str) -> str:  # Occupancy.cpp:164-170
     rows = ["teams,max_regs,max_vars"]
     for t in MAX_VARS_TEAM_POINTS:

@@ -193,3 +193,13 @@ def test_compute_entry_point_raises_ompds_error_without_gpu():
     with pytest.raises(P.OmpdsError) as e:
         runtime.replay([(0, 0, 8)])
     assert e.value.code == P.ERR_CUDA
+
+
+def test_b200_kernel_occupancy_table_from_ptxas_log():
+    log = os.path.join(ROOT, "paper_1711_10413_b200", "_build", "ptxas.log")
+    csv = occupancy.b200_kernel_occupancy_csv(log)
+    rows = [r.split(",") for r in csv.strip().splitlines()[1:]]
+    assert {r[0] for r in rows} >= {"RegionsProgIiE", "StreamProgIdE", "SharedArrayProgIdE"}
+    for r in rows:
+        regs, thr = int(r[2]), int(r[3])
+        assert int(r[5]) == 65536 // (regs * thr)  # teams_by_regs
