@@ -180,35 +180,34 @@ struct Master {
     unsigned long long packed = 0;
     if (leader) {
       const int32_t s = prepare_parallel(t, kMaster, fn, nargs, &list);
+      if (s)
+        t.trap(s); // the team's first trap, before any worker can record one
       // one shuffle carries the list, or the trap code with bit 63 set
       packed = s ? (static_cast<unsigned long long>(s) | (1ull << 63))
                  : reinterpret_cast<unsigned long long>(list);
     }
     packed = __shfl_sync(0xffffffffu, packed, 0);
-    if (__builtin_expect(packed >> 63, 0))
-      return prepare_failed(static_cast<int32_t>(packed & 0xffffffffu));
+    const bool ok = (packed >> 63) == 0;
     list = reinterpret_cast<void **>(packed);
     // The reserved warp publishes the pointer list lane-parallel (one
     // coalesced store per 32 entries) instead of nargs scalar stores.
     const int lane = static_cast<int>(lane_id());
-    if (lane < nargs)
+    if (ok && lane < nargs)
       list[lane] = addr_of(lane);
-    for (int j = lane + 32; j < nargs; j += 32) // lists longer than a warp
+    for (int j = lane + 32; ok && j < nargs; j += 32) // lists longer than a warp
       list[j] = addr_of(j);
+    // Released even when prepare trapped (keeps the handoff branch-free):
+    // nothing is staged then, workers observe a non-Staged phase and skip.
     bar_sync(kBarHandoff, team_threads); // release the workers
     bar_sync(kBarHandoff, team_threads); // join
     barriers += 2;
+    if (__builtin_expect(!ok, 0)) {
+      if (!trap)
+        trap = static_cast<int32_t>(packed & 0xffffffffu);
+      return trap;
+    }
     regions += 1;
     return OMPDS_OK;
-  }
-
-  __device__ __forceinline__ int32_t prepare_failed(int32_t s) {
-    if (!trap) {
-      trap = s;
-      if (leader)
-        t.trap(s);
-    }
-    return s;
   }
 
   __device__ __forceinline__ void finish() {
