@@ -240,11 +240,11 @@ def main():
     lo, hi = sharding.shard_range(n_total, rank, world)
     n = hi - lo
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    # Tuned on B200 (tools/sweep.py, profiles/r1_sweep.json): 128-thread
-    # teams (W=96 + the master warp), 32 teams per SM = 4 waves of 8
-    # resident teams; 0.4-5 % faster than one wave of 1024-thread teams.
+    # Tuned on B200 (tools/sweep.py, profiles/r1_sweep*.json): 128-thread
+    # teams (W=96 + the master warp), 8 teams per SM, 2 x 16-byte units of x
+    # and y in flight per thread; ~4 % faster than one wave of 1024-thread teams.
     workers = args.workers or 96
-    teams = args.teams or sms * 32
+    teams = args.teams or sms * 8
 
     x = torch.empty(n, dtype=torch.float64, device=dev)
     y = torch.empty(n, dtype=torch.float64, device=dev)

@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_build", "libompds_b200.so")
+LIB_PATH = os.environ.get("OMPDS_LIB_PATH") or os.path.join(HERE, "_build", "libompds_b200.so")
 
 # ---------------------------------------------------------------------------
 # constants (ompds.h)
@@ -155,7 +155,7 @@ _SIGS = {
     "ompds_run_nested": (C.c_int32, [C.POINTER(Launch), C.c_int32, C.c_int32, C.c_int64,
                                       C.c_int64, _P, _P, _P, _P]),
     "ompds_run_program": (C.c_int32, [C.POINTER(Launch), C.POINTER(Program), _P, _P]),
-    "ompds_run_stream_host":(C.c_int32, [C.POINTER(Launch), C.c_int32, C.c_int64, _P, _P, _P,
+    "ompds_run_stream_host": (C.c_int32, [C.POINTER(Launch), C.c_int32, C.c_int64, _P, _P, _P,
                                            _P, _P]),
     "ompds_fill_uniform": (C.c_int32, [C.c_int32, _P, C.c_int64, C.c_uint64, C.c_int64, _P]),
     "ompds_checksum": (C.c_int32, [C.c_int32, _P, C.c_int64, _P, _P]),

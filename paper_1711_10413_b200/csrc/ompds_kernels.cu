@@ -425,7 +425,14 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src,
 // Streaming 16-byte accesses for bodies that touch each element once
 // (evict-first: `ld.global.cs` / `st.global.cs`).
 __device__ __forceinline__ double2 ld_stream(const double2 *p) {
+#if defined(OMPDS_STREAM_L2PF) && OMPDS_STREAM_L2PF
+  double2 v;
+  asm volatile("ld.global.cs.L2::256B.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+#else
   return __ldcs(p);
+#endif
 }
 __device__ __forceinline__ int4 ld_stream(const int4 *p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(double2 *p, double2 v) {
@@ -567,7 +574,10 @@ template <class T> struct StreamProg {
       return;
     constexpr int V = 16 / sizeof(T);
     using Vec = typename std::conditional<sizeof(T) == 8, double2, int4>::type;
-    constexpr int U = 4; // 16-byte units in flight per thread per array
+#ifndef OMPDS_STREAM_U
+#define OMPDS_STREAM_U 2 // swept 2/4/8 on B200: 2 leaves room for more resident teams
+#endif
+    constexpr int U = OMPDS_STREAM_U; // 16-byte units in flight per thread per array
     const int64_t gid = int64_t(w.team) * w.workers + w.wid;
     const int64_t pool = int64_t(w.teams) * w.workers;
     const int64_t units = a.n / V;

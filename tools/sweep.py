@@ -57,8 +57,8 @@ def main():
     y = torch.empty(n, dtype=torch.float64, device="cuda")
     RG.fill_uniform(x, 1)
     RG.fill_uniform(y, 2)
-    geoms = [(992, 2), (96, 16), (96, 8), (96, 24), (96, 32), (64, 16), (64, 32), (32, 32),
-             (32, 64), (160, 12), (224, 8), (224, 16), (128, 16), (480, 4)]
+    geoms = [(992, 2), (96, 16), (96, 8), (96, 12), (96, 24), (96, 32), (96, 48), (64, 16),
+             (64, 32), (32, 32), (160, 12), (224, 6), (224, 8), (224, 16), (128, 16), (480, 4)]
     if len(sys.argv) > 1 and sys.argv[1] == "quick":
         geoms = geoms[:3]
     if len(sys.argv) > 1 and sys.argv[1] == "regions":
