@@ -52,7 +52,11 @@ def make_launch(teams: int, workers: int, prealloc_entries: int = L.DEFAULT_PREA
                 fail_dynamic_alloc: bool = False, depot_capacity: int = -1,
                 log_events: bool = False, max_events: int = 0,
                 stream: Optional[torch.cuda.Stream] = None) -> L.Launch:
-    s = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    cur = torch.cuda.current_stream()
+    if stream is not None and stream.cuda_stream != cur.cuda_stream:
+        # outputs/inputs prepared on the current stream must be ready first
+        stream.wait_stream(cur)
+    s = stream.cuda_stream if stream is not None else cur.cuda_stream
     return L.Launch(teams, workers, prealloc_entries, 1 if fail_dynamic_alloc else 0,
                     depot_capacity, 1 if log_events else 0, max_events if log_events else 0,
                     C.c_void_p(s))
@@ -75,6 +79,7 @@ class Outputs:
         return C.c_void_p(self.events.data_ptr()) if self.events is not None else None
 
     def team_stats(self) -> List[TeamStats]:
+        torch.cuda.synchronize(self.stats.device)  # the launch may be on another stream
         raw = bytes(self.stats.cpu().numpy().tobytes())
         arr = (L.TeamStats * self.teams).from_buffer_copy(raw)
         return [TeamStats(s.trap, s.master_barriers, s.barrier_releases, s.regions,
@@ -154,6 +159,25 @@ def run_nested(a: torch.Tensor, teams: int, workers: int, regions: int,
                          s.max_depth, s.high_water) for s in arr[t * warps:(t + 1) * warps]]
               for t in range(teams)]
     return out, stacks
+
+
+def prepared_shared_array(a: torch.Tensor, teams: int, workers: int,
+                          d_init: Optional[torch.Tensor] = None,
+                          stream: Optional[torch.cuda.Stream] = None):
+    """A zero-argument callable that only issues the config-2 launch (all
+    arguments marshalled up front), for timing without host overhead."""
+    _require_cuda(a)
+    launch = make_launch(teams, workers, stream=stream)
+    dp = C.c_void_p(d_init.data_ptr()) if d_init is not None else None
+    ap = C.c_void_p(a.data_ptr())
+    fn = L.lib().ompds_run_shared_array
+    elem, n = ELEM[a.dtype], a.numel()
+    lref = C.byref(launch)
+
+    def go():
+        L.check(fn(lref, elem, n, ap, dp, None, None), "ompds_run_shared_array")
+    go.launch = launch  # keep the struct alive
+    return go
 
 
 def coef_buffer(dtype: torch.dtype, coef) -> C.Array:
