@@ -466,6 +466,17 @@ static json runtimeGolden() {
                               {{0, M, 8}, {1, M, N}}, 20, false));
     }
   }
+  // Acceptance criterion 8's allocation law (AcceptanceMain.cpp:368-385:
+  // mt19937(20260815), int N in [0,128], 400 rounds, workers 8).
+  {
+    std::mt19937 Rng(20260815);
+    std::uniform_int_distribution<int> Dist(0, 128);
+    for (int Round = 0; Round < 400; ++Round) {
+      int N = Dist(Rng);
+      Out.push_back(runScript("acceptance_law_" + std::to_string(Round),
+                              {{0, M, 8}, {1, M, N}}, 20, false));
+    }
+  }
   // Seeded protocol fuzz: random roles, ops and counts, legal and not.
   {
     std::mt19937 Rng(0x5eed01ab);
