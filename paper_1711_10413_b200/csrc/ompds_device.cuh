@@ -223,6 +223,62 @@ __device__ __forceinline__ TeamCtx make_team(unsigned char *smem,
   return t;
 }
 
+// Team state snapshots: every load issued in one asm block, so the
+// compiler cannot sink a later load below a branch on an earlier one (one
+// shared-memory round trip instead of a chain).
+struct PrepareState {
+  uint8_t phase;
+  int32_t active;
+};
+__device__ __forceinline__ PrepareState load_prepare_state(const TeamCtx &t) {
+  const uint32_t rt = static_cast<uint32_t>(__cvta_generic_to_shared(t.rt));
+  uint32_t ph, aw;
+  asm volatile("ld.shared.u8 %0, [%2+48];\n\t"
+               "ld.shared.u32 %1, [%2+20];"
+               : "=r"(ph), "=r"(aw)
+               : "r"(rt)
+               : "memory");
+  static_assert(Rt::kPhase == 48 && Rt::kActive == 20, "rt layout");
+  return PrepareState{static_cast<uint8_t>(ph), static_cast<int32_t>(aw & 0xffffu)};
+}
+struct StagedState {
+  uint8_t phase;
+  int32_t fn;
+  int32_t nargs;
+  int32_t workers;
+  void **args;
+  void *win; // this lane's window entry (prefetch), or nullptr
+};
+// `win_off`: shared address of this lane's window entry, 0 = none.
+__device__ __forceinline__ StagedState load_staged_state(const TeamCtx &t,
+                                                         uint32_t win_off) {
+  const uint32_t rt = static_cast<uint32_t>(__cvta_generic_to_shared(t.rt));
+  uint32_t ph, fn, na, wk;
+  unsigned long long args, win = 0;
+  static_assert(Rt::kArgs == 0 && Rt::kWorkFn == 8 && Rt::kNArgs == 12 &&
+                    Rt::kWorkers == 16, "rt layout");
+  if (win_off)
+    asm volatile("ld.shared.u8 %0, [%7+48];\n\t"
+                 "ld.shared.u64 %4, [%7];\n\t"
+                 "ld.shared.v2.u32 {%1, %2}, [%7+8];\n\t"
+                 "ld.shared.u32 %3, [%7+16];\n\t"
+                 "ld.shared.u64 %5, [%6];"
+                 : "=r"(ph), "=r"(fn), "=r"(na), "=r"(wk), "=l"(args), "=l"(win)
+                 : "r"(win_off), "r"(rt)
+                 : "memory");
+  else
+    asm volatile("ld.shared.u8 %0, [%5+48];\n\t"
+                 "ld.shared.u64 %4, [%5];\n\t"
+                 "ld.shared.v2.u32 {%1, %2}, [%5+8];\n\t"
+                 "ld.shared.u32 %3, [%5+16];"
+                 : "=r"(ph), "=r"(fn), "=r"(na), "=r"(wk), "=l"(args)
+                 : "r"(rt)
+                 : "memory");
+  return StagedState{static_cast<uint8_t>(ph), static_cast<int32_t>(fn),
+                     static_cast<int32_t>(na), static_cast<int32_t>(wk),
+                     reinterpret_cast<void **>(args), reinterpret_cast<void *>(win)};
+}
+
 __device__ __forceinline__ void rt_zero(const TeamCtx &t) {
   for (int i = 0; i < Rt::kBytes; ++i)
     t.rt[i] = 0;
@@ -248,6 +304,50 @@ __device__ inline int32_t kernel_init(const TeamCtx &t, int role,
   return OMPDS_OK;
 }
 
+// The phase checks of prepareParallel in the reference's order
+// (DeviceRuntime.cpp:46-60), as a pure function of the team state so a warp
+// can evaluate them on broadcast loads.
+__device__ __forceinline__ int32_t prepare_check(uint8_t ph, int32_t active,
+                                                 int64_t nargs) {
+  if (ph == kUninit)
+    return OMPDS_TRAP_PREPARE_BEFORE_INIT;
+  if (ph == kTerminated)
+    return OMPDS_TRAP_PREPARE_AFTER_DEINIT;
+  if (ph == kStaged || active > 0)
+    return OMPDS_TRAP_PREPARE_IN_FLIGHT;
+  if (nargs < 0)
+    return OMPDS_TRAP_NEGATIVE_NARGS;
+  return OMPDS_OK;
+}
+
+// Placement decision of the shared-args list (DeviceRuntime.cpp:61-74):
+// the preallocated window when nargs <= PreallocEntries, else a block of the
+// team's global slab (nullptr: shared-args-alloc-failed).
+__device__ __forceinline__ void **alloc_args_list(const TeamCtx &t, int32_t fn,
+                                                  int64_t nargs) {
+  if (nargs <= t.prealloc) {
+    t.log(OMPDS_EV_PREPARE_PREALLOC, fn, nargs, 0);
+    return t.window;
+  }
+  const int64_t bytes = nargs * OMPDS_SHARED_ARG_ENTRY_BYTES;
+  void *p = t.fail_dyn ? nullptr : t.slab_alloc(bytes);
+  if (p == nullptr)
+    return nullptr;
+  t.at<uint32_t>(Rt::kDynAllocs) += 1;
+  t.at<uint32_t>(Rt::kDynBytes) += static_cast<uint32_t>(bytes);
+  t.log(OMPDS_EV_PREPARE_DYNAMIC, fn, nargs, bytes);
+  return static_cast<void **>(p);
+}
+
+// Stages the region: Idle -> Staged.
+__device__ __forceinline__ void stage_region(const TeamCtx &t, int32_t fn,
+                                             int64_t nargs, void **list) {
+  t.args() = list;
+  t.nargs() = static_cast<int32_t>(nargs);
+  t.work_fn() = fn;
+  t.phase() = kStaged;
+}
+
 // __kmpc_kernel_prepare_parallel / begin-sharing-variables: stages work
 // function `fn` and returns the list the master fills with nargs pointers.
 __device__ inline int32_t prepare_parallel(const TeamCtx &t, int role,
@@ -255,33 +355,14 @@ __device__ inline int32_t prepare_parallel(const TeamCtx &t, int role,
                                            void ***out) {
   if (role != kMaster)
     return OMPDS_TRAP_PREPARE_FROM_WORKER;
-  uint8_t ph = t.phase();
-  if (ph == kUninit)
-    return OMPDS_TRAP_PREPARE_BEFORE_INIT;
-  if (ph == kTerminated)
-    return OMPDS_TRAP_PREPARE_AFTER_DEINIT;
-  if (ph == kStaged || t.active() > 0)
-    return OMPDS_TRAP_PREPARE_IN_FLIGHT;
-  if (nargs < 0)
-    return OMPDS_TRAP_NEGATIVE_NARGS;
-  void **list;
-  if (nargs <= t.prealloc) {
-    list = t.window;
-    t.log(OMPDS_EV_PREPARE_PREALLOC, fn, nargs, 0);
-  } else {
-    int64_t bytes = nargs * OMPDS_SHARED_ARG_ENTRY_BYTES;
-    void *p = t.fail_dyn ? nullptr : t.slab_alloc(bytes);
-    if (p == nullptr)
-      return OMPDS_TRAP_ARGS_ALLOC_FAILED;
-    list = static_cast<void **>(p);
-    t.at<uint32_t>(Rt::kDynAllocs) += 1;
-    t.at<uint32_t>(Rt::kDynBytes) += static_cast<uint32_t>(bytes);
-    t.log(OMPDS_EV_PREPARE_DYNAMIC, fn, nargs, bytes);
-  }
-  t.args() = list;
-  t.nargs() = static_cast<int32_t>(nargs);
-  t.work_fn() = fn;
-  t.phase() = kStaged;
+  const PrepareState st = load_prepare_state(t);
+  const int32_t s = prepare_check(st.phase, st.active, nargs);
+  if (s)
+    return s;
+  void **list = alloc_args_list(t, fn, nargs);
+  if (list == nullptr)
+    return OMPDS_TRAP_ARGS_ALLOC_FAILED;
+  stage_region(t, fn, nargs, list);
   *out = list;
   return OMPDS_OK;
 }
@@ -364,14 +445,88 @@ struct Fetch {
   void **args;
   int32_t nargs;
   int32_t status;
+  void *win;         // this lane's window entry, loaded speculatively
+  int32_t workers;   // the team's Workers (kernel_init), read with the state
 };
 
+#ifndef OMPDS_PREFETCH_WINDOW
+#define OMPDS_PREFETCH_WINDOW 1
+#endif
+
+// Participation of a worker warp's lanes (mine = tid < W).  It does not
+// change between regions, so the worker loop computes it once instead of a
+// ballot per fetch and per retire.
+struct WarpMask {
+  uint32_t ballot;  // participating lanes
+  uint32_t n;       // their count
+  uint32_t leader;  // lowest participating lane (does the warp's bookkeeping)
+  bool is_leader;
+  __device__ __forceinline__ static WarpMask of(bool mine) {
+    WarpMask m;
+    m.ballot = __ballot_sync(0xffffffffu, mine);
+    m.n = __popc(m.ballot);
+    m.leader = m.ballot ? __ffs(m.ballot) - 1 : 0;
+    m.is_leader = m.ballot != 0 && lane_id() == m.leader;
+    return m;
+  }
+};
+
+// Branch-free bookkeeping: shared-memory updates predicated on `p` (the
+// warp stays converged; no reconvergence barrier around a leader-only block).
+__device__ __forceinline__ void red_add_if(uint32_t saddr, uint32_t v, bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+               "@q red.shared.add.u32 [%0], %1;\n\t}" ::"r"(saddr), "r"(v),
+               "r"(static_cast<uint32_t>(p))
+               : "memory");
+}
+// retire of a region whose list is the window: args = null, work_fn = -1,
+// nargs = 0, Active word = 0, phase = Idle (retire_last's window case).
+__device__ __forceinline__ void retire_window_if(const TeamCtx &t, bool p) {
+  const uint32_t rt = static_cast<uint32_t>(__cvta_generic_to_shared(t.rt));
+  static_assert(Rt::kArgs == 0 && Rt::kWorkFn == 8 && Rt::kNArgs == 12 &&
+                    Rt::kActive == 20 && Rt::kPhase == 48, "rt layout");
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t"
+               "@q st.shared.u64 [%0], %2;\n\t"
+               "@q st.shared.v2.u32 [%0+8], {%3, %4};\n\t"
+               "@q st.shared.u32 [%0+20], %4;\n\t"
+               "@q st.shared.u8 [%0+48], %5;\n\t}" ::"r"(rt),
+               "r"(static_cast<uint32_t>(p)), "l"(0ull), "r"(0xffffffffu), "r"(0u),
+               "r"(static_cast<uint32_t>(kIdle))
+               : "memory");
+}
+// staging of a region (stage_region's stores), predicated on `p`.
+__device__ __forceinline__ void stage_region_if(const TeamCtx &t, int32_t fn,
+                                                int32_t nargs, void **list, bool p) {
+  const uint32_t rt = static_cast<uint32_t>(__cvta_generic_to_shared(t.rt));
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t"
+               "@q st.shared.u64 [%0], %2;\n\t"
+               "@q st.shared.v2.u32 [%0+8], {%3, %4};\n\t"
+               "@q st.shared.u8 [%0+48], %5;\n\t}" ::"r"(rt),
+               "r"(static_cast<uint32_t>(p)),
+               "l"(reinterpret_cast<unsigned long long>(list)),
+               "r"(static_cast<uint32_t>(fn)), "r"(static_cast<uint32_t>(nargs)),
+               "r"(static_cast<uint32_t>(kStaged))
+               : "memory");
+}
+
 // All 32 lanes of a worker warp call this after the release barrier.
-// `mine` = this lane is a requested worker (tid < W).
+// `mine` = this lane is a requested worker (tid < W); `m` = WarpMask::of(mine).
 __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
+                                                     const WarpMask &m,
                                                      bool mine) {
   Fetch f;
-  uint8_t ph = t.phase();
+  // Lane j's entry of the preallocated window is loaded alongside the team
+  // state (no dependency on the staged list pointer): when the region's list
+  // is the window, get-shared-variables needs no further load.
+  uint32_t win_off = 0;
+#if OMPDS_PREFETCH_WINDOW
+  if (static_cast<int32_t>(lane_id()) < t.prealloc)
+    win_off = static_cast<uint32_t>(__cvta_generic_to_shared(t.window)) + 8u * lane_id();
+#endif
+  const StagedState st = load_staged_state(t, win_off);
+  const uint8_t ph = st.phase;
+  f.win = st.win;
+  f.workers = st.workers;
   f.status = OMPDS_OK;
   if (ph == kTerminated) {
     f.fn = -1;
@@ -379,35 +534,48 @@ __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
     f.nargs = 0;
     return f;
   }
-  f.fn = t.work_fn();
-  f.args = static_cast<void **>(t.args());
-  f.nargs = t.nargs();
+  f.fn = st.fn;
+  f.args = st.args;
+  f.nargs = st.nargs;
   if (ph != kStaged) {
     f.status = mine ? t.trap(OMPDS_TRAP_PARALLEL_NOT_STAGED) : OMPDS_OK;
     f.fn = -1;
     return f;
   }
-  const uint32_t ballot = __ballot_sync(0xffffffffu, mine);
-  const uint32_t lane = lane_id();
-  const uint32_t n = __popc(ballot);
-  if (n) {
-    const uint32_t leader = __ffs(ballot) - 1;
-    if (t.events == nullptr) { // fast path: one fire-and-forget shared atomic
-      if (lane == leader)
-        atomicAdd(&t.active_word(), n);
-      return f;
-    }
-    int64_t ev = -1;
-    if (lane == leader) {
-      atomicAdd(&t.active_word(), n);
-      ev = t.log_reserve(n);
-    }
-    ev = __shfl_sync(0xffffffffu, ev, leader);
-    if (mine && ev >= 0)
-      t.log_at(ev + __popc(ballot & ((1u << lane) - 1u)), OMPDS_EV_FETCH, f.fn,
-               0, 0);
+  if (m.n == 0)
+    return f;
+  const uint32_t active = static_cast<uint32_t>(__cvta_generic_to_shared(&t.active_word()));
+  if (t.events == nullptr) { // fast path: one fire-and-forget shared atomic
+    red_add_if(active, m.n, m.is_leader);
+    return f;
   }
+  int64_t ev = -1;
+  if (m.is_leader) {
+    atomicAdd(&t.active_word(), m.n);
+    ev = t.log_reserve(m.n);
+  }
+  ev = __shfl_sync(0xffffffffu, ev, m.leader);
+  const uint32_t lane = lane_id();
+  if (mine && ev >= 0)
+    t.log_at(ev + __popc(m.ballot & ((1u << lane) - 1u)), OMPDS_EV_FETCH, f.fn,
+             0, 0);
   return f;
+}
+__device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
+                                                     bool mine) {
+  return begin_parallel_warp(t, WarpMask::of(mine), mine);
+}
+
+// What a worker warp needs to retire the region it fetched, packed in one
+// register so nothing else stays live across the region body: bit 0 = this
+// lane is the warp's leader, bit 1 = the warp holds all W participants,
+// bit 2 = the list is the window (nothing to free), bits 8.. = participants.
+__device__ __forceinline__ uint32_t retire_plan(const TeamCtx &t,
+                                                const WarpMask &m,
+                                                const Fetch &f) {
+  return (m.n << 8) | (m.is_leader ? 1u : 0u) |
+         (m.n == static_cast<uint32_t>(f.workers) ? 2u : 0u) |
+         (f.args == t.window || f.args == nullptr ? 4u : 0u);
 }
 
 // All 32 lanes of a worker warp call this when the region body is done.
@@ -416,14 +584,35 @@ __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
 // the one whose retirement brings the region's retired count to W (every
 // worker participates in every staged region, Codegen.cpp:403-513).  Under
 // the reference's schedule (all fetches before any retire) both rules agree.
-__device__ __forceinline__ void end_parallel_warp(const TeamCtx &t, bool mine) {
-  const uint32_t ballot = __ballot_sync(0xffffffffu, mine);
-  const uint32_t n = __popc(ballot);
+__device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
+                                                  uint32_t plan) {
+  const uint32_t n = plan >> 8;
   if (n == 0)
     return;
-  const uint32_t lane = lane_id();
-  const uint32_t leader = __ffs(ballot) - 1;
-  if (lane == leader) {
+  const bool leader = plan & 1u;
+#ifndef OMPDS_SOLE_WARP_RETIRE
+#define OMPDS_SOLE_WARP_RETIRE 1
+#endif
+#if OMPDS_SOLE_WARP_RETIRE
+  // A warp holding all W participants retires the region's last one whatever
+  // the order: no other warp touches the staged region, so its bookkeeping
+  // needs no returning atomic (the leader's own fetch atomic precedes it in
+  // program order).  Config 1 (W = 32) takes this path.
+  if (plan & 2u) {
+    if (t.events && leader) {
+      const int64_t ev = t.log_reserve(n);
+      for (uint32_t k = 0; k < n; ++k)
+        t.log_at(ev + k, OMPDS_EV_RETIRE, -1, int64_t(n) - int64_t(k + 1), 0);
+    }
+    if (plan & 4u)
+      retire_window_if(t, leader);
+    else if (leader)
+      retire_last(t); // frees the global list
+    return;
+  }
+#endif
+  if (leader) {
+    const uint32_t w = static_cast<uint32_t>(t.at<int32_t>(Rt::kWorkers));
     // retired += n (high half), Active -= n (low half; >= n: our own fetch).
     // acq_rel at CTA scope: every participant's reads of the staged region
     // happen-before the last retiree's bookkeeping writes (retire_last).
@@ -438,18 +627,26 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t, bool mine) {
                  : "memory");
 #endif
     const uint32_t retired = (old >> 16) + n;
-    const uint32_t w = static_cast<uint32_t>(t.at<int32_t>(Rt::kWorkers));
     if (t.events) {
       int64_t ev = t.log_reserve(n);
       for (uint32_t k = 0; k < n; ++k)
         t.log_at(ev + k, OMPDS_EV_RETIRE, -1,
                  int64_t(w) - int64_t((old >> 16) + k + 1), 0);
     }
-    if (retired == w)
-      retire_last(t); // this warp retired the region's last participant
+    if (retired == w) // this warp retired the region's last participant
+      retire_last(t);
   }
   // no __syncwarp: the join barrier that follows orders the leader's
   // shared-memory updates for every participant
+}
+__device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
+                                                  const WarpMask &m,
+                                                  const Fetch &f) {
+  end_parallel_warp(t, retire_plan(t, m, f));
+}
+__device__ __forceinline__ void end_parallel_warp(const TeamCtx &t, bool mine,
+                                                  const Fetch &f) {
+  end_parallel_warp(t, WarpMask::of(mine), f);
 }
 
 //===----------------------------------------------------------------------===//
@@ -482,6 +679,20 @@ __device__ __forceinline__ SharedVars get_shared_variables(void **args,
     }
   }
   return v;
+}
+
+// get-shared-variables for a fetched region: the window entry was already
+// loaded by begin_parallel_warp; a global list is read here.
+__device__ __forceinline__ SharedVars get_shared_variables(const TeamCtx &t,
+                                                           const Fetch &f) {
+#if OMPDS_PREFETCH_WINDOW
+  if (f.args == t.window) {
+    SharedVars v;
+    v.mine = static_cast<int32_t>(lane_id()) < f.nargs ? f.win : nullptr;
+    return v;
+  }
+#endif
+  return get_shared_variables(f.args, f.nargs);
 }
 
 // Loads capture j's value through its pointer: lane j dereferences, then a

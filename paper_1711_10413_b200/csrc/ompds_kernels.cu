@@ -48,6 +48,27 @@ static int32_t cuda_fail(cudaError_t e, const char *what) {
 
 constexpr int kMaxCaptures = 32;
 
+// Region timeline (tools/timeline.cu only): clock64 stamps of the master's
+// and worker warp 0's steps for the first OMPDS_TIMELINE regions of team 0.
+#ifdef OMPDS_TIMELINE
+__device__ long long g_timeline[OMPDS_TIMELINE][16];
+__device__ __forceinline__ long long tl_clock() {
+  long long c; // volatile + memory clobber: stays between the barriers
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c)::"memory");
+  return c;
+}
+#define OMPDS_TL(r, k)                                                         \
+  do {                                                                         \
+    const long long c_ = tl_clock();                                           \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (r) < OMPDS_TIMELINE)    \
+      g_timeline[(r)][(k)] = c_;                                               \
+  } while (0)
+#else
+#define OMPDS_TL(r, k)                                                         \
+  do {                                                                         \
+  } while (0)
+#endif
+
 struct TeamParams {
   int32_t workers;       // W
   int32_t prealloc;      // PreallocEntries
@@ -176,8 +197,45 @@ struct Master {
   template <class AddrOf>
   __device__ __forceinline__ int32_t parallel_with(int32_t fn, int32_t nargs,
                                                    AddrOf addr_of) {
+    OMPDS_TL(regions, 0);
     void **list = nullptr;
     unsigned long long packed = 0;
+#ifndef OMPDS_WARP_PREPARE
+#define OMPDS_WARP_PREPARE 1
+#endif
+#if OMPDS_WARP_PREPARE
+    // Every lane evaluates prepare_parallel's phase checks on broadcast
+    // loads, so the window case needs no shuffle from the master lane; only
+    // a global list (nargs > PreallocEntries) is allocated by the master and
+    // shuffled.  The __syncwarp orders every lane's reads before the
+    // master's staging writes.
+    {
+      const PrepareState st = load_prepare_state(t);
+      int32_t s = prepare_check(st.phase, st.active, nargs);
+      list = t.window;
+      if (s == OMPDS_OK && nargs > t.prealloc) {
+        if (leader) {
+          list = alloc_args_list(t, fn, nargs);
+          packed = list ? reinterpret_cast<unsigned long long>(list)
+                        : (static_cast<unsigned long long>(OMPDS_TRAP_ARGS_ALLOC_FAILED) |
+                           (1ull << 63));
+        }
+        packed = __shfl_sync(0xffffffffu, packed, 0);
+        if (packed >> 63)
+          s = static_cast<int32_t>(packed & 0xffffffffu);
+        list = reinterpret_cast<void **>(packed);
+      } else if (s == OMPDS_OK && leader && t.events) {
+        alloc_args_list(t, fn, nargs); // the window: logs PreparePrealloc
+      }
+      __syncwarp();
+      OMPDS_TL(regions, 1);
+      stage_region_if(t, fn, static_cast<int32_t>(nargs), list, leader && s == OMPDS_OK);
+      if (__builtin_expect(s != OMPDS_OK, 0) && leader)
+        t.trap(s); // the team's first trap, before any worker can record one
+      packed = s ? (static_cast<unsigned long long>(s) | (1ull << 63))
+                 : reinterpret_cast<unsigned long long>(list);
+    }
+#else
     if (leader) {
       const int32_t s = prepare_parallel(t, kMaster, fn, nargs, &list);
       if (s)
@@ -187,6 +245,7 @@ struct Master {
                  : reinterpret_cast<unsigned long long>(list);
     }
     packed = __shfl_sync(0xffffffffu, packed, 0);
+#endif
     const bool ok = (packed >> 63) == 0;
     list = reinterpret_cast<void **>(packed);
     // The reserved warp publishes the pointer list lane-parallel (one
@@ -198,8 +257,11 @@ struct Master {
       list[j] = addr_of(j);
     // Released even when prepare trapped (keeps the handoff branch-free):
     // nothing is staged then, workers observe a non-Staged phase and skip.
+    OMPDS_TL(regions, 2);
     bar_sync(kBarHandoff, team_threads); // release the workers
+    OMPDS_TL(regions, 3);
     bar_sync(kBarHandoff, team_threads); // join
+    OMPDS_TL(regions, 4);
     barriers += 2;
     if (__builtin_expect(!ok, 0)) {
       if (!trap)
@@ -296,9 +358,12 @@ __global__ void OMPDS_GENERIC_LB
         p.warp_ovf ? p.warp_ovf + (size_t(blockIdx.x) * worker_warps + warp) * p.warp_ovf_bytes
                    : nullptr;
     w.ds.init(slot, p.warp_slot_bytes, ovf, p.warp_ovf ? p.warp_ovf_bytes : 0);
-    for (;;) {
+    const WarpMask wm = WarpMask::of(w.mine); // loop-invariant participation
+    for (int32_t rr = 0;; ++rr) {
       bar_sync(kBarHandoff, team_threads); // await.work
-      Fetch f = begin_parallel_warp(t, w.mine);
+      OMPDS_TL(rr, 5);
+      Fetch f = begin_parallel_warp(t, wm, w.mine);
+      OMPDS_TL(rr, 6);
       if (f.fn < 0) {
         if (f.status == OMPDS_OK)
           break; // termination sentinel (wf == null)
@@ -307,10 +372,15 @@ __global__ void OMPDS_GENERIC_LB
       }
       w.args = f.args;
       w.nargs = f.nargs;
-      SharedVars sv = get_shared_variables(f.args, f.nargs);
+      const uint32_t plan = retire_plan(t, wm, f);
+      SharedVars sv = get_shared_variables(t, f);
+      OMPDS_TL(rr, 7);
       Prog::region(f.fn, sv, w, a);
-      end_parallel_warp(t, w.mine);
+      OMPDS_TL(rr, 8);
+      end_parallel_warp(t, plan);
+      OMPDS_TL(rr, 9);
       bar_sync(kBarHandoff, team_threads); // barrier.parallel (join)
+      OMPDS_TL(rr, 10);
     }
   } else {
     Master m;

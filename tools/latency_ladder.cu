@@ -42,8 +42,9 @@ __global__ void ladder(int32_t *a, int R, long long *cycles, const __grid_consta
       int32_t fn = 0;
       void **args = nullptr;
       int32_t nargs = 0;
+      Fetch f{};
       if (V >= 1) {
-        Fetch f = begin_parallel_warp(t, mine);
+        f = begin_parallel_warp(t, mine);
         fn = f.fn;
         args = f.args;
         nargs = f.nargs;
@@ -63,7 +64,7 @@ __global__ void ladder(int32_t *a, int R, long long *cycles, const __grid_consta
       else
         acc += sum;
       if (V >= 4)
-        end_parallel_warp(t, mine);
+        end_parallel_warp(t, mine, f);
       bar_sync(kBarHandoff, nthr);
     }
     if (V < 3)
@@ -151,7 +152,7 @@ int main() {
   run<7>(a, c, R);
   cudaError_t e = cudaDeviceSynchronize();
   printf("status %s\n", cudaGetErrorString(e));
-  int main_product();
+  int main_product(void);
   return main_product();
 }
 
@@ -296,6 +297,18 @@ int main_product() {
     cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
     printf("product kernel (status %d): %7.1f cycles/region inside the master loop\n", s,
            double(h) / R);
+  }
+  // several worker warps: the retire takes the atomic path
+  int32_t *a2;
+  cudaMalloc(&a2, 4 * 1024);
+  cudaMemset(a2, 0, 4 * 1024);
+  for (int w : {64, 96, 224, 480, 992}) {
+    ompds_launch l2{1, w, 20, 0, -1, 0, 0, nullptr};
+    int32_t s = launch_generic<ProbeProg>(&l2, lay, 4, ProbeProg::Args{a2, R, c}, nullptr, nullptr);
+    cudaDeviceSynchronize();
+    long long h = 0;
+    cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+    printf("product kernel W=%d (status %d): %7.1f cycles/region\n", w, s, double(h) / R);
   }
   return 0;
 }

@@ -44,7 +44,7 @@ __global__ void probe(int32_t *a, long long *ts, int variant) {
       long long t2 = clock64();
       a[threadIdx.x] = old + c1 + c2 + c3 + c4;
       long long t3 = clock64();
-      end_parallel_warp(t, mine);
+      end_parallel_warp(t, mine, f);
       long long t4 = clock64();
       if (threadIdx.x == 0) {
         T[0] = t0; T[1] = t1; T[2] = t2; T[3] = t3; T[4] = t4;
