@@ -528,15 +528,30 @@ __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
   f.win = st.win;
   f.workers = st.workers;
   f.status = OMPDS_OK;
+  f.fn = st.fn;
+  f.args = st.args;
+  f.nargs = st.nargs;
+  const uint32_t active = static_cast<uint32_t>(__cvta_generic_to_shared(&t.active_word()));
+  if (__builtin_expect(ph == kStaged && t.events == nullptr, 1)) {
+    // The common case in one branch: a staged region and no event log.
+    // Active += n: a plain store when this warp holds every participant
+    // (Active is 0 between regions and no other warp fetches), otherwise
+    // one fire-and-forget shared atomic.
+    if (m.n == static_cast<uint32_t>(st.workers))
+      asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+                   "@q st.shared.u32 [%0], %1;\n\t}" ::"r"(active), "r"(m.n),
+                   "r"(static_cast<uint32_t>(m.is_leader))
+                   : "memory");
+    else
+      red_add_if(active, m.n, m.is_leader);
+    return f;
+  }
   if (ph == kTerminated) {
     f.fn = -1;
     f.args = nullptr;
     f.nargs = 0;
     return f;
   }
-  f.fn = st.fn;
-  f.args = st.args;
-  f.nargs = st.nargs;
   if (ph != kStaged) {
     f.status = mine ? t.trap(OMPDS_TRAP_PARALLEL_NOT_STAGED) : OMPDS_OK;
     f.fn = -1;
@@ -544,11 +559,7 @@ __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
   }
   if (m.n == 0)
     return f;
-  const uint32_t active = static_cast<uint32_t>(__cvta_generic_to_shared(&t.active_word()));
-  if (t.events == nullptr) { // fast path: one fire-and-forget shared atomic
-    red_add_if(active, m.n, m.is_leader);
-    return f;
-  }
+  // staged, event log on
   int64_t ev = -1;
   if (m.is_leader) {
     atomicAdd(&t.active_word(), m.n);
@@ -586,10 +597,14 @@ __device__ __forceinline__ uint32_t retire_plan(const TeamCtx &t,
 // the reference's schedule (all fetches before any retire) both rules agree.
 __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
                                                   uint32_t plan) {
+  const bool leader = plan & 1u;
+  if (__builtin_expect((plan & 6u) == 6u && t.events == nullptr, 1)) {
+    retire_window_if(t, leader); // sole warp, window list, no event log
+    return;
+  }
   const uint32_t n = plan >> 8;
   if (n == 0)
     return;
-  const bool leader = plan & 1u;
 #ifndef OMPDS_SOLE_WARP_RETIRE
 #define OMPDS_SOLE_WARP_RETIRE 1
 #endif

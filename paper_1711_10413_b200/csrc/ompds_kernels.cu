@@ -198,6 +198,38 @@ struct Master {
   __device__ __forceinline__ int32_t parallel_with(int32_t fn, int32_t nargs,
                                                    AddrOf addr_of) {
     OMPDS_TL(regions, 0);
+    // The common case of prepare_parallel in one branch: every check passes,
+    // the list fits the window and no event log is kept.  Everything else
+    // (traps, a global list, events) takes parallel_general.
+    const PrepareState st = load_prepare_state(t);
+    if (__builtin_expect(st.phase == kIdle && st.active == 0 && nargs >= 0 &&
+                             nargs <= t.prealloc && t.events == nullptr, 1)) {
+      __syncwarp(); // every lane has read the state before the master stages
+      OMPDS_TL(regions, 1);
+      stage_region_if(t, fn, nargs, t.window, leader);
+      const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(t.window));
+      for (int j = static_cast<int>(lane_id()); j < nargs; j += 32)
+        asm volatile("st.shared.u64 [%0], %1;" ::"r"(sa + 8u * j),
+                     "l"(reinterpret_cast<unsigned long long>(addr_of(j)))
+                     : "memory");
+      OMPDS_TL(regions, 2);
+      bar_sync(kBarHandoff, team_threads); // release the workers
+      OMPDS_TL(regions, 3);
+      bar_sync(kBarHandoff, team_threads); // join
+      OMPDS_TL(regions, 4);
+      barriers += 2;
+      regions += 1;
+      return OMPDS_OK;
+    }
+    return parallel_general(fn, nargs, addr_of);
+  }
+
+#ifndef OMPDS_GENERAL_ATTR
+#define OMPDS_GENERAL_ATTR __forceinline__
+#endif
+  template <class AddrOf>
+  __device__ OMPDS_GENERAL_ATTR int32_t parallel_general(int32_t fn, int32_t nargs,
+                                                   AddrOf addr_of) {
     void **list = nullptr;
     unsigned long long packed = 0;
 #ifndef OMPDS_WARP_PREPARE
@@ -251,10 +283,18 @@ struct Master {
     // The reserved warp publishes the pointer list lane-parallel (one
     // coalesced store per 32 entries) instead of nargs scalar stores.
     const int lane = static_cast<int>(lane_id());
-    if (ok && lane < nargs)
-      list[lane] = addr_of(lane);
-    for (int j = lane + 32; ok && j < nargs; j += 32) // lists longer than a warp
-      list[j] = addr_of(j);
+    if (list == t.window) { // the smem window: STS, not generic stores
+      const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(t.window));
+      for (int j = lane; ok && j < nargs; j += 32)
+        asm volatile("st.shared.u64 [%0], %1;" ::"r"(sa + 8u * j),
+                     "l"(reinterpret_cast<unsigned long long>(addr_of(j)))
+                     : "memory");
+    } else {
+      if (ok && lane < nargs)
+        list[lane] = addr_of(lane);
+      for (int j = lane + 32; ok && j < nargs; j += 32) // lists longer than a warp
+        list[j] = addr_of(j);
+    }
     // Released even when prepare trapped (keeps the handoff branch-free):
     // nothing is staged then, workers observe a non-Staged phase and skip.
     OMPDS_TL(regions, 2);
@@ -436,10 +476,22 @@ template <class T> struct RegionsProg {
     // first so its latency overlaps get-shared-variables.
     T *dst = a.a + size_t(w.team) * w.workers + w.wid;
     const T old = w.mine ? *dst : T(0);
-    const int32_t c1 = shared_value<int32_t>(sv, 0);
-    const int32_t c2 = shared_value<int32_t>(sv, 1);
-    const T c3 = shared_value<T>(sv, 2);
-    const T c4 = shared_value<T>(sv, 3);
+    // get-shared-variables: lane j < 4 dereferences capture j once (slots
+    // are 8-byte sized and aligned, so one 8-byte load covers an int or a
+    // T slot), shuffles spread the four values.
+    unsigned long long raw = 0;
+    if (lane_id() < 4 && sv.mine)
+      raw = *static_cast<const unsigned long long *>(sv.mine);
+    const int32_t c1 = __shfl_sync(0xffffffffu, static_cast<int32_t>(raw), 0);
+    const int32_t c2 = __shfl_sync(0xffffffffu, static_cast<int32_t>(raw), 1);
+    T c3, c4;
+    if constexpr (sizeof(T) == 4) {
+      c3 = __builtin_bit_cast(T, __shfl_sync(0xffffffffu, static_cast<uint32_t>(raw), 2));
+      c4 = __builtin_bit_cast(T, __shfl_sync(0xffffffffu, static_cast<uint32_t>(raw), 3));
+    } else {
+      c3 = __builtin_bit_cast(T, __shfl_sync(0xffffffffu, raw, 2));
+      c4 = __builtin_bit_cast(T, __shfl_sync(0xffffffffu, raw, 3));
+    }
     if (w.mine) {
       T sum = (T(c1 + c2) + c3) + c4;
       *dst = old + sum;
