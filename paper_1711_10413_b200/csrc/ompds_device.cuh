@@ -598,11 +598,21 @@ __device__ __forceinline__ uint32_t retire_plan(const TeamCtx &t,
 __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
                                                   uint32_t plan) {
   const bool leader = plan & 1u;
-  if (__builtin_expect((plan & 6u) == 6u && t.events == nullptr, 1)) {
-    retire_window_if(t, leader); // sole warp, window list, no event log
+  const uint32_t n = plan >> 8;
+  if (__builtin_expect((plan & 4u) && t.events == nullptr, 1)) {
+    if (plan & 2u) {
+      retire_window_if(t, leader); // sole warp: it retires the last participant
+    } else {
+      // Several worker warps, window list, no event log: each warp retires
+      // its participants with one fire-and-forget atomic (retired += n,
+      // Active -= n); the join barrier orders every retirement before the
+      // master, which observes retired == W and completes the last
+      // retirement (complete_region) -- no returning atomic on any worker.
+      red_add_if(static_cast<uint32_t>(__cvta_generic_to_shared(&t.active_word())),
+                 (n << 16) - n, leader);
+    }
     return;
   }
-  const uint32_t n = plan >> 8;
   if (n == 0)
     return;
 #ifndef OMPDS_SOLE_WARP_RETIRE
@@ -654,6 +664,26 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
   // no __syncwarp: the join barrier that follows orders the leader's
   // shared-memory updates for every participant
 }
+// Master warp, after the join barrier of a region it staged with the window
+// list and no event log: if the workers retired with fire-and-forget atomics
+// (several worker warps), every retirement is visible now (the join barrier
+// orders them), so the region's last retirement -- Active 0, retired W --
+// is completed here: the team returns to Idle.  Sole-warp regions and
+// regions with a global list or an event log were completed by their last
+// retiring worker (retired count already reset).
+__device__ __forceinline__ bool completes_at_join(const TeamCtx &t, int32_t workers) {
+  return workers > kWarp && t.events == nullptr;
+}
+__device__ __forceinline__ void complete_region(const TeamCtx &t, int32_t workers,
+                                                bool leader) {
+  const uint32_t aw = t.active_word();
+  if ((aw >> 16) == static_cast<uint32_t>(workers) && (aw & 0xffffu) == 0) {
+    __syncwarp(); // every lane has read the word before the master resets it
+    retire_window_if(t, leader);
+    __syncwarp(); // ... and sees the reset in its next prepare checks
+  }
+}
+
 __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
                                                   const WarpMask &m,
                                                   const Fetch &f) {

@@ -131,6 +131,7 @@ struct Master {
   TeamCtx t;
   const TeamParams *p;
   bool leader;
+  bool join_completes; // completes_at_join(): several worker warps, no event log
   uint32_t team_threads;
   int32_t trap = 0;
   int32_t barriers = 0;
@@ -217,6 +218,8 @@ struct Master {
       OMPDS_TL(regions, 3);
       bar_sync(kBarHandoff, team_threads); // join
       OMPDS_TL(regions, 4);
+      if (join_completes)
+        complete_region(t, p->workers, leader);
       barriers += 2;
       regions += 1;
       return OMPDS_OK;
@@ -303,6 +306,8 @@ struct Master {
     bar_sync(kBarHandoff, team_threads); // join
     OMPDS_TL(regions, 4);
     barriers += 2;
+    if (ok && list == t.window && join_completes)
+      complete_region(t, p->workers, leader);
     if (__builtin_expect(!ok, 0)) {
       if (!trap)
         trap = static_cast<int32_t>(packed & 0xffffffffu);
@@ -427,6 +432,7 @@ __global__ void OMPDS_GENERIC_LB
     m.t = t;
     m.p = &p;
     m.leader = lane_id() == 0;
+    m.join_completes = completes_at_join(t, p.workers);
     m.team_threads = team_threads;
     if (m.init() == OMPDS_OK && m.push_depot() == OMPDS_OK)
       Prog::master(m, a);
