@@ -209,10 +209,16 @@ struct Master {
       OMPDS_TL(regions, 1);
       stage_region_if(t, fn, nargs, t.window, leader);
       const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(t.window));
-      for (int j = static_cast<int>(lane_id()); j < nargs; j += 32)
-        asm volatile("st.shared.u64 [%0], %1;" ::"r"(sa + 8u * j),
-                     "l"(reinterpret_cast<unsigned long long>(addr_of(j)))
+      const int lane = static_cast<int>(lane_id());
+      if (lane < nargs) // one predicated STS per lane for lists up to 32 entries
+        asm volatile("st.shared.u64 [%0], %1;" ::"r"(sa + 8u * lane),
+                     "l"(reinterpret_cast<unsigned long long>(addr_of(lane)))
                      : "memory");
+      if (__builtin_expect(nargs > 32, 0)) // windows of more than 32 entries
+        for (int j = lane + 32; j < nargs; j += 32)
+          asm volatile("st.shared.u64 [%0], %1;" ::"r"(sa + 8u * j),
+                       "l"(reinterpret_cast<unsigned long long>(addr_of(j)))
+                       : "memory");
       OMPDS_TL(regions, 2);
       bar_sync(kBarHandoff, team_threads); // release the workers
       OMPDS_TL(regions, 3);
