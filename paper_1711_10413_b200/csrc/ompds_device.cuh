@@ -601,7 +601,11 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
   const uint32_t n = plan >> 8;
   if (__builtin_expect((plan & 4u) && t.events == nullptr, 1)) {
     if (plan & 2u) {
-      retire_window_if(t, leader); // sole warp: it retires the last participant
+      // sole warp: it retires the last participant.  The __syncwarp orders
+      // every lane's fetch reads before the leader's reset (lanes of one
+      // warp are not implicitly ordered under independent thread scheduling).
+      __syncwarp();
+      retire_window_if(t, leader);
     } else {
       // Several worker warps, window list, no event log: each warp retires
       // its participants with one fire-and-forget atomic (retired += n,
@@ -629,6 +633,7 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
       for (uint32_t k = 0; k < n; ++k)
         t.log_at(ev + k, OMPDS_EV_RETIRE, -1, int64_t(n) - int64_t(k + 1), 0);
     }
+    __syncwarp(); // every lane's fetch reads before the leader's reset
     if (plan & 4u)
       retire_window_if(t, leader);
     else if (leader)

@@ -153,6 +153,7 @@ struct Master {
     int32_t s = 0;
     if (leader)
       s = kernel_init(t, kMaster, p->workers);
+    __syncwarp(); // the master's init writes before any lane reads the state
     return sync_status(s);
   }
 
