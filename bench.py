@@ -43,7 +43,7 @@ COEF = [k / 8 for k in range(1, 9)]
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--elements", type=int, default=1 << 28, help="elements per GPU (weak) or in total (strong)")
@@ -105,6 +105,11 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes ~0.1-0.5 s to start: wait for its first sample
+            # so the samples cover the timed region, not the time after it
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 3.0 and self.proc.poll() is None:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
 
@@ -400,7 +405,11 @@ def other_configs(RG, dev, stream, sms):
     for _ in range(10):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
-            flush.sum()  # same stream, still running while e0 and the launch are queued
+            flush.sum()  # same stream
+            # keep the GPU busy (~50 us) while the host enqueues e0, the
+            # launch and e1, so no host-side launch gap lands between e0 and
+            # the kernel (the kernel is ~45 us; a gap would be charged to it)
+            torch.cuda._sleep(100_000)
             e0.record(stream)
             go()
             e1.record(stream)
@@ -469,10 +478,32 @@ def e2e(args, teams, workers, n, dev, world=1):
         t = torch.tensor([ms, wall], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, wall = float(t[0]), float(t[1])
-    return {"value": round(BYTES_PER_ELEM * n * world / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+    value = BYTES_PER_ELEM * n * world / (ms * 1e-3) / 1e9
+    # The host link bounds this path: 16 B/element host->device (x, y) and
+    # 8 B/element device->host (y).  Measure each direction alone (pinned,
+    # one 2 GiB copy, CUDA events); with both directions overlapped the
+    # bound is max(16n/h2d, 8n/d2h).
+    link = {}
+    for name, dst, src in (("h2d", xd, xh), ("d2h", yh, yd)):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            dst.copy_(src, non_blocking=True)  # warm
+            e0.record(stream)
+            dst.copy_(src, non_blocking=True)
+            e1.record(stream)
+        e1.synchronize()
+        link[name] = 8 * n / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    bound_s = max(16 * n / (link["h2d"] * 1e9), 8 * n / (link["d2h"] * 1e9))
+    bound = BYTES_PER_ELEM * n * world / bound_s / 1e9
+    return {"value": round(value, 2), "unit": "GB/s",
             "h2d_bytes_per_step": 16 * n * world, "d2h_bytes_per_step": 8 * n * world,
             "ms_per_step": round(ms, 3), "wall_ms_per_step": round(wall / args.e2e_steps * 1e3, 3),
-            "path": "ompds_run_stream_host (C ABI, pinned host buffers)"}
+            "path": "ompds_run_stream_host (C ABI, pinned host buffers)",
+            "link_roofline": {"bound": "host link (PCIe)", "h2d_GBps": round(link["h2d"], 1),
+                              "d2h_GBps": round(link["d2h"], 1),
+                              "bound_GBps": round(bound, 2), "frac": round(value / bound, 4),
+                              "how": "each direction alone: one pinned 2 GiB copy, CUDA events; "
+                                     "bound = 24n / max(16n/h2d, 8n/d2h)"}}
 
 
 if __name__ == "__main__":
