@@ -226,3 +226,34 @@ def test_config4_full_size_checksum_vs_oracle():
     O.lib().orc_fill(1, O.ptr(ys), n, 0x5eed01ac, 0)
     O.lib().orc_stream(1, n, O.ptr(xs), O.ptr(ys), O.ptr(np.array(COEF)), 0)
     assert got == O.lib().orc_checksum(1, O.ptr(ys), n)
+
+
+# --------------------------------------------------------------------------- config 5
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_config5_shards_on_one_gpu_gather_to_whole_checksum(world):
+    """Config 5 on one GPU: each shard g of the element range runs the region
+    with its own teams on inputs generated for [lo, hi) (first = lo, as each
+    rank of bench.py does); the shards' checksums summed mod 2^64 -- what the
+    all-reduce gathers -- equal the oracle's whole-range checksum, and every
+    element equals the unsharded oracle bit for bit."""
+    from paper_1711_10413_b200 import sharding
+    n = (1 << 22) + 13
+    teams_total = 148 * 8
+    parts, total = [], 0
+    for g in range(world):
+        lo, hi = sharding.shard_range(n, g, world)
+        x, y = _f64_inputs(hi - lo, first=lo)
+        teams = max(1, sharding.shard_range(teams_total, g, world)[1]
+                    - sharding.shard_range(teams_total, g, world)[0])
+        out = RG.run_stream(x, y, COEF, teams, 96)
+        assert all(s.trap == 0 and s.regions == 1 for s in out.team_stats())
+        total = (total + RG.checksum(y)) & sharding.MASK64
+        parts.append(y.cpu().numpy())
+    xs = np.empty(n)
+    ys = np.empty(n)
+    O.lib().orc_fill(1, O.ptr(xs), n, 0x5eed01ab, 0)
+    O.lib().orc_fill(1, O.ptr(ys), n, 0x5eed01ac, 0)
+    O.lib().orc_stream(1, n, O.ptr(xs), O.ptr(ys), O.ptr(np.array(COEF)), 0)
+    assert total == O.lib().orc_checksum(1, O.ptr(ys), n)
+    assert np.array_equal(np.concatenate(parts).view(np.uint64), ys.view(np.uint64))
