@@ -311,8 +311,10 @@ def main():
     e1.record(stream)
     e1.synchronize()
     ns_per_region = e0.elapsed_time(e1) * 1e6 / R
-    # the same protocol on every SM: 8 teams/SM x 32 workers, 2000 regions each
-    R2, teams2 = 2000, sms * 8
+    # the same protocol on every SM: 16 teams/SM x 32 workers, 2000 regions
+    # each (tools/agg_sweep.py: 8/SM 2.6, 16/SM 4.3 G regions/s; more teams
+    # than the register limit's 19/SM run in two waves)
+    R2, teams2 = 2000, sms * 16
     a2 = torch.zeros(teams2 * 32, dtype=torch.int32, device=dev)
     RG.run_regions(a2, teams2, 32, 10, stream=stream)
     e0.record(stream)
