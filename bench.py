@@ -334,7 +334,8 @@ def main():
         c2["roofline_frac"] = round(c2["GBps"] / peak, 4)
     roofline = {"bound": "hbm", "achieved": round(value / world, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(value / world / peak, 4), "traffic": None,
-                "peak_source": peak_src,
+                "peak_source": peak_src, "peak_nominal": 8000.0,
+                "frac_nominal": round(value / world / 8000.0, 4),
                 "algorithmic_bytes_per_launch": BYTES_PER_ELEM * n}
     tr = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr):
@@ -426,23 +427,27 @@ def other_configs(RG, dev, stream, sms):
         "roofline_frac": None,
         "l2": "evicted before every launch by reading a 256 MB buffer"}
     del a, flush
-    # config 3: nested regions (depth 3) on per-warp data-sharing stacks
+    # config 3: nested regions (depth 3) on per-warp data-sharing stacks;
+    # "overflow": a zero-byte shared-memory slot puts every frame on the
+    # warp's global overflow chain (the placement decision's other side)
     R = 2000
-    for teams in (1, sms * 8):
+    for key, teams, slot in (("config3_nested_1team", 1, 2048),
+                             ("config3_nested_full", sms * 8, 2048),
+                             ("config3_nested_1team_overflow", 1, 0)):
         a3 = torch.zeros(teams * 96, dtype=torch.float64, device=dev)
-        RG.run_nested(a3, teams, 96, 10, stream=stream)
+        RG.run_nested(a3, teams, 96, 10, warp_slot_bytes=slot, stream=stream)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        _, stacks = RG.run_nested(a3, teams, 96, R, stream=stream)
+        _, stacks = RG.run_nested(a3, teams, 96, R, warp_slot_bytes=slot, stream=stream)
         e1.record(stream)
         e1.synchronize()
         ms = e0.elapsed_time(e1)
-        key = "config3_nested_1team" if teams == 1 else "config3_nested_full"
         out[key] = {"teams": teams, "workers": 96, "regions": R,
                     "ns_per_region": round(ms * 1e6 / R, 1),
                     "aggregate_regions_per_s": round(teams * R / (ms * 1e-3), 0),
                     "stack_depth": stacks[0][0].max_depth,
-                    "frames_in_smem": stacks[0][0].frame_in_smem}
+                    "frames_in_smem": stacks[0][0].frame_in_smem,
+                    "warp_slot_bytes": slot}
     return out
 
 
