@@ -1,0 +1,102 @@
+// reduction_region.cu -- a user-defined region program on the B200 runtime.
+//
+// What a compiler targeting this runtime would emit for
+//
+//   #pragma omp target teams map(to: x[0:n]) map(from: out[0:2*teams])
+//   {
+//     long sum = 0, thr, cnt = 0;              // kernel locals, captured below
+//     #pragma omp parallel                     // region 0 shares {sum}
+//     { long s = 0; for (i = mine) s += x[i];  #pragma omp atomic  sum += s; }
+//     thr = sum / n_team;                       // sequential code reads sum
+//     #pragma omp parallel                     // region 1 shares {thr, cnt}
+//     { long c = 0; for (i = mine) c += x[i] > thr;  #pragma omp atomic  cnt += c; }
+//     out[2*team] = sum; out[2*team+1] = cnt;
+//   }
+//
+// The three locals are implicitly shared: they live in the team's depot in
+// shared memory, the workers reach them through get-shared-variables, and
+// their writes (the atomics) are what the master reads after each join --
+// the data-sharing semantics of arXiv 1711.10413 end to end.  Each team
+// reduces its own contiguous slice of x; the host checks every team's sum
+// and count against numpy (tests/test_example_region.py).
+//
+// Built by paper_1711_10413_b200/build.py into _build/libompds_example.so
+// against the runtime headers and libompds_b200.so.
+#include "ompds_generic.cuh"
+
+namespace {
+
+using namespace ompds;
+
+struct ReductionProg {
+  struct Args {
+    const int32_t *x;
+    int64_t n;
+    long long *out; // 2 per team: sum, count above the team's mean
+  };
+  __device__ static void team_range(const Args &a, int64_t *lo, int64_t *hi) {
+    *lo = a.n * blockIdx.x / gridDim.x;
+    *hi = a.n * (blockIdx.x + 1) / gridDim.x;
+  }
+  __device__ static void master(Master &m, const Args &a) {
+    long long *sum = reinterpret_cast<long long *>(m.cap(0));
+    long long *thr = reinterpret_cast<long long *>(m.cap(1));
+    long long *cnt = reinterpret_cast<long long *>(m.cap(2));
+    if (m.leader) {
+      *sum = 0;
+      *cnt = 0;
+    }
+    __syncwarp();
+    if (m.parallel(0, 1) != OMPDS_OK) // shares {sum}
+      return;
+    int64_t lo, hi;
+    team_range(a, &lo, &hi);
+    if (m.leader) // sequential code between the regions reads the shared sum
+      *thr = hi > lo ? *sum / (hi - lo) : 0;
+    __syncwarp();
+    if (m.parallel_with(1, 2, [&](int j) -> void * { return m.cap(1 + j); }) !=
+        OMPDS_OK) // shares {thr, cnt}
+      return;
+    if (m.leader) {
+      a.out[2 * blockIdx.x] = *sum;
+      a.out[2 * blockIdx.x + 1] = *cnt;
+    }
+  }
+  __device__ static void region(int32_t fn, const SharedVars &sv, Worker &w,
+                                const Args &a) {
+    int64_t lo, hi;
+    team_range(a, &lo, &hi);
+    long long *s0 = static_cast<long long *>(sv.get(0));
+    long long *s1 = static_cast<long long *>(sv.get(1));
+    long long part = 0;
+    if (fn == 0) {
+      for (int64_t i = lo + w.wid; w.mine && i < hi; i += w.workers)
+        part += a.x[i];
+    } else {
+      const long long thr = *s0;
+      for (int64_t i = lo + w.wid; w.mine && i < hi; i += w.workers)
+        part += a.x[i] > thr ? 1 : 0;
+    }
+    for (int o = 16; o > 0; o >>= 1)
+      part += __shfl_xor_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0) // one atomic per warp on the shared variable
+      atomicAdd(reinterpret_cast<unsigned long long *>(fn == 0 ? s0 : s1),
+                static_cast<unsigned long long>(part));
+  }
+};
+
+} // namespace
+
+extern "C" int32_t example_reduction(const ompds_launch *launch, const int32_t *x,
+                                     int64_t n, long long *out,
+                                     ompds_team_stats *stats) {
+  if (!x || !out || n < 0)
+    return OMPDS_ERR_INVALID;
+  FixedLayout lay;
+  // kernel frame group: sum, thr, cnt (captured, 8 B each), then
+  // __omp_worker's wf.addr / args.addr -- 40 B, team footprint 249 B
+  const int32_t s = build_fixed_layout({8, 8, 8}, 0, &lay);
+  if (s)
+    return s;
+  return launch_generic<ReductionProg>(launch, lay, 3, {x, n, out}, stats, nullptr);
+}

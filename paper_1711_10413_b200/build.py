@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_build")
 LIB = os.path.join(OUT_DIR, "libompds_b200.so")
 SOURCES = [os.path.join(CSRC, "ompds_kernels.cu"), os.path.join(CSRC, "ompds_host.cpp")]
-HEADERS = [os.path.join(CSRC, "ompds_device.cuh"),
+HEADERS = [os.path.join(CSRC, "ompds_device.cuh"), os.path.join(CSRC, "ompds_generic.cuh"),
            os.path.join(os.path.dirname(HERE), "include", "ompds.h")]
 
 NVCC_FLAGS = [
@@ -43,8 +43,30 @@ def _stale() -> bool:
     return any(os.path.getmtime(s) > t for s in SOURCES + HEADERS)
 
 
+EXAMPLE_SRC = os.path.join(os.path.dirname(HERE), "examples", "reduction_region.cu")
+EXAMPLE_LIB = os.path.join(OUT_DIR, "libompds_example.so")
+
+
+def build_example(force: bool = False) -> str:
+    """examples/reduction_region.cu: a user-defined region program compiled
+    against the runtime headers and linked to libompds_b200.so."""
+    if not force and os.path.exists(EXAMPLE_LIB) and all(
+            os.path.getmtime(f) <= os.path.getmtime(EXAMPLE_LIB)
+            for f in [EXAMPLE_SRC, LIB] + HEADERS):
+        return EXAMPLE_LIB
+    cmd = [nvcc()] + NVCC_FLAGS + ["-I", CSRC, "-o", EXAMPLE_LIB + ".tmp", EXAMPLE_SRC,
+                                   "-L", OUT_DIR, "-lompds_b200", "-Xlinker", "-rpath,$ORIGIN"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"nvcc failed ({res.returncode}) building {EXAMPLE_LIB}")
+    os.replace(EXAMPLE_LIB + ".tmp", EXAMPLE_LIB)
+    return EXAMPLE_LIB
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
+        build_example()
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
     tmp = LIB + ".tmp"
@@ -59,6 +81,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         sys.stderr.write(log)
     os.replace(tmp, LIB)
+    build_example(force=True)
     return LIB
 
 

@@ -12,440 +12,9 @@
 // termination release (the reference's "master death" release,
 // Simulator.cpp:475-478, is an explicit barrier with a null-work sentinel
 // here because exited threads never arrive at a hardware barrier).
-#include "ompds_device.cuh"
-
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <cstdio>
-#include <cstring>
-#include <mutex>
-#include <vector>
+#include "ompds_generic.cuh"
 
 namespace ompds {
-
-thread_local char g_last_error[512] = "";
-
-static int32_t cuda_fail(cudaError_t e, const char *what) {
-  std::snprintf(g_last_error, sizeof(g_last_error), "%s: %s", what,
-                cudaGetErrorString(e));
-  return OMPDS_ERR_CUDA;
-}
-#define OMPDS_CUDA(call)                                                       \
-  do {                                                                         \
-    cudaError_t e_ = (call);                                                   \
-    if (e_ != cudaSuccess)                                                     \
-      return cuda_fail(e_, #call);                                             \
-  } while (0)
-
-//===----------------------------------------------------------------------===//
-// Launch parameters shared by every generic-mode kernel.
-//===----------------------------------------------------------------------===//
-
-#ifndef OMPDS_GENERIC_LB
-#define OMPDS_GENERIC_LB __launch_bounds__(1024, 1)
-#endif
-
-constexpr int kMaxCaptures = 32;
-
-// Region timeline (tools/timeline.cu only): clock64 stamps of the master's
-// and worker warp 0's steps for the first OMPDS_TIMELINE regions of team 0.
-#ifdef OMPDS_TIMELINE
-__device__ long long g_timeline[OMPDS_TIMELINE][16];
-__device__ __forceinline__ long long tl_clock() {
-  long long c; // volatile + memory clobber: stays between the barriers
-  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c)::"memory");
-  return c;
-}
-#define OMPDS_TL(r, k)                                                         \
-  do {                                                                         \
-    const long long c_ = tl_clock();                                           \
-    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (r) < OMPDS_TIMELINE)    \
-      g_timeline[(r)][(k)] = c_;                                               \
-  } while (0)
-#else
-#define OMPDS_TL(r, k)                                                         \
-  do {                                                                         \
-  } while (0)
-#endif
-
-struct TeamParams {
-  int32_t workers;       // W
-  int32_t prealloc;      // PreallocEntries
-  int32_t fail_dyn;
-  int32_t max_events;
-  int64_t depot_cap;     // master data-sharing slot in smem (bytes, 8-aligned)
-  int64_t total_shared;  // the layout's depot size (frame pushed by master)
-  unsigned char *slabs;  // teams * slab_bytes of global memory
-  uint32_t slab_bytes;
-  int32_t n_caps;
-  ompds_event *events;   // teams * max_events, or nullptr
-  ompds_team_stats *stats;
-  int64_t cap_off[kMaxCaptures]; // depot offsets of the captures (layout)
-  int64_t aux_off;       // depot offset of the sequential loop counter (-1)
-  int64_t warp_slot_bytes;       // per-warp data-sharing slot in smem
-  unsigned char *warp_ovf;       // teams * worker_warps * warp_ovf_bytes
-  int64_t warp_ovf_bytes;
-};
-
-// Depot accessors for the master's sequential code (see Master::with_depot).
-struct SmemDepot {
-  uint32_t base;        // shared-window address of the depot frame
-  unsigned char *gbase; // the same frame as a generic pointer
-  __device__ __forceinline__ void *ptr(int64_t off) const { return gbase + off; }
-  template <class T> __device__ __forceinline__ T ld(int64_t off) const {
-    static_assert(sizeof(T) == 4 || sizeof(T) == 8, "4/8-byte slots");
-    if constexpr (sizeof(T) == 4) {
-      uint32_t v;
-      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(base + uint32_t(off)) : "memory");
-      return __builtin_bit_cast(T, v);
-    } else {
-      unsigned long long v;
-      asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(base + uint32_t(off)) : "memory");
-      return __builtin_bit_cast(T, v);
-    }
-  }
-  template <class T> __device__ __forceinline__ void st(int64_t off, T x) const {
-    if constexpr (sizeof(T) == 4)
-      asm volatile("st.shared.b32 [%0], %1;" ::"r"(base + uint32_t(off)),
-                   "r"(__builtin_bit_cast(uint32_t, x)) : "memory");
-    else
-      asm volatile("st.shared.b64 [%0], %1;" ::"r"(base + uint32_t(off)),
-                   "l"(__builtin_bit_cast(unsigned long long, x)) : "memory");
-  }
-};
-struct GlobalDepot {
-  unsigned char *gbase;
-  __device__ __forceinline__ void *ptr(int64_t off) const { return gbase + off; }
-  template <class T> __device__ __forceinline__ T ld(int64_t off) const {
-    return *reinterpret_cast<const volatile T *>(gbase + off);
-  }
-  template <class T> __device__ __forceinline__ void st(int64_t off, T x) const {
-    *reinterpret_cast<volatile T *>(gbase + off) = x;
-  }
-};
-
-// Master-warp view of the sequential region.  Every lane runs it; lane 0
-// (the master) commits side effects.
-struct Master {
-  TeamCtx t;
-  const TeamParams *p;
-  bool leader;
-  bool join_completes; // completes_at_join(): several worker warps, no event log
-  uint32_t team_threads;
-  int32_t trap = 0;
-  int32_t barriers = 0;
-  int32_t regions = 0;
-  DsStack ds;
-  Frame depot;
-
-  __device__ __forceinline__ int32_t sync_status(int32_t s) {
-    s = __shfl_sync(0xffffffffu, s, 0);
-    if (s && !trap) {
-      trap = s;
-      if (leader)
-        t.trap(s);
-    }
-    return s;
-  }
-
-  __device__ __forceinline__ int32_t init() {
-    int32_t s = 0;
-    if (leader)
-      s = kernel_init(t, kMaster, p->workers);
-    __syncwarp(); // the master's init writes before any lane reads the state
-    return sync_status(s);
-  }
-
-  // The kernel frame group's depot is the first frame of the master's
-  // data-sharing stack: the shared-memory slot when it fits, else the
-  // team's global overflow chain (placement decision of config 2).
-  __device__ __forceinline__ int32_t push_depot() {
-    unsigned char *ovf = t.slab ? t.slab + (t.slab_bytes / 2) : nullptr;
-    ds.init(t.region, p->depot_cap, ovf, t.slab_bytes / 2);
-    depot = ds.push(p->total_shared, 1);
-    if (depot.status == OMPDS_OK && !depot.in_smem) {
-      // zero-fill like pushActivation (Simulator.cpp:453-456); smem was
-      // zeroed in the prologue.
-      for (int64_t i = lane_id() * 8; i < p->total_shared; i += 32 * 8)
-        *reinterpret_cast<uint64_t *>(depot.base + i) = 0;
-      __syncwarp();
-    }
-    return sync_status(depot.status);
-  }
-
-  __device__ __forceinline__ unsigned char *cap(int j) const {
-    return depot.base + p->cap_off[j];
-  }
-
-  // Runs the sequential code `f(depot)` with a depot accessor that issues
-  // shared-memory instructions (LDS/STS, 32-bit addresses) when the depot
-  // frame is in the smem slot, generic ones when it is on the global chain.
-  template <class F> __device__ __forceinline__ void with_depot(F &&f) {
-    if (depot.in_smem)
-      f(SmemDepot{static_cast<uint32_t>(__cvta_generic_to_shared(depot.base)),
-                  depot.base});
-    else
-      f(GlobalDepot{depot.base});
-  }
-
-  // prepare_parallel + publish &capture_j into the list + release + join.
-  __device__ __forceinline__ int32_t parallel(int32_t fn, int32_t nargs) {
-    return parallel_with(fn, nargs, [this](int j) -> void * {
-      return cap(j < kMaxCaptures ? j : 0);
-    });
-  }
-
-  template <class AddrOf>
-  __device__ __forceinline__ int32_t parallel_with(int32_t fn, int32_t nargs,
-                                                   AddrOf addr_of) {
-    OMPDS_TL(regions, 0);
-    // The common case of prepare_parallel in one branch: every check passes,
-    // the list fits the window and no event log is kept.  Everything else
-    // (traps, a global list, events) takes parallel_general.
-    const PrepareState st = load_prepare_state(t);
-    if (__builtin_expect(st.phase == kIdle && st.active == 0 && nargs >= 0 &&
-                             nargs <= t.prealloc && t.events == nullptr, 1)) {
-      __syncwarp(); // every lane has read the state before the master stages
-      OMPDS_TL(regions, 1);
-      stage_region_if(t, fn, nargs, t.window, leader);
-      const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(t.window));
-      const int lane = static_cast<int>(lane_id());
-      if (lane < nargs) // one predicated STS per lane for lists up to 32 entries
-        asm volatile("st.shared.u64 [%0], %1;" ::"r"(sa + 8u * lane),
-                     "l"(reinterpret_cast<unsigned long long>(addr_of(lane)))
-                     : "memory");
-      if (__builtin_expect(nargs > 32, 0)) // windows of more than 32 entries
-        for (int j = lane + 32; j < nargs; j += 32)
-          asm volatile("st.shared.u64 [%0], %1;" ::"r"(sa + 8u * j),
-                       "l"(reinterpret_cast<unsigned long long>(addr_of(j)))
-                       : "memory");
-      OMPDS_TL(regions, 2);
-      bar_sync(kBarHandoff, team_threads); // release the workers
-      OMPDS_TL(regions, 3);
-      bar_sync(kBarHandoff, team_threads); // join
-      OMPDS_TL(regions, 4);
-      if (join_completes)
-        complete_region(t, p->workers, leader);
-      barriers += 2;
-      regions += 1;
-      return OMPDS_OK;
-    }
-    return parallel_general(fn, nargs, addr_of);
-  }
-
-#ifndef OMPDS_GENERAL_ATTR
-#define OMPDS_GENERAL_ATTR __forceinline__
-#endif
-  template <class AddrOf>
-  __device__ OMPDS_GENERAL_ATTR int32_t parallel_general(int32_t fn, int32_t nargs,
-                                                   AddrOf addr_of) {
-    void **list = nullptr;
-    unsigned long long packed = 0;
-#ifndef OMPDS_WARP_PREPARE
-#define OMPDS_WARP_PREPARE 1
-#endif
-#if OMPDS_WARP_PREPARE
-    // Every lane evaluates prepare_parallel's phase checks on broadcast
-    // loads, so the window case needs no shuffle from the master lane; only
-    // a global list (nargs > PreallocEntries) is allocated by the master and
-    // shuffled.  The __syncwarp orders every lane's reads before the
-    // master's staging writes.
-    {
-      const PrepareState st = load_prepare_state(t);
-      int32_t s = prepare_check(st.phase, st.active, nargs);
-      list = t.window;
-      if (s == OMPDS_OK && nargs > t.prealloc) {
-        if (leader) {
-          list = alloc_args_list(t, fn, nargs);
-          packed = list ? reinterpret_cast<unsigned long long>(list)
-                        : (static_cast<unsigned long long>(OMPDS_TRAP_ARGS_ALLOC_FAILED) |
-                           (1ull << 63));
-        }
-        packed = __shfl_sync(0xffffffffu, packed, 0);
-        if (packed >> 63)
-          s = static_cast<int32_t>(packed & 0xffffffffu);
-        list = reinterpret_cast<void **>(packed);
-      } else if (s == OMPDS_OK && leader && t.events) {
-        alloc_args_list(t, fn, nargs); // the window: logs PreparePrealloc
-      }
-      __syncwarp();
-      OMPDS_TL(regions, 1);
-      stage_region_if(t, fn, static_cast<int32_t>(nargs), list, leader && s == OMPDS_OK);
-      if (__builtin_expect(s != OMPDS_OK, 0) && leader)
-        t.trap(s); // the team's first trap, before any worker can record one
-      packed = s ? (static_cast<unsigned long long>(s) | (1ull << 63))
-                 : reinterpret_cast<unsigned long long>(list);
-    }
-#else
-    if (leader) {
-      const int32_t s = prepare_parallel(t, kMaster, fn, nargs, &list);
-      if (s)
-        t.trap(s); // the team's first trap, before any worker can record one
-      // one shuffle carries the list, or the trap code with bit 63 set
-      packed = s ? (static_cast<unsigned long long>(s) | (1ull << 63))
-                 : reinterpret_cast<unsigned long long>(list);
-    }
-    packed = __shfl_sync(0xffffffffu, packed, 0);
-#endif
-    const bool ok = (packed >> 63) == 0;
-    list = reinterpret_cast<void **>(packed);
-    // The reserved warp publishes the pointer list lane-parallel (one
-    // coalesced store per 32 entries) instead of nargs scalar stores.
-    const int lane = static_cast<int>(lane_id());
-    if (list == t.window) { // the smem window: STS, not generic stores
-      const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(t.window));
-      for (int j = lane; ok && j < nargs; j += 32)
-        asm volatile("st.shared.u64 [%0], %1;" ::"r"(sa + 8u * j),
-                     "l"(reinterpret_cast<unsigned long long>(addr_of(j)))
-                     : "memory");
-    } else {
-      if (ok && lane < nargs)
-        list[lane] = addr_of(lane);
-      for (int j = lane + 32; ok && j < nargs; j += 32) // lists longer than a warp
-        list[j] = addr_of(j);
-    }
-    // Released even when prepare trapped (keeps the handoff branch-free):
-    // nothing is staged then, workers observe a non-Staged phase and skip.
-    OMPDS_TL(regions, 2);
-    bar_sync(kBarHandoff, team_threads); // release the workers
-    OMPDS_TL(regions, 3);
-    bar_sync(kBarHandoff, team_threads); // join
-    OMPDS_TL(regions, 4);
-    barriers += 2;
-    if (ok && list == t.window && join_completes)
-      complete_region(t, p->workers, leader);
-    if (__builtin_expect(!ok, 0)) {
-      if (!trap)
-        trap = static_cast<int32_t>(packed & 0xffffffffu);
-      return trap;
-    }
-    regions += 1;
-    return OMPDS_OK;
-  }
-
-  __device__ __forceinline__ void finish() {
-    int32_t s = 0;
-    if (leader)
-      s = kernel_deinit(t, kMaster);
-    sync_status(s);
-    if (leader && p->stats) {
-      ompds_team_stats st{};
-      st.trap = trap ? trap : t.at<int32_t>(Rt::kTrap);
-      st.master_barriers = barriers;
-      st.barrier_releases = barriers + 1;
-      st.regions = regions;
-      st.dynamic_alloc_bytes = t.at<uint32_t>(Rt::kDynBytes);
-      st.dynamic_allocs = static_cast<int32_t>(t.at<uint32_t>(Rt::kDynAllocs));
-      st.dynamic_frees = static_cast<int32_t>(t.at<uint32_t>(Rt::kDynFrees));
-      st.depot_in_smem = depot.in_smem;
-      st.depot_offset = depot.offset;
-      st.n_events = static_cast<int32_t>(t.at<uint32_t>(Rt::kEvents));
-      st.smem_bytes = team_region_bytes(p->depot_cap, p->prealloc);
-      if (p->warp_slot_bytes > 0)
-        st.smem_bytes = round_up(st.smem_bytes, 16) +
-                        int64_t(team_threads / 32 - 1) * p->warp_slot_bytes;
-      p->stats[blockIdx.x] = st;
-    }
-    __syncwarp();
-    // Termination release: workers parked at await.work observe Terminated
-    // (the null work function) and leave their loop.
-    bar_sync(kBarHandoff, team_threads);
-  }
-};
-
-// Worker-side context handed to region bodies.
-struct Worker {
-  int32_t wid;  // omp_get_thread_num
-  bool mine;    // wid < W (padding lanes of the last worker warp idle)
-  int32_t team;
-  int32_t teams;
-  int32_t workers;
-  int32_t warp;
-  DsStack ds;   // this warp's data-sharing stack (nested regions)
-  const TeamCtx *t;
-  void **args;  // the fetched shared-args list
-  int32_t nargs;
-};
-
-template <class Prog>
-__global__ void OMPDS_GENERIC_LB
-    generic_mode_kernel(const __grid_constant__ TeamParams p,
-                        const __grid_constant__ typename Prog::Args a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const uint32_t team_threads = blockDim.x;
-  const int warp = threadIdx.x >> 5;
-  const int worker_warps = static_cast<int>(team_threads >> 5) - 1;
-
-  TeamCtx t = make_team(
-      smem, p.depot_cap, p.prealloc, p.fail_dyn,
-      p.slabs ? p.slabs + size_t(blockIdx.x) * p.slab_bytes : nullptr,
-      p.slab_bytes,
-      p.events ? p.events + size_t(blockIdx.x) * p.max_events : nullptr,
-      p.max_events);
-  // Prologue: zero the team region (Simulator.cpp:286), runtime span last.
-  const int64_t region = team_region_bytes(p.depot_cap, p.prealloc);
-  for (int64_t i = threadIdx.x; i < region; i += team_threads)
-    smem[i] = 0;
-  __syncthreads();
-  if (threadIdx.x == 0)
-    t.work_fn() = -1;
-  __syncthreads();
-
-  if (warp < worker_warps) {
-    Worker w;
-    w.wid = threadIdx.x;
-    w.mine = w.wid < p.workers;
-    w.team = blockIdx.x;
-    w.teams = gridDim.x;
-    w.workers = p.workers;
-    w.warp = warp;
-    w.t = &t;
-    w.args = nullptr;
-    w.nargs = 0;
-    // Per-warp data-sharing stack: a statically sized slot after the team
-    // region, then this warp's slice of the global overflow chain.
-    unsigned char *slot = smem + round_up(region, 16) + int64_t(warp) * p.warp_slot_bytes;
-    unsigned char *ovf =
-        p.warp_ovf ? p.warp_ovf + (size_t(blockIdx.x) * worker_warps + warp) * p.warp_ovf_bytes
-                   : nullptr;
-    w.ds.init(slot, p.warp_slot_bytes, ovf, p.warp_ovf ? p.warp_ovf_bytes : 0);
-    const WarpMask wm = WarpMask::of(w.mine); // loop-invariant participation
-    for (int32_t rr = 0;; ++rr) {
-      bar_sync(kBarHandoff, team_threads); // await.work
-      OMPDS_TL(rr, 5);
-      Fetch f = begin_parallel_warp(t, wm, w.mine);
-      OMPDS_TL(rr, 6);
-      if (f.fn < 0) {
-        if (f.status == OMPDS_OK)
-          break; // termination sentinel (wf == null)
-        bar_sync(kBarHandoff, team_threads); // trapped fetch: skip the region
-        continue;
-      }
-      w.args = f.args;
-      w.nargs = f.nargs;
-      const uint32_t plan = retire_plan(t, wm, f);
-      SharedVars sv = get_shared_variables(t, f);
-      OMPDS_TL(rr, 7);
-      Prog::region(f.fn, sv, w, a);
-      OMPDS_TL(rr, 8);
-      end_parallel_warp(t, plan);
-      OMPDS_TL(rr, 9);
-      bar_sync(kBarHandoff, team_threads); // barrier.parallel (join)
-      OMPDS_TL(rr, 10);
-    }
-  } else {
-    Master m;
-    m.t = t;
-    m.p = &p;
-    m.leader = lane_id() == 0;
-    m.join_completes = completes_at_join(t, p.workers);
-    m.team_threads = team_threads;
-    if (m.init() == OMPDS_OK && m.push_depot() == OMPDS_OK)
-      Prog::master(m, a);
-    m.finish();
-  }
-}
 
 //===----------------------------------------------------------------------===//
 // Config 1: latency -- R regions sharing 4 scalars (2 int, 2 elem).
@@ -1154,158 +723,9 @@ __global__ void checksum_kernel(const T *data, int64_t n,
   }
 }
 
-//===----------------------------------------------------------------------===//
-// Host side: workspace, layouts for the fixed configs, launch helpers.
-//===----------------------------------------------------------------------===//
-
-// Library-owned global memory reused across launches on a device: buffer 0
-// holds the teams' overflow slabs (args lists, master depot overflow),
-// buffer 1 the worker warps' data-sharing overflow chains, buffer 2 a region
-// program's tables, buffer 3 the masters' local depot mirrors.  Launches
-// that run concurrently on different streams must not share a device.
-struct Workspace {
-  std::mutex mu;
-  int device = -1;
-  unsigned char *buf[4] = {nullptr, nullptr, nullptr, nullptr};
-  size_t bytes[4] = {0, 0, 0, 0};
-};
-static Workspace g_ws;
-
-static int32_t ensure_buffer(int which, size_t bytes, unsigned char **out) {
-  std::lock_guard<std::mutex> lk(g_ws.mu);
-  int dev = 0;
-  OMPDS_CUDA(cudaGetDevice(&dev));
-  if (g_ws.device != dev) {
-    for (int i = 0; i < 4; ++i) { // leaked on device switch (bounded, rare)
-      g_ws.buf[i] = nullptr;
-      g_ws.bytes[i] = 0;
-    }
-    g_ws.device = dev;
-  }
-  if (g_ws.bytes[which] < bytes) {
-    if (g_ws.buf[which]) {
-      OMPDS_CUDA(cudaDeviceSynchronize());
-      OMPDS_CUDA(cudaFree(g_ws.buf[which]));
-    }
-    g_ws.buf[which] = nullptr;
-    OMPDS_CUDA(cudaMalloc(&g_ws.buf[which], bytes));
-    g_ws.bytes[which] = bytes;
-  }
-  *out = g_ws.buf[which];
-  return OMPDS_OK;
-}
-
 } // namespace ompds
 
 using namespace ompds;
-
-// Host layout builder (ompds_host.cpp).
-extern "C" int32_t ompds_layout_build(const ompds_frame_var *, int32_t, int32_t,
-                                      int32_t, ompds_depot_layout *,
-                                      ompds_depot_slot *, int32_t, int32_t *,
-                                      int32_t);
-
-namespace {
-
-// Kernel frame group of a fixed config, in the reference's emission order:
-// captured locals, then sequential loop counters, then __omp_worker's
-// wf.addr / args.addr (Codegen.cpp:413-430, LoweringPasses.cpp:264-305).
-struct FixedLayout {
-  int64_t total_shared = 0;
-  int64_t cap_off[kMaxCaptures] = {};
-  int64_t aux_off = -1;
-};
-
-int32_t build_fixed_layout(const std::vector<int64_t> &cap_bytes,
-                           int64_t aux_bytes, FixedLayout *out) {
-  std::vector<ompds_frame_var> vars;
-  for (int64_t b : cap_bytes)
-    vars.push_back({0, 0, OMPDS_VAR_ESCAPES, -1, b, -1, -1});
-  if (aux_bytes > 0)
-    vars.push_back({0, 0, 0, -1, aux_bytes, -1, -1});
-  vars.push_back({0, 1, OMPDS_VAR_PINNED, -1, 8, -1, -1}); // wf.addr
-  vars.push_back({0, 1, OMPDS_VAR_PINNED, -1, 8, -1, -1}); // args.addr
-  ompds_depot_layout lay{};
-  ompds_depot_slot slots[kMaxCaptures + 4];
-  int32_t owners[kMaxCaptures + 4];
-  int32_t s = ompds_layout_build(vars.data(), static_cast<int32_t>(vars.size()),
-                                 1, OMPDS_PIPELINE_DEFAULT, &lay, slots,
-                                 kMaxCaptures + 4, owners, kMaxCaptures + 4);
-  if (s)
-    return s;
-  out->total_shared = lay.total_shared;
-  // Without merges every var owns its slot, in order.
-  for (size_t j = 0; j < cap_bytes.size(); ++j)
-    out->cap_off[j] = slots[j].offset;
-  if (aux_bytes > 0)
-    out->aux_off = slots[cap_bytes.size()].offset;
-  return OMPDS_OK;
-}
-
-int32_t validate_launch(const ompds_launch *l) {
-  if (!l || l->teams <= 0 || l->workers <= 0 || l->workers > 992 ||
-      l->prealloc_entries < 0 || l->prealloc_entries > 4096)
-    return OMPDS_ERR_INVALID;
-  return OMPDS_OK;
-}
-
-constexpr uint32_t kSlabBytes = 8192; // per team: args lists + depot overflow
-
-template <class Prog>
-int32_t launch_generic(const ompds_launch *l, const FixedLayout &lay,
-                       int32_t n_caps, const typename Prog::Args &args,
-                       ompds_team_stats *stats, ompds_event *events,
-                       int64_t warp_slot_bytes = 0, int64_t warp_ovf_bytes = 0) {
-  int32_t s = validate_launch(l);
-  if (s)
-    return s;
-  int ndev = 0;
-  OMPDS_CUDA(cudaGetDeviceCount(&ndev));
-  TeamParams p{};
-  p.workers = l->workers;
-  p.prealloc = l->prealloc_entries;
-  p.fail_dyn = l->fail_dynamic_alloc;
-  p.max_events = l->log_events ? l->max_events : 0;
-  p.total_shared = lay.total_shared;
-  p.depot_cap = l->depot_capacity < 0 ? lay.total_shared
-                                      : round_up(l->depot_capacity, 8);
-  p.events = l->log_events ? events : nullptr;
-  p.stats = stats;
-  p.n_caps = n_caps;
-  for (int j = 0; j < kMaxCaptures; ++j)
-    p.cap_off[j] = lay.cap_off[j];
-  p.aux_off = lay.aux_off;
-  p.slab_bytes = std::max<uint32_t>(
-      kSlabBytes, static_cast<uint32_t>(round_up(2 * lay.total_shared + 64, 256)));
-  s = ensure_buffer(0, size_t(p.slab_bytes) * l->teams, &p.slabs);
-  if (s)
-    return s;
-  const int threads = static_cast<int>(round_up(l->workers, 32)) + 32;
-  const int worker_warps = threads / 32 - 1;
-  p.warp_slot_bytes = round_up(warp_slot_bytes, 16);
-  p.warp_ovf_bytes = round_up(warp_ovf_bytes, 256);
-  if (p.warp_ovf_bytes > 0) {
-    s = ensure_buffer(1, size_t(p.warp_ovf_bytes) * worker_warps * l->teams, &p.warp_ovf);
-    if (s)
-      return s;
-  }
-  size_t smem = static_cast<size_t>(team_region_bytes(p.depot_cap, p.prealloc));
-  if (p.warp_slot_bytes > 0)
-    smem = static_cast<size_t>(round_up(int64_t(smem), 16) + worker_warps * p.warp_slot_bytes);
-  if (smem > 227 * 1024)
-    return OMPDS_ERR_INVALID;
-  auto kern = generic_mode_kernel<Prog>;
-  if (smem > 48 * 1024)
-    OMPDS_CUDA(cudaFuncSetAttribute(kern,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-  cudaStream_t st = static_cast<cudaStream_t>(l->stream);
-  kern<<<l->teams, threads, smem, st>>>(p, args);
-  OMPDS_CUDA(cudaGetLastError());
-  return OMPDS_OK;
-}
-
-} // namespace
 
 extern "C" {
 

@@ -1,0 +1,63 @@
+"""A user-defined region program (examples/reduction_region.cu) compiled
+against the runtime headers: two parallel regions per team share kernel
+locals by reference -- the workers' atomics on the shared `sum` / `cnt` are
+what the master reads after each join, and the master's write of `thr`
+between the regions is what the second region's workers read."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+from paper_1711_10413_b200 import _lib as L
+from paper_1711_10413_b200 import build as B
+
+
+def lib():
+    path = B.build_example()
+    lb = C.CDLL(path)
+    lb.example_reduction.argtypes = [C.POINTER(L.Launch), C.c_void_p, C.c_int64, C.c_void_p,
+                                     C.c_void_p]
+    lb.example_reduction.restype = C.c_int32
+    return lb
+
+
+def test_example_library_exports_its_entry_point():
+    lb = lib()
+    assert hasattr(lb, "example_reduction")
+    assert os.path.basename(B.EXAMPLE_LIB) == "libompds_example.so"
+
+
+def _expected(x, teams):
+    n = len(x)
+    out = []
+    for t in range(teams):
+        lo, hi = n * t // teams, n * (t + 1) // teams
+        s = int(x[lo:hi].astype(np.int64).sum())
+        c = hi - lo
+        thr = 0 if c == 0 else (abs(s) // c) * (1 if s >= 0 else -1)  # C division
+        out += [s, int((x[lo:hi].astype(np.int64) > thr).sum())]
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("teams,workers,n", [(1, 32, 1000), (4, 96, 100_003), (296, 480, 1 << 22),
+                                             (3, 1, 17)])
+def test_example_region_program_matches_numpy(teams, workers, n):
+    import torch
+    from paper_1711_10413_b200 import regions as RG
+    x = torch.empty(n, dtype=torch.int32, device="cuda")
+    RG.fill_uniform(x, 0x5eed01ab)
+    out = torch.zeros(2 * teams, dtype=torch.int64, device="cuda")
+    res = RG.Outputs(teams, x.device, 0)
+    launch = RG.make_launch(teams, workers)
+    L.check(lib().example_reduction(C.byref(launch), C.c_void_p(x.data_ptr()), n,
+                                    C.c_void_p(out.data_ptr()), res.stats_ptr()),
+            "example_reduction")
+    torch.cuda.synchronize()
+    assert out.cpu().tolist() == _expected(x.cpu().numpy(), teams)
+    for st in res.team_stats():
+        # two regions: 4 master barriers, 5 releases; team region = the
+        # 40-byte depot + 160 B window + 49 B runtime span
+        assert (st.trap, st.master_barriers, st.barrier_releases, st.regions) == (0, 4, 5, 2)
+        assert st.smem_bytes == 40 + 160 + 49 and st.depot_in_smem
