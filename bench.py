@@ -322,6 +322,24 @@ def main():
     e1.record(stream)
     e1.synchronize()
     agg_regions_per_s = teams2 * R2 / (e0.elapsed_time(e1) * 1e-3)
+    # where the shared-args list lives (PAPER.md: the shared-memory list vs
+    # the malloc back-up scheme, "as large as an order of magnitude"): the
+    # 4-capture region with the 20-entry window, with a 2-entry window so the
+    # list spills to the team's global slab, and spilled to device malloc
+    placement = {}
+    for name, pe, alloc in (("window", 20, 0), ("global_slab", 2, 0), ("device_malloc", 2, 1)):
+        row = {}
+        for label, tm, rr in (("1team", 1, 2000), ("full", sms * 16, 200)):
+            ap = torch.zeros(tm * 32, dtype=torch.int32, device=dev)
+            RG.run_regions(ap, tm, 32, 10, prealloc_entries=pe, list_allocator=alloc, stream=stream)
+            e0.record(stream)
+            RG.run_regions(ap, tm, 32, rr, prealloc_entries=pe, list_allocator=alloc, stream=stream)
+            e1.record(stream)
+            e1.synchronize()
+            ms_p = e0.elapsed_time(e1)
+            row[f"ns_per_region_{label}"] = round(ms_p * 1e6 / rr, 1)
+            row[f"regions_per_s_{label}"] = round(tm * rr / (ms_p * 1e-3), 0)
+        placement[name] = row
     configs = other_configs(RG, dev, stream, sms) if rank == 0 else {}
     from paper_1711_10413_b200 import occupancy as OCC
     regs = ptxas_regs("StreamProgIdE") or 64
@@ -362,7 +380,8 @@ def main():
                     "workload": "config 1: 1 team x 32 workers, 4 shared scalars, "
                                 f"{R} regions in a sequential loop",
                     "aggregate_regions_per_s": round(agg_regions_per_s, 0),
-                    "aggregate_workload": f"{teams2} teams x 32 workers x {R2} regions"},
+                    "aggregate_workload": f"{teams2} teams x 32 workers x {R2} regions",
+                    "args_list_placement": placement},
         "smem_bytes_per_cta": smem_bytes,
         "smem_layout": "depot 80 + args window 160 + runtime span 49 (reference footprint 289)",
         "regs_per_thread": regs,

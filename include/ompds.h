@@ -267,7 +267,16 @@ typedef struct ompds_launch {
   int32_t log_events;       /* record per-team runtime events             */
   int32_t max_events;       /* per-team event capacity when logging       */
   void *stream;             /* cudaStream_t (NULL = default stream)       */
+  int32_t list_allocator;   /* where args lists past the window live:
+                               OMPDS_LIST_SLAB (0, default) a per-team
+                               global slab, LIFO; OMPDS_LIST_MALLOC (1)
+                               device malloc/free per region -- the
+                               paper's fallback (PAPER.md "back-up scheme") */
+  int32_t reserved0;        /* must be 0                                  */
 } ompds_launch;
+
+#define OMPDS_LIST_SLAB 0
+#define OMPDS_LIST_MALLOC 1
 
 typedef struct ompds_team_stats { /* per team, written by the kernel */
   int32_t trap;                   /* first trap code, 0 = none            */

@@ -35,6 +35,7 @@ EVENT_KIND_NAMES = ["init", "prepare_prealloc", "prepare_dynamic", "fetch", "ret
 VAR_ESCAPES, VAR_PINNED = 1, 2
 PIPELINE_DEFAULT, PIPELINE_O0, PIPELINE_BAD_ORDER = range(3)
 ELEM_I32, ELEM_F64 = 0, 1
+LIST_SLAB, LIST_MALLOC = 0, 1
 
 
 class RuntimeConfig(C.Structure):
@@ -92,7 +93,8 @@ class Occupancy(C.Structure):
 class Launch(C.Structure):
     _fields_ = [("teams", C.c_int32), ("workers", C.c_int32), ("prealloc_entries", C.c_int32),
                 ("fail_dynamic_alloc", C.c_int32), ("depot_capacity", C.c_int64),
-                ("log_events", C.c_int32), ("max_events", C.c_int32), ("stream", C.c_void_p)]
+                ("log_events", C.c_int32), ("max_events", C.c_int32), ("stream", C.c_void_p),
+                ("list_allocator", C.c_int32), ("reserved0", C.c_int32)]
 
 
 class TeamStats(C.Structure):

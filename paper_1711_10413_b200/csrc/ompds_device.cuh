@@ -136,6 +136,7 @@ struct TeamCtx {
   int32_t fail_dyn;        // FailDynamicAlloc
   ompds_event *events;     // per-team event log (nullptr: off)
   int32_t max_events;
+  int32_t list_malloc;     // args lists past the window: 1 device malloc, 0 slab
 
   template <class T> __device__ __forceinline__ T &at(int off) const {
     return *reinterpret_cast<T *>(rt + off);
@@ -199,6 +200,20 @@ struct TeamCtx {
     at<uint32_t>(Rt::kHeapTop) =
         static_cast<uint32_t>(static_cast<unsigned char *>(p) - slab);
   }
+  // An args list that does not fit the window: the team slab (default), or
+  // -- OMPDS_LIST_MALLOC, the paper's back-up scheme -- device malloc, freed
+  // by the last retirement.
+  __device__ __forceinline__ void *list_alloc(int64_t bytes) const {
+    if (list_malloc)
+      return malloc(static_cast<size_t>(bytes));
+    return slab_alloc(bytes);
+  }
+  __device__ __forceinline__ void list_free(void *p) const {
+    if (list_malloc)
+      free(p);
+    else
+      slab_free(p);
+  }
 };
 
 // Carves the team region out of dynamic shared memory and zero-initialises
@@ -208,7 +223,8 @@ __device__ __forceinline__ TeamCtx make_team(unsigned char *smem,
                                              int fail_dyn, unsigned char *slab,
                                              uint32_t slab_bytes,
                                              ompds_event *events,
-                                             int max_events) {
+                                             int max_events,
+                                             int list_malloc = 0) {
   TeamCtx t;
   t.region = smem;
   t.depot_cap = depot_cap;
@@ -220,6 +236,7 @@ __device__ __forceinline__ TeamCtx make_team(unsigned char *smem,
   t.fail_dyn = fail_dyn;
   t.events = events;
   t.max_events = max_events;
+  t.list_malloc = list_malloc;
   return t;
 }
 
@@ -330,7 +347,7 @@ __device__ __forceinline__ void **alloc_args_list(const TeamCtx &t, int32_t fn,
     return t.window;
   }
   const int64_t bytes = nargs * OMPDS_SHARED_ARG_ENTRY_BYTES;
-  void *p = t.fail_dyn ? nullptr : t.slab_alloc(bytes);
+  void *p = t.fail_dyn ? nullptr : t.list_alloc(bytes);
   if (p == nullptr)
     return nullptr;
   t.at<uint32_t>(Rt::kDynAllocs) += 1;
@@ -393,7 +410,7 @@ __device__ inline int32_t kernel_parallel(const TeamCtx &t, int role,
 __device__ __forceinline__ void retire_last(const TeamCtx &t) {
   if (t.args_dynamic()) {
     int64_t bytes = int64_t(t.nargs()) * OMPDS_SHARED_ARG_ENTRY_BYTES;
-    t.slab_free(t.args());
+    t.list_free(t.args());
     t.at<uint32_t>(Rt::kDynFrees) += 1;
     t.log(OMPDS_EV_DYNAMIC_FREE, -1, 0, bytes);
   }

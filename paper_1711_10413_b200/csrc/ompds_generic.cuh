@@ -89,6 +89,7 @@ struct TeamParams {
   int64_t warp_slot_bytes;       // per-warp data-sharing slot in smem
   unsigned char *warp_ovf;       // teams * worker_warps * warp_ovf_bytes
   int64_t warp_ovf_bytes;
+  int32_t list_malloc;           // OMPDS_LIST_MALLOC
 };
 
 // Depot accessors for the master's sequential code (see Master::with_depot).
@@ -385,7 +386,7 @@ __global__ void OMPDS_GENERIC_LB
       p.slabs ? p.slabs + size_t(blockIdx.x) * p.slab_bytes : nullptr,
       p.slab_bytes,
       p.events ? p.events + size_t(blockIdx.x) * p.max_events : nullptr,
-      p.max_events);
+      p.max_events, p.list_malloc);
   // Prologue: zero the team region (Simulator.cpp:286), runtime span last.
   const int64_t region = team_region_bytes(p.depot_cap, p.prealloc);
   for (int64_t i = threadIdx.x; i < region; i += team_threads)
@@ -529,7 +530,9 @@ inline int32_t build_fixed_layout(const std::vector<int64_t> &cap_bytes,
 
 inline int32_t validate_launch(const ompds_launch *l) {
   if (!l || l->teams <= 0 || l->workers <= 0 || l->workers > 992 ||
-      l->prealloc_entries < 0 || l->prealloc_entries > 4096)
+      l->prealloc_entries < 0 || l->prealloc_entries > 4096 ||
+      (l->list_allocator != OMPDS_LIST_SLAB && l->list_allocator != OMPDS_LIST_MALLOC) ||
+      l->reserved0 != 0)
     return OMPDS_ERR_INVALID;
   return OMPDS_OK;
 }
@@ -555,6 +558,7 @@ int32_t launch_generic(const ompds_launch *l, const FixedLayout &lay,
   p.depot_cap = l->depot_capacity < 0 ? lay.total_shared
                                       : round_up(l->depot_capacity, 8);
   p.events = l->log_events ? events : nullptr;
+  p.list_malloc = l->list_allocator == OMPDS_LIST_MALLOC;
   p.stats = stats;
   p.n_caps = n_caps;
   for (int j = 0; j < kMaxCaptures; ++j)

@@ -257,3 +257,32 @@ def test_config5_shards_on_one_gpu_gather_to_whole_checksum(world):
     O.lib().orc_stream(1, n, O.ptr(xs), O.ptr(ys), O.ptr(np.array(COEF)), 0)
     assert total == O.lib().orc_checksum(1, O.ptr(ys), n)
     assert np.array_equal(np.concatenate(parts).view(np.uint64), ys.view(np.uint64))
+
+
+# --------------------------------------------------------------------------- list allocators
+
+@pytest.mark.parametrize("allocator", [0, 1])
+@pytest.mark.parametrize("teams,workers,log", [(3, 40, True), (148, 32, False), (2, 96, False)])
+def test_args_lists_past_the_window_slab_and_malloc(allocator, teams, workers, log):
+    """4 captures with a 2-entry window: every region's list goes to global
+    memory -- the team slab or device malloc (the paper's back-up scheme) --
+    and is freed by the last retirement; values, barrier counts and the
+    allocation statistics are the reference's either way."""
+    from paper_1711_10413_b200 import _lib as L
+    regions = 5
+    a = torch.zeros(teams * workers, dtype=torch.int32, device=DEV)
+    out = RG.run_regions(a, teams, workers, regions, prealloc_entries=2,
+                         max_events=1024 if log else 0, list_allocator=allocator)
+    want = np.zeros(teams * workers, dtype=np.int32)
+    O.lib().orc_regions(0, teams, workers, regions, O.ptr(want))
+    assert np.array_equal(a.cpu().numpy(), want)
+    for t, st in enumerate(out.team_stats()):
+        assert (st.trap, st.master_barriers, st.barrier_releases, st.regions) == \
+            (0, 2 * regions, 2 * regions + 1, regions)
+        assert (st.dynamic_allocs, st.dynamic_frees, st.dynamic_alloc_bytes) == \
+            (regions, regions, regions * 32)
+        if log:
+            ev = canon(out.team_events()[t])
+            assert sum(1 for e in ev if e[0] == "prepare_dynamic") == regions
+            assert sum(1 for e in ev if e[0] == "dynamic_free") == regions
+    assert L.LIST_MALLOC == allocator or allocator == L.LIST_SLAB

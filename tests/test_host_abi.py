@@ -42,7 +42,7 @@ def test_struct_sizes_match_the_c_abi():
     assert C.sizeof(P.FrameVar) == 32
     assert C.sizeof(P.DepotSlot) == 32
     assert C.sizeof(P.DepotLayout) == 32
-    assert C.sizeof(P.Launch) == 40
+    assert C.sizeof(P.Launch) == 48
     assert C.sizeof(P.TeamStats) == 56
 
 
