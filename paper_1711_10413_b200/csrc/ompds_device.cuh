@@ -687,23 +687,20 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
   // shared-memory updates for every participant
 }
 // Master warp, after the join barrier of a region it staged with the window
-// list and no event log: if the workers retired with fire-and-forget atomics
-// (several worker warps), every retirement is visible now (the join barrier
-// orders them), so the region's last retirement -- Active 0, retired W --
-// is completed here: the team returns to Idle.  Sole-warp regions and
-// regions with a global list or an event log were completed by their last
-// retiring worker (retired count already reset).
+// list and no event log, when the workers retired with fire-and-forget
+// atomics (several worker warps): the region was staged successfully, so
+// every one of the W workers fetched it and retired before arriving at the
+// join, and the join barrier orders all of those retirements before this
+// point -- retired == W and Active == 0 hold.  The master completes the
+// region's last retirement (the team returns to Idle) without re-reading
+// the word.  Sole-warp regions, global lists and logged regions were
+// completed by their last retiring worker.
 __device__ __forceinline__ bool completes_at_join(const TeamCtx &t, int32_t workers) {
   return workers > kWarp && t.events == nullptr;
 }
-__device__ __forceinline__ void complete_region(const TeamCtx &t, int32_t workers,
-                                                bool leader) {
-  const uint32_t aw = t.active_word();
-  if ((aw >> 16) == static_cast<uint32_t>(workers) && (aw & 0xffffu) == 0) {
-    __syncwarp(); // every lane has read the word before the master resets it
-    retire_window_if(t, leader);
-    __syncwarp(); // ... and sees the reset in its next prepare checks
-  }
+__device__ __forceinline__ void complete_region(const TeamCtx &t, bool leader) {
+  retire_window_if(t, leader);
+  __syncwarp(); // every lane sees the reset in its next prepare checks
 }
 
 __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,

@@ -230,7 +230,7 @@ struct Master {
       bar_sync(kBarHandoff, team_threads); // join
       OMPDS_TL(regions, 4);
       if (join_completes)
-        complete_region(t, p->workers, leader);
+        complete_region(t, leader);
       barriers += 2;
       regions += 1;
       return OMPDS_OK;
@@ -318,7 +318,7 @@ struct Master {
     OMPDS_TL(regions, 4);
     barriers += 2;
     if (ok && list == t.window && join_completes)
-      complete_region(t, p->workers, leader);
+      complete_region(t, leader);
     if (__builtin_expect(!ok, 0)) {
       if (!trap)
         trap = static_cast<int32_t>(packed & 0xffffffffu);
