@@ -461,6 +461,28 @@ def other_configs(RG, dev, stream, sms):
     alone = statistics.median(queued(False) for _ in range(3))
     ms_queued = (both - alone) / K
     ms = ms_single
+    # the placement decision's other side: a zero-byte depot slot puts the
+    # kernel frame (d[] included) on the master's global overflow chain;
+    # the reserved warp copies d[] there and the body reads it from L1/L2
+    st_o = RG.run_shared_array(a, t2, w2, d_init=d_init, depot_capacity=0,
+                               stream=stream).team_stats()[0]
+    go_o = RG.prepared_shared_array(a, t2, w2, d_init=d_init, stream=stream, depot_capacity=0)
+    times_o = []
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            flush.sum()
+            torch.cuda._sleep(100_000)
+            e0.record(stream)
+            go_o()
+            e1.record(stream)
+        e1.synchronize()
+        times_o.append(e0.elapsed_time(e1))
+    ms_o = statistics.median(times_o)
+    out["config2_shared_array_overflow"] = {
+        "elements": n2, "teams": t2, "workers": w2, "ms": round(ms_o, 4),
+        "GBps": round(16 * n2 / ms_o / 1e6, 1), "depot_capacity": 0,
+        "depot_in_smem": st_o.depot_in_smem, "smem_bytes_per_cta": st_o.smem_bytes}
     out["config2_shared_array"] = {
         "elements": n2, "teams": t2, "workers": w2, "ms": round(ms, 4),
         "GBps": round(16 * n2 / ms / 1e6, 1), "bytes_per_element": 16,

@@ -164,11 +164,12 @@ def run_nested(a: torch.Tensor, teams: int, workers: int, regions: int,
 
 def prepared_shared_array(a: torch.Tensor, teams: int, workers: int,
                           d_init: Optional[torch.Tensor] = None,
-                          stream: Optional[torch.cuda.Stream] = None):
+                          stream: Optional[torch.cuda.Stream] = None,
+                          depot_capacity: int = -1):
     """A zero-argument callable that only issues the config-2 launch (all
     arguments marshalled up front), for timing without host overhead."""
     _require_cuda(a)
-    launch = make_launch(teams, workers, stream=stream)
+    launch = make_launch(teams, workers, stream=stream, depot_capacity=depot_capacity)
     dp = C.c_void_p(d_init.data_ptr()) if d_init is not None else None
     ap = C.c_void_p(a.data_ptr())
     fn = L.lib().ompds_run_shared_array
