@@ -327,7 +327,7 @@ def compile_program(ast: dict, layouts: Sequence[dict], kernel_root: str, teams:
 
 def run_program(prog: Program, buffers, prealloc_entries: int = L.DEFAULT_PREALLOC_ENTRIES,
                 fail_dynamic_alloc: bool = False, depot_capacity: int = -1,
-                max_events: int = 0, stream=None):
+                max_events: int = 0, stream=None, list_allocator: int = L.LIST_SLAB):
     """Launches the program: `buffers` are int32 CUDA tensors, one per mapped
     array, in host declaration order.  Returns regions.Outputs."""
     import torch
@@ -354,7 +354,8 @@ def run_program(prog: Program, buffers, prealloc_entries: int = L.DEFAULT_PREALL
                      total_local=prog.total_local, priv_bytes=prog.priv_bytes)
     out = RG.Outputs(prog.teams, buffers[0].device if buffers else "cuda", max_events)
     launch = RG.make_launch(prog.teams, prog.workers, prealloc_entries, fail_dynamic_alloc,
-                            depot_capacity, max_events > 0, max_events, stream)
+                            depot_capacity, max_events > 0, max_events, stream,
+                            list_allocator)
     L.check(L.lib().ompds_run_program(C.byref(launch), C.byref(desc), out.stats_ptr(),
                                       out.events_ptr()), "ompds_run_program")
     return out

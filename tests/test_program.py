@@ -259,3 +259,37 @@ def test_gpu_out_of_bounds_traps():
     a = torch.zeros(16, dtype=torch.int32, device="cuda")
     out = PG.run_program(prog, [a])
     assert any(s.trap == 20 for s in out.team_stats())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prealloc,allocator", [(64, 0), (33, 0), (0, 0), (20, 1)])
+def test_gpu_window_sizes_and_allocators_keep_reference_outputs(prealloc, allocator):
+    """The 32- and 64-capture corpus programs with windows of 64 (every list
+    in shared memory, 2 entries per publishing lane), 33, 0 (every list in
+    global memory) entries, and with device-malloc lists: outputs and barrier
+    counts stay the reference's; only the allocation statistics follow the
+    window (DeviceRuntime.cpp:61-74: dynamic iff nargs > PreallocEntries)."""
+    import torch
+    checked = 0
+    for p in programs():
+        if p["stem"] not in ("scalars_32", "scalars_64", "shared_scalar", "mixed_captures"):
+            continue
+        for t, w, run in launches(p)[:2]:
+            prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], t, w)
+            bufs = [torch.full((sz,), init, dtype=torch.int32, device="cuda")
+                    for _, sz, init in prog.buffers]
+            out = PG.run_program(prog, bufs, prealloc_entries=prealloc,
+                                 list_allocator=allocator)
+            sim = run["sim"]
+            for (name, _, _), b in zip(prog.buffers, bufs):
+                assert b.cpu().tolist() == sim["globals"][name], (p["stem"], prealloc, name)
+            st = out.team_stats()
+            assert [s.trap for s in st] == [0] * t
+            assert [s.master_barriers for s in st] == sim["master_barrier_entries"]
+            nregions = [len(r.captures) for r in prog.regions]
+            dyn = sum(1 for n in nregions if n > prealloc)
+            for s in st:
+                assert s.dynamic_allocs == s.dynamic_frees
+                assert s.dynamic_allocs >= dyn and (dyn > 0 or s.dynamic_allocs == 0)
+            checked += 1
+    assert checked >= 4
