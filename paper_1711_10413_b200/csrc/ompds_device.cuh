@@ -781,29 +781,32 @@ __device__ __forceinline__ T shared_value(const SharedVars &v, int j) {
 
 struct Frame {
   unsigned char *base; // lane 0's frame (lane l: base + l*bytes_per_lane)
-  int64_t offset;      // offset inside its segment
+  int32_t offset;      // offset inside its segment, -1: none
   int32_t in_smem;     // 1: shared-memory slot, 0: global overflow chain
   int32_t status;
 };
 
+// Offsets and sizes are 32-bit (a slot is at most 227 KB, a chain slice is
+// sized by the launcher): the push/pop bookkeeping is a handful of 32-bit
+// register operations, no 64-bit arithmetic on the region's critical path.
 struct DsStack {
   unsigned char *slot; // shared-memory slot (generic address)
-  int64_t slot_cap;
-  int64_t top;         // bytes used in the slot
   unsigned char *ovf;  // global overflow chain for this warp
-  int64_t ovf_cap;
-  int64_t ovf_top;     // bytes used on the chain
+  uint32_t slot_cap;
+  uint32_t top;        // bytes used in the slot
+  uint32_t ovf_cap;
+  uint32_t ovf_top;    // bytes used on the chain
   int32_t depth;
   int32_t max_depth;
-  int64_t high_water;  // max bytes in use (slot + chain)
+  uint32_t high_water; // max bytes in use (slot + chain)
 
   __device__ __forceinline__ void init(unsigned char *s, int64_t cap,
                                        unsigned char *o, int64_t ocap) {
     slot = s;
-    slot_cap = cap;
+    slot_cap = static_cast<uint32_t>(cap < 0 ? 0 : cap > 0x7fffffff ? 0x7fffffff : cap);
     top = 0;
     ovf = o;
-    ovf_cap = ocap;
+    ovf_cap = static_cast<uint32_t>(ocap < 0 ? 0 : ocap > 0x7fffffff ? 0x7fffffff : ocap);
     ovf_top = 0;
     depth = 0;
     max_depth = 0;
@@ -813,16 +816,20 @@ struct DsStack {
   // __kmpc_data_sharing_push_stack(bytes_per_lane * lanes)
   __device__ __forceinline__ Frame push(int64_t bytes_per_lane, int lanes) {
     Frame f;
-    const int64_t need = round_up(bytes_per_lane * lanes, 8);
+    const int64_t want = bytes_per_lane * lanes;
+    // frames over 2 GB cannot fit anywhere: overflow
+    const uint32_t need = want < 0 || want > 0x7ffffff0
+                              ? 0xffffffffu
+                              : (static_cast<uint32_t>(want) + 7u) & ~7u;
     f.status = OMPDS_OK;
-    if (ovf_top == 0 && top + need <= slot_cap) {
+    if (ovf_top == 0 && need <= slot_cap - top) {
       f.base = slot + top;
-      f.offset = top;
+      f.offset = static_cast<int32_t>(top);
       f.in_smem = 1;
       top += need;
-    } else if (ovf != nullptr && ovf_top + need <= ovf_cap) {
+    } else if (ovf != nullptr && need <= ovf_cap - ovf_top) {
       f.base = ovf + ovf_top;
-      f.offset = ovf_top;
+      f.offset = static_cast<int32_t>(ovf_top);
       f.in_smem = 0;
       ovf_top += need;
     } else {
@@ -844,14 +851,15 @@ struct DsStack {
   __device__ __forceinline__ int32_t pop(const Frame &f) {
     if (depth <= 0 || f.offset < 0)
       return OMPDS_TRAP_STACK_UNDERFLOW;
+    const uint32_t off = static_cast<uint32_t>(f.offset);
     if (f.in_smem) {
-      if (ovf_top != 0 || f.offset > top)
+      if (ovf_top != 0 || off > top)
         return OMPDS_TRAP_STACK_UNDERFLOW;
-      top = f.offset;
+      top = off;
     } else {
-      if (f.offset > ovf_top)
+      if (off > ovf_top)
         return OMPDS_TRAP_STACK_UNDERFLOW;
-      ovf_top = f.offset;
+      ovf_top = off;
     }
     --depth;
     return OMPDS_OK;

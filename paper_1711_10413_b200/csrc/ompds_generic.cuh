@@ -370,6 +370,7 @@ struct Worker {
   const TeamCtx *t;
   void **args;  // the fetched shared-args list
   int32_t nargs;
+  int32_t region_index; // regions this warp ran before the current one
 };
 
 template <class Prog>
@@ -428,6 +429,7 @@ __global__ void OMPDS_GENERIC_LB
       }
       w.args = f.args;
       w.nargs = f.nargs;
+      w.region_index = rr;
       const uint32_t plan = retire_plan(t, wm, f);
       SharedVars sv = get_shared_variables(t, f);
       OMPDS_TL(rr, 7);

@@ -404,7 +404,9 @@ template <class T> struct NestedProg {
     }
   done:
     __syncwarp();
-    if (lane == 0 && a.wstats) {
+    // the warp's stack statistics: after its last region, or at a failure
+    const int32_t st_any = f1.status | f2.status | s1 | s2;
+    if (lane == 0 && a.wstats && (w.region_index == a.regions - 1 || st_any != OMPDS_OK)) {
       ompds_warp_stack_stats st;
       st.frame_in_smem[0] = f1.in_smem;
       st.frame_in_smem[1] = f2.in_smem;
