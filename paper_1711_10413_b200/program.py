@@ -358,4 +358,5 @@ def run_program(prog: Program, buffers, prealloc_entries: int = L.DEFAULT_PREALL
                             list_allocator)
     L.check(L.lib().ompds_run_program(C.byref(launch), C.byref(desc), out.stats_ptr(),
                                       out.events_ptr()), "ompds_run_program")
+    out.used_on(stream)
     return out

@@ -63,6 +63,17 @@ def make_launch(teams: int, workers: int, prealloc_entries: int = L.DEFAULT_PREA
                     C.c_void_p(s), list_allocator, 0)
 
 
+def _used_on(stream: Optional[torch.cuda.Stream], *ts) -> None:
+    """Buffers allocated on the current stream and written by a launch on a
+    side stream: tell the caching allocator, so a buffer the caller drops
+    is not handed out again while the launch still writes it."""
+    if stream is None or stream.cuda_stream == torch.cuda.current_stream().cuda_stream:
+        return
+    for t in ts:
+        if t is not None:
+            t.record_stream(stream)
+
+
 class Outputs:
     """Device buffers for per-team statistics and event logs."""
 
@@ -72,6 +83,9 @@ class Outputs:
         self.stats = torch.zeros(teams * STATS_DTYPE_BYTES, dtype=torch.uint8, device=device)
         self.events = (torch.zeros(max(teams * max_events, 1) * EVENT_BYTES, dtype=torch.uint8,
                                    device=device) if max_events else None)
+
+    def used_on(self, stream: Optional[torch.cuda.Stream]) -> None:
+        _used_on(stream, self.stats, self.events)
 
     def stats_ptr(self):
         return C.c_void_p(self.stats.data_ptr())
@@ -112,6 +126,7 @@ def run_regions(a: torch.Tensor, teams: int, workers: int, regions: int, **kw) -
     L.check(L.lib().ompds_run_regions(C.byref(launch), ELEM[a.dtype], regions,
                                       C.c_void_p(a.data_ptr()), out.stats_ptr(),
                                       out.events_ptr()), "ompds_run_regions")
+    out.used_on(kw.get("stream"))
     return out
 
 
@@ -126,6 +141,7 @@ def run_shared_array(a: torch.Tensor, teams: int, workers: int,
     L.check(L.lib().ompds_run_shared_array(C.byref(launch), ELEM[a.dtype], a.numel(),
                                            C.c_void_p(a.data_ptr()), dp, out.stats_ptr(),
                                            out.events_ptr()), "ompds_run_shared_array")
+    out.used_on(kw.get("stream"))
     return out
 
 
@@ -154,6 +170,9 @@ def run_nested(a: torch.Tensor, teams: int, workers: int, regions: int,
                                      warp_overflow_bytes, C.c_void_p(a.data_ptr()),
                                      out.stats_ptr(), C.c_void_p(ws.data_ptr()),
                                      out.events_ptr()), "ompds_run_nested")
+    out.used_on(kw.get("stream"))
+    _used_on(kw.get("stream"), ws)
+    torch.cuda.synchronize(a.device)  # the launch may be on another stream
     raw = bytes(ws.cpu().numpy().tobytes())
     arr = (L.WarpStackStats * (teams * warps)).from_buffer_copy(raw)
     stacks = [[WarpStack([bool(x) for x in s.frame_in_smem], list(s.frame_offset), s.status,
@@ -200,6 +219,8 @@ def run_stream(x: torch.Tensor, y: torch.Tensor, coef, teams: int, workers: int,
                                      C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), cb,
                                      out.stats_ptr() if out else None,
                                      out.events_ptr() if out else None), "ompds_run_stream")
+    if out is not None:
+        out.used_on(kw.get("stream"))
     return out
 
 

@@ -91,3 +91,17 @@ def test_gpu_nested_overflow_chain_exhausted():
     assert st == 18
     assert all(ws.status == 18 for t in stacks for ws in t)
     assert torch.count_nonzero(a).item() == 0  # the nested body never ran
+
+
+@pytest.mark.gpu
+def test_gpu_nested_stack_statistics_on_a_side_stream():
+    """The warp statistics are written by each warp's last region; reading
+    them must wait for a launch issued on another stream."""
+    import torch
+    from paper_1711_10413_b200 import regions as RG
+    a = torch.zeros(96, dtype=torch.float64, device="cuda")
+    _, stacks = RG.run_nested(a, 1, 96, 300, stream=torch.cuda.Stream())
+    st, ins, off, md, hw = predict_stack(2048, 4096, 40, 8)
+    for ws in stacks[0]:
+        assert ws.status == 0 and ws.max_depth == md == 2
+        assert ws.frame_in_smem == [bool(x) for x in ins] and ws.frame_offset == off
