@@ -272,6 +272,12 @@ typedef struct ompds_launch {
                                global slab, LIFO; OMPDS_LIST_MALLOC (1)
                                device malloc/free per region -- the
                                paper's fallback (PAPER.md "back-up scheme") */
+  int32_t first_team;       /* team range [first_team, first_team+teams)
+                               of a grid of total_teams (0: total = teams):
+                               omp_get_team_num() / omp_get_num_teams()
+                               of the launched CTAs, so a team grid can be
+                               sharded across GPUs by range             */
+  int32_t total_teams;
   int32_t reserved0;        /* must be 0                                  */
 } ompds_launch;
 

@@ -90,6 +90,8 @@ struct TeamParams {
   unsigned char *warp_ovf;       // teams * worker_warps * warp_ovf_bytes
   int64_t warp_ovf_bytes;
   int32_t list_malloc;           // OMPDS_LIST_MALLOC
+  int32_t first_team;            // omp_get_team_num() of CTA 0
+  int32_t total_teams;           // omp_get_num_teams()
 };
 
 // Depot accessors for the master's sequential code (see Master::with_depot).
@@ -362,8 +364,10 @@ struct Master {
 struct Worker {
   int32_t wid;  // omp_get_thread_num
   bool mine;    // wid < W (padding lanes of the last worker warp idle)
-  int32_t team;
-  int32_t teams;
+  int32_t team;  // omp_get_team_num (first_team + CTA index)
+  int32_t teams; // omp_get_num_teams (the whole grid, across shards)
+  int32_t local_team;  // CTA index in this launch
+  int32_t local_teams; // CTAs in this launch
   int32_t workers;
   int32_t warp;
   DsStack ds;   // this warp's data-sharing stack (nested regions)
@@ -401,8 +405,10 @@ __global__ void OMPDS_GENERIC_LB
     Worker w;
     w.wid = threadIdx.x;
     w.mine = w.wid < p.workers;
-    w.team = blockIdx.x;
-    w.teams = gridDim.x;
+    w.team = p.first_team + static_cast<int32_t>(blockIdx.x);
+    w.teams = p.total_teams;
+    w.local_team = blockIdx.x;
+    w.local_teams = gridDim.x;
     w.workers = p.workers;
     w.warp = warp;
     w.t = &t;
@@ -534,7 +540,9 @@ inline int32_t validate_launch(const ompds_launch *l) {
   if (!l || l->teams <= 0 || l->workers <= 0 || l->workers > 992 ||
       l->prealloc_entries < 0 || l->prealloc_entries > 4096 ||
       (l->list_allocator != OMPDS_LIST_SLAB && l->list_allocator != OMPDS_LIST_MALLOC) ||
-      l->reserved0 != 0)
+      l->reserved0 != 0 || l->first_team < 0 || l->total_teams < 0 ||
+      (l->total_teams > 0 && int64_t(l->first_team) + l->teams > l->total_teams) ||
+      (l->total_teams == 0 && l->first_team != 0))
     return OMPDS_ERR_INVALID;
   return OMPDS_OK;
 }
@@ -561,6 +569,8 @@ int32_t launch_generic(const ompds_launch *l, const FixedLayout &lay,
                                       : round_up(l->depot_capacity, 8);
   p.events = l->log_events ? events : nullptr;
   p.list_malloc = l->list_allocator == OMPDS_LIST_MALLOC;
+  p.first_team = l->first_team;
+  p.total_teams = l->total_teams > 0 ? l->total_teams : l->teams;
   p.stats = stats;
   p.n_caps = n_caps;
   for (int j = 0; j < kMaxCaptures; ++j)

@@ -187,8 +187,10 @@ template <class T> struct SharedArrayProg {
     const T *d = static_cast<const T *>(sv.get(0));
     if (!w.mine)
       return;
-    const int64_t gid = int64_t(w.team) * w.workers + w.wid;
-    const int64_t pool = int64_t(w.teams) * w.workers;
+    // the shard's own element range: local team indices (config 5 shards
+    // elements across GPUs; each launch sees its slice)
+    const int64_t gid = int64_t(w.local_team) * w.workers + w.wid;
+    const int64_t pool = int64_t(w.local_teams) * w.workers;
     // Cyclic schedule over 16-byte units (AstLowering.cpp:429-462 applied
     // to vectors; the body is element-wise, so results are identical).
     constexpr int V = 16 / sizeof(T);
@@ -282,8 +284,10 @@ template <class T> struct StreamProg {
 #define OMPDS_STREAM_U 2 // swept 2/4/8 on B200: 2 leaves room for more resident teams
 #endif
     constexpr int U = OMPDS_STREAM_U; // 16-byte units in flight per thread per array
-    const int64_t gid = int64_t(w.team) * w.workers + w.wid;
-    const int64_t pool = int64_t(w.teams) * w.workers;
+    // the shard's own element range: local team indices (config 5 shards
+    // elements across GPUs; each launch sees its slice)
+    const int64_t gid = int64_t(w.local_team) * w.workers + w.wid;
+    const int64_t pool = int64_t(w.local_teams) * w.workers;
     const int64_t units = a.n / V;
     const Vec *xv = reinterpret_cast<const Vec *>(a.x);
     Vec *yv = reinterpret_cast<Vec *>(a.y);
@@ -415,7 +419,7 @@ template <class T> struct NestedProg {
       st.status = f1.status ? f1.status : f2.status ? f2.status : s2 ? s2 : s1;
       st.max_depth = w.ds.max_depth;
       st.high_water = w.ds.high_water;
-      a.wstats[size_t(w.team) * (blockDim.x / 32 - 1) + w.warp] = st;
+      a.wstats[size_t(w.local_team) * (blockDim.x / 32 - 1) + w.warp] = st;
     }
   }
 };
@@ -549,7 +553,7 @@ struct ProgramProg {
       *reinterpret_cast<int32_t *>(ml + i) = 0;
     __syncwarp();
     VmCtx c{a.code, a.vars, a.bufs, m.depot.base, ml, nullptr, nullptr,
-            0, static_cast<int32_t>(blockIdx.x), 1, static_cast<int32_t>(gridDim.x)};
+            0, m.p->first_team + static_cast<int32_t>(blockIdx.x), 1, m.p->total_teams};
     int32_t pc = 0;
     for (;;) {
       int32_t ev = 0, r = 0;

@@ -52,7 +52,8 @@ def make_launch(teams: int, workers: int, prealloc_entries: int = L.DEFAULT_PREA
                 fail_dynamic_alloc: bool = False, depot_capacity: int = -1,
                 log_events: bool = False, max_events: int = 0,
                 stream: Optional[torch.cuda.Stream] = None,
-                list_allocator: int = L.LIST_SLAB) -> L.Launch:
+                list_allocator: int = L.LIST_SLAB, first_team: int = 0,
+                total_teams: int = 0) -> L.Launch:
     cur = torch.cuda.current_stream()
     if stream is not None and stream.cuda_stream != cur.cuda_stream:
         # outputs/inputs prepared on the current stream must be ready first
@@ -60,7 +61,7 @@ def make_launch(teams: int, workers: int, prealloc_entries: int = L.DEFAULT_PREA
     s = stream.cuda_stream if stream is not None else cur.cuda_stream
     return L.Launch(teams, workers, prealloc_entries, 1 if fail_dynamic_alloc else 0,
                     depot_capacity, 1 if log_events else 0, max_events if log_events else 0,
-                    C.c_void_p(s), list_allocator, 0)
+                    C.c_void_p(s), list_allocator, first_team, total_teams, 0)
 
 
 def _used_on(stream: Optional[torch.cuda.Stream], *ts) -> None:

@@ -286,3 +286,24 @@ def test_args_lists_past_the_window_slab_and_malloc(allocator, teams, workers, l
             assert sum(1 for e in ev if e[0] == "prepare_dynamic") == regions
             assert sum(1 for e in ev if e[0] == "dynamic_free") == regions
     assert L.LIST_MALLOC == allocator or allocator == L.LIST_SLAB
+
+
+# --------------------------------------------------------------------------- team ranges
+
+@pytest.mark.parametrize("shards", [2, 3])
+def test_team_grid_sharded_by_range_equals_one_launch(shards):
+    """The north_star's multi-GPU partition for team-indexed programs: each
+    shard launches teams [g*T/G, (g+1)*T/G) of a T-team grid (first_team,
+    total_teams); omp_get_team_num() is the global team, so the shards
+    together write exactly what one launch of T teams writes."""
+    from paper_1711_10413_b200 import sharding
+    teams, workers, regions = 7, 40, 3
+    for dt, elem in ((torch.int32, 0), (torch.float64, 1)):
+        a = torch.zeros(teams * workers, dtype=dt, device=DEV)
+        for g in range(shards):
+            lo, hi = sharding.shard_range(teams, g, shards)
+            out = RG.run_regions(a, hi - lo, workers, regions, first_team=lo, total_teams=teams)
+            assert all(s.trap == 0 and s.regions == regions for s in out.team_stats())
+        want = np.zeros(teams * workers, dtype=np.float64 if elem else np.int32)
+        O.lib().orc_regions(elem, teams, workers, regions, O.ptr(want))
+        assert np.array_equal(a.cpu().numpy(), want)

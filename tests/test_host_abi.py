@@ -42,7 +42,7 @@ def test_struct_sizes_match_the_c_abi():
     assert C.sizeof(P.FrameVar) == 32
     assert C.sizeof(P.DepotSlot) == 32
     assert C.sizeof(P.DepotLayout) == 32
-    assert C.sizeof(P.Launch) == 48
+    assert C.sizeof(P.Launch) == 56
     assert C.sizeof(P.TeamStats) == 56
 
 
@@ -203,3 +203,13 @@ def test_b200_kernel_occupancy_table_from_ptxas_log():
     for r in rows:
         regs, thr = int(r[2]), int(r[3])
         assert int(r[5]) == 65536 // (regs * thr)  # teams_by_regs
+
+
+@pytest.mark.parametrize("first,teams,total", [(-1, 2, 4), (3, 2, 4), (1, 2, 0), (0, 2, -1)])
+def test_team_range_outside_the_grid_is_rejected(first, teams, total):
+    """ompds_launch.first_team/total_teams (team-range sharding) are validated
+    before anything touches a GPU."""
+    import ctypes as C
+    launch = P.Launch(teams, 32, 20, 0, -1, 0, 0, None, 0, first, total, 0)
+    rc = P.lib().ompds_run_regions(C.byref(launch), 0, 1, C.c_void_p(16), None, None)
+    assert rc == P.ERR_INVALID

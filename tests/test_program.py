@@ -293,3 +293,28 @@ def test_gpu_window_sizes_and_allocators_keep_reference_outputs(prealloc, alloca
                 assert s.dynamic_allocs >= dyn and (dyn > 0 or s.dynamic_allocs == 0)
             checked += 1
     assert checked >= 4
+
+
+@pytest.mark.gpu
+def test_gpu_reference_programs_sharded_by_team_range():
+    """Every multi-team reference program run as two team-range shards
+    (first_team / total_teams; omp_get_team_num and omp_get_num_teams are
+    the grid's) leaves the same buffers as the reference simulator."""
+    import torch
+    checked = 0
+    for p in programs():
+        for t, w, run in launches(p):
+            if t < 2:
+                continue
+            prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], t, w)
+            bufs = [torch.full((sz,), init, dtype=torch.int32, device="cuda")
+                    for _, sz, init in prog.buffers]
+            half = t // 2
+            for lo, n in ((0, half), (half, t - half)):
+                out = PG.run_program(prog, bufs, first_team=lo, total_teams=t, teams=n)
+                assert [s.trap for s in out.team_stats()] == [0] * n
+            for (name, _, _), b in zip(prog.buffers, bufs):
+                assert b.cpu().tolist() == run["sim"]["globals"][name], (p["stem"], t, w, name)
+            checked += 1
+            break
+    assert checked >= 10
