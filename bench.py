@@ -314,14 +314,24 @@ def main():
     # the same protocol on every SM: 16 teams/SM x 32 workers, 2000 regions
     # each (tools/agg_sweep.py: 8/SM 2.6, 16/SM 4.3 G regions/s; more teams
     # than the register limit's 19/SM run in two waves)
+    # With N ranks the team grid (N x 16 teams/SM) is sharded by range: rank r
+    # launches teams [r*T, (r+1)*T) of the N*T grid (first_team/total_teams),
+    # the whole-job rate is N*T*R2 over the slowest rank's time.
     R2, teams2 = 2000, sms * 16
-    a2 = torch.zeros(teams2 * 32, dtype=torch.int32, device=dev)
-    RG.run_regions(a2, teams2, 32, 10, stream=stream)
+    a2 = torch.zeros(world * teams2 * 32, dtype=torch.int32, device=dev)
+    rng = dict(first_team=rank * teams2, total_teams=world * teams2)
+    RG.run_regions(a2, teams2, 32, 10, stream=stream, **rng)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     e0.record(stream)
-    RG.run_regions(a2, teams2, 32, R2, stream=stream)
+    RG.run_regions(a2, teams2, 32, R2, stream=stream, **rng)
     e1.record(stream)
     e1.synchronize()
-    agg_regions_per_s = teams2 * R2 / (e0.elapsed_time(e1) * 1e-3)
+    ms2 = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
+    agg_regions_per_s = world * teams2 * R2 / (float(ms2.item()) * 1e-3)
     # where the shared-args list lives (PAPER.md: the shared-memory list vs
     # the malloc back-up scheme, "as large as an order of magnitude"): the
     # 4-capture region with the 20-entry window, with a 2-entry window so the
@@ -380,7 +390,9 @@ def main():
                     "workload": "config 1: 1 team x 32 workers, 4 shared scalars, "
                                 f"{R} regions in a sequential loop",
                     "aggregate_regions_per_s": round(agg_regions_per_s, 0),
-                    "aggregate_workload": f"{teams2} teams x 32 workers x {R2} regions",
+                    "aggregate_workload": f"{world * teams2} teams x 32 workers x {R2} regions"
+                                          + (f", team grid sharded by range over {world} GPUs"
+                                             if world > 1 else ""),
                     "args_list_placement": placement},
         "smem_bytes_per_cta": smem_bytes,
         "smem_layout": "depot 80 + args window 160 + runtime span 49 (reference footprint 289)",
