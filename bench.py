@@ -301,7 +301,9 @@ def main():
 
     # config-1 latency: 1 team x 32 workers, R regions in a loop, 4 shared scalars
     R = 10_000
-    a = torch.zeros(32, dtype=torch.int32, device=dev)
+    # config 1 shares 2 int and 2 double scalars (RegionsProg<double>: c1, c2
+    # int, c3, c4 and a[] double)
+    a = torch.zeros(32, dtype=torch.float64, device=dev)
     RG.run_regions(a, 1, 32, 10, stream=stream)
     stream.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -318,7 +320,7 @@ def main():
     # launches teams [r*T, (r+1)*T) of the N*T grid (first_team/total_teams),
     # the whole-job rate is N*T*R2 over the slowest rank's time.
     R2, teams2 = 2000, sms * 16
-    a2 = torch.zeros(world * teams2 * 32, dtype=torch.int32, device=dev)
+    a2 = torch.zeros(world * teams2 * 32, dtype=torch.float64, device=dev)
     rng = dict(first_team=rank * teams2, total_teams=world * teams2)
     RG.run_regions(a2, teams2, 32, 10, stream=stream, **rng)
     if world > 1:
@@ -340,7 +342,7 @@ def main():
     for name, pe, alloc in (("window", 20, 0), ("global_slab", 2, 0), ("device_malloc", 2, 1)):
         row = {}
         for label, tm, rr in (("1team", 1, 2000), ("full", sms * 16, 200)):
-            ap = torch.zeros(tm * 32, dtype=torch.int32, device=dev)
+            ap = torch.zeros(tm * 32, dtype=torch.float64, device=dev)
             RG.run_regions(ap, tm, 32, 10, prealloc_entries=pe, list_allocator=alloc, stream=stream)
             e0.record(stream)
             RG.run_regions(ap, tm, 32, rr, prealloc_entries=pe, list_allocator=alloc, stream=stream)
@@ -387,7 +389,7 @@ def main():
         "roofline": roofline,
         "regions": {"ns_per_region": round(ns_per_region, 1),
                     "regions_per_s": round(1e9 / ns_per_region, 1),
-                    "workload": "config 1: 1 team x 32 workers, 4 shared scalars, "
+                    "workload": "config 1: 1 team x 32 workers, 4 shared scalars (2 int, 2 double), "
                                 f"{R} regions in a sequential loop",
                     "aggregate_regions_per_s": round(agg_regions_per_s, 0),
                     "aggregate_workload": f"{world * teams2} teams x 32 workers x {R2} regions"
