@@ -38,7 +38,6 @@ namespace ompds {
 
 constexpr int kWarp = 32;
 constexpr uint32_t kBarHandoff = 1; // master <-> worker region handoff
-constexpr uint32_t kBarWorkers = 2; // worker-only sync inside a region
 
 enum Phase : uint8_t { kUninit = 0, kIdle = 1, kStaged = 2, kTerminated = 3 };
 enum Role : int { kMaster = OMPDS_ROLE_MASTER, kWorker = OMPDS_ROLE_WORKER };
@@ -78,35 +77,16 @@ __host__ __device__ constexpr int64_t team_region_bytes(int64_t depot,
 // Low-level primitives
 //===----------------------------------------------------------------------===//
 
-// Named barrier.  Default (0): the non-.aligned `barrier.sync` -- each
-// thread arrives individually, so master and worker warps may reach the
-// handoff barrier from different instructions and after divergent code.
-// `.aligned` (`bar.sync`) requires every participating thread of the CTA to
-// execute the same instruction; inlined at the master's and the workers'
-// different call sites that is undefined behaviour, and compute-sanitizer
-// synccheck reports it (mode 1, measured ~50 cycles/region faster).  Mode 2
-// keeps `.aligned` legal with one out-of-line barrier instruction, but the
-// call costs more than the non-aligned form saves (tools/latency_ladder.cu).
-#ifndef OMPDS_BAR_ALIGNED
-#define OMPDS_BAR_ALIGNED 0
-#endif
-#if OMPDS_BAR_ALIGNED == 2
-// One out-of-line copy: master and worker warps execute the SAME barrier
-// instruction, as .aligned requires of every participating thread.
-__device__ __noinline__ void bar_sync_aligned(uint32_t id, uint32_t count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-#endif
+// Named barrier: the non-.aligned `barrier.sync` -- each thread arrives
+// individually, so master and worker warps may reach the handoff barrier
+// from different instructions and after divergent code.  `.aligned`
+// (`bar.sync`) requires every participating thread of the CTA to execute
+// the same instruction; at the master's and the workers' different call
+// sites that is undefined behaviour (compute-sanitizer synccheck reports it),
+// and a two-warp ping-pong measures both forms at 16 cycles per barrier
+// (tools/micro_lat.cu).
 __device__ __forceinline__ void bar_sync(uint32_t id, uint32_t count) {
-#if OMPDS_BAR_ALIGNED == 2
-  __syncwarp();
-  bar_sync_aligned(id, count);
-#elif OMPDS_BAR_ALIGNED
-  __syncwarp();
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-#else
   asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-#endif
 }
 
 // Not volatile: the lane id is invariant, so the compiler may hoist the
@@ -115,10 +95,6 @@ __device__ __forceinline__ uint32_t lane_id() {
   uint32_t l;
   asm("mov.u32 %0, %%laneid;" : "=r"(l));
   return l;
-}
-
-__device__ __forceinline__ bool is_shared_addr(const void *p) {
-  return __isShared(p);
 }
 
 //===----------------------------------------------------------------------===//
@@ -664,15 +640,11 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
     // acq_rel at CTA scope: every participant's reads of the staged region
     // happen-before the last retiree's bookkeeping writes (retire_last).
     uint32_t old;
-#if defined(OMPDS_RETIRE_RELAXED) && OMPDS_RETIRE_RELAXED
-    old = atomicAdd(&t.active_word(), (n << 16) - n);
-#else
     asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
                  : "=r"(old)
                  : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(&t.active_word()))),
                    "r"((n << 16) - n)
                  : "memory");
-#endif
     const uint32_t retired = (old >> 16) + n;
     if (t.events) {
       int64_t ev = t.log_reserve(n);

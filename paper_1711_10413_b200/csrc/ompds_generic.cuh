@@ -240,18 +240,11 @@ struct Master {
     return parallel_general(fn, nargs, addr_of);
   }
 
-#ifndef OMPDS_GENERAL_ATTR
-#define OMPDS_GENERAL_ATTR __forceinline__
-#endif
   template <class AddrOf>
-  __device__ OMPDS_GENERAL_ATTR int32_t parallel_general(int32_t fn, int32_t nargs,
+  __device__ __forceinline__ int32_t parallel_general(int32_t fn, int32_t nargs,
                                                    AddrOf addr_of) {
     void **list = nullptr;
     unsigned long long packed = 0;
-#ifndef OMPDS_WARP_PREPARE
-#define OMPDS_WARP_PREPARE 1
-#endif
-#if OMPDS_WARP_PREPARE
     // Every lane evaluates prepare_parallel's phase checks on broadcast
     // loads, so the window case needs no shuffle from the master lane; only
     // a global list (nargs > PreallocEntries) is allocated by the master and
@@ -283,17 +276,6 @@ struct Master {
       packed = s ? (static_cast<unsigned long long>(s) | (1ull << 63))
                  : reinterpret_cast<unsigned long long>(list);
     }
-#else
-    if (leader) {
-      const int32_t s = prepare_parallel(t, kMaster, fn, nargs, &list);
-      if (s)
-        t.trap(s); // the team's first trap, before any worker can record one
-      // one shuffle carries the list, or the trap code with bit 63 set
-      packed = s ? (static_cast<unsigned long long>(s) | (1ull << 63))
-                 : reinterpret_cast<unsigned long long>(list);
-    }
-    packed = __shfl_sync(0xffffffffu, packed, 0);
-#endif
     const bool ok = (packed >> 63) == 0;
     list = reinterpret_cast<void **>(packed);
     // The reserved warp publishes the pointer list lane-parallel (one

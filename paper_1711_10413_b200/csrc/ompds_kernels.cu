@@ -128,16 +128,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src,
 
 // Streaming 16-byte accesses for bodies that touch each element once
 // (evict-first: `ld.global.cs` / `st.global.cs`).
-__device__ __forceinline__ double2 ld_stream(const double2 *p) {
-#if defined(OMPDS_STREAM_L2PF) && OMPDS_STREAM_L2PF
-  double2 v;
-  asm volatile("ld.global.cs.L2::256B.v2.f64 {%0, %1}, [%2];"
-               : "=d"(v.x), "=d"(v.y) : "l"(p));
-  return v;
-#else
-  return __ldcs(p);
-#endif
-}
+__device__ __forceinline__ double2 ld_stream(const double2 *p) { return __ldcs(p); }
 __device__ __forceinline__ int4 ld_stream(const int4 *p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(double2 *p, double2 v) {
   __stcs(p, v);

@@ -10,14 +10,11 @@ set -e
 cd "$(dirname "$0")/.."
 NVCC=${NVCC:-/usr/local/cuda/bin/nvcc}
 declare -A V
-V[base]="-DOMPDS_WARP_PREPARE=0 -DOMPDS_PREFETCH_WINDOW=0 -DOMPDS_SOLE_WARP_RETIRE=0"
-V[prepare]="-DOMPDS_WARP_PREPARE=1 -DOMPDS_PREFETCH_WINDOW=0 -DOMPDS_SOLE_WARP_RETIRE=0"
-V[prefetch]="-DOMPDS_WARP_PREPARE=0 -DOMPDS_PREFETCH_WINDOW=1 -DOMPDS_SOLE_WARP_RETIRE=0"
-V[sole]="-DOMPDS_WARP_PREPARE=0 -DOMPDS_PREFETCH_WINDOW=0 -DOMPDS_SOLE_WARP_RETIRE=1"
+V[base]="-DOMPDS_PREFETCH_WINDOW=0 -DOMPDS_SOLE_WARP_RETIRE=0"
+V[prefetch]="-DOMPDS_PREFETCH_WINDOW=1 -DOMPDS_SOLE_WARP_RETIRE=0"
+V[sole]="-DOMPDS_PREFETCH_WINDOW=0 -DOMPDS_SOLE_WARP_RETIRE=1"
 V[all]=""
-V[all_aligned]="-DOMPDS_BAR_ALIGNED=1"
-V[all_relaxed]="-DOMPDS_RETIRE_RELAXED=1"
-ORDER="base prepare prefetch sole all all_aligned all_relaxed"
+ORDER="base prefetch sole all"
 case "$1" in
 build)
   for k in $ORDER; do
