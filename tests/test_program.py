@@ -318,3 +318,51 @@ def test_gpu_reference_programs_sharded_by_team_range():
             checked += 1
             break
     assert checked >= 10
+
+
+@pytest.mark.gpu
+def test_gpu_runtime_parameters_never_change_program_outputs():
+    """Seeded fuzz over the reference's programs x the runtime's knobs: window
+    size (0/1/2/20/64 entries), args-list allocator (slab / device malloc),
+    event log on/off, depot slot capacity (smem or the global chain) and
+    team-range sharding (1-3 launches).  The final globals and the barrier
+    counts must be the reference simulator's for every combination; the
+    dynamic allocations must follow the window (every region whose capture
+    count exceeds the window allocates and frees once)."""
+    import random
+    import torch
+    rng = random.Random(0x5eed01ab)
+    cases = []
+    for p in programs():
+        for t, w, run in launches(p):
+            cases.append((p, t, w, run))
+    rng.shuffle(cases)
+    checked = 0
+    for p, t, w, run in cases[:80]:
+        pe = rng.choice([0, 1, 2, 20, 64])
+        alloc = rng.choice([0, 0, 1])
+        log = rng.random() < 0.3 and t * w <= 4096
+        depot_cap = rng.choice([-1, -1, 0])
+        shards = rng.choice([1, 1, 2, 3]) if t >= 2 else 1
+        prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], t, w)
+        bufs = [torch.full((sz,), init, dtype=torch.int32, device="cuda")
+                for _, sz, init in prog.buffers]
+        stats = []
+        for g in range(shards):
+            lo, hi = g * t // shards, (g + 1) * t // shards
+            if hi == lo:
+                continue
+            out = PG.run_program(prog, bufs, prealloc_entries=pe, list_allocator=alloc,
+                                 max_events=4096 if log else 0, depot_capacity=depot_cap,
+                                 first_team=lo, total_teams=t, teams=hi - lo)
+            stats += out.team_stats()
+        key = (p["stem"], t, w, pe, alloc, log, depot_cap, shards)
+        for (name, _, _), b in zip(prog.buffers, bufs):
+            assert b.cpu().tolist() == run["sim"]["globals"][name], key
+        assert [s.trap for s in stats] == [0] * t, key
+        assert [s.master_barriers for s in stats] == run["sim"]["master_barrier_entries"], key
+        assert all(s.dynamic_allocs == s.dynamic_frees for s in stats), key
+        if all(len(r.captures) <= pe for r in prog.regions):
+            assert all(s.dynamic_allocs == 0 for s in stats), key
+        checked += 1
+    assert checked == 80
