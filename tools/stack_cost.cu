@@ -21,7 +21,7 @@ __global__ void stack_cost(unsigned char *chain, long long *out) {
   const uint32_t lane = threadIdx.x & 31;
   DsStack ds;
   // mode 0: baseline (no push/pop); 1: frames in the slot; 2: on the chain
-  ds.init(slot, mode == 2 ? 0 : 4096, chain, 1 << 16);  // mode 3: slot, STS/LDS
+  ds.init(slot, mode == 2 ? 0 : 4096, chain, 1 << 16);
   int32_t acc = 0;
   __syncwarp();
   const long long t0 = clock64();
@@ -34,17 +34,9 @@ __global__ void stack_cost(unsigned char *chain, long long *out) {
       f = ds.push(40, kWarp);
       base = f.base;
     }
-    if (mode == 3 && f.in_smem) { // the frame through the shared window (mode 3)
-      const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(base)) + lane * 40;
-      int32_t v;
-      asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(i + acc) : "memory");
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(sa) : "memory");
-      acc += v;
-    } else {
-      volatile int32_t *e = reinterpret_cast<volatile int32_t *>(base + lane * 40);
-      *e = i + acc;
-      acc += *e;
-    }
+    volatile int32_t *e = reinterpret_cast<volatile int32_t *>(base + lane * 40);
+    *e = i + acc;
+    acc += *e;
     if constexpr (mode != 0)
       acc += ds.pop(f);
   }
@@ -62,17 +54,15 @@ int main() {
   cudaMalloc(&out, 64);
   const char *names[] = {"store+load at a fixed smem address (baseline)",
                          "push + store/load in the frame + pop, smem slot",
-                         "push + store/load in the frame + pop, global chain",
-                         "push + STS/LDS via the shared window + pop, smem slot"};
-  long long h[8];
+                         "push + store/load in the frame + pop, global chain"};
+  long long h[6];
   for (int rep = 0; rep < 2; ++rep) {
     stack_cost<0><<<1, 32>>>(chain, out);
     stack_cost<1><<<1, 32>>>(chain, out);
     stack_cost<2><<<1, 32>>>(chain, out);
-    stack_cost<3><<<1, 32>>>(chain, out);
   }
   cudaMemcpy(h, out, sizeof h, cudaMemcpyDeviceToHost);
-  for (int mode = 0; mode < 4; ++mode)
+  for (int mode = 0; mode < 3; ++mode)
     printf("%-52s %7.1f cycles/iteration\n", names[mode], double(h[2 * mode]) / N);
   printf("status %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
