@@ -129,6 +129,8 @@ typedef struct ompds_event {
   int32_t fn;    /* work-function id (-1 when not applicable)    */
   int64_t nargs; /* NArgs field: workers / nargs / remaining     */
   int64_t bytes; /* Bytes field                                  */
+  int64_t t_ns;  /* device %globaltimer when logged (trace; the
+                    reference's RuntimeEvent has no time)        */
 } ompds_event;
 
 typedef struct ompds_rt_summary { /* TeamRuntime accessors DeviceRuntime.h:97-102 */

@@ -36,7 +36,7 @@ typedef struct {
 
 static void rt_log(Rt *t, int32_t kind, int32_t fn, int64_t nargs, int64_t bytes) {
   if (t->ev && t->n_ev < t->max_ev) {
-    ompds_event e = {kind, fn, nargs, bytes};
+    ompds_event e = {kind, fn, nargs, bytes, 0}; /* no device time on the CPU */
     t->ev[t->n_ev] = e;
   }
   t->n_ev++;

@@ -17,7 +17,8 @@ _lib = None
 
 
 def build() -> str:
-    src = [os.path.join(HERE, "ompds_oracle.c"), os.path.join(HERE, "ompds_oracle.h")]
+    src = [os.path.join(HERE, "ompds_oracle.c"), os.path.join(HERE, "ompds_oracle.h"),
+           os.path.join(os.path.dirname(HERE), "include", "ompds.h")]  # shared ABI structs
     if os.path.exists(LIB_PATH) and all(os.path.getmtime(s) <= os.path.getmtime(LIB_PATH)
                                         for s in src):
         return LIB_PATH

@@ -52,7 +52,8 @@ class RtResult(C.Structure):
 
 
 class Event(C.Structure):
-    _fields_ = [("kind", C.c_int32), ("fn", C.c_int32), ("nargs", C.c_int64), ("bytes", C.c_int64)]
+    _fields_ = [("kind", C.c_int32), ("fn", C.c_int32), ("nargs", C.c_int64), ("bytes", C.c_int64),
+                ("t_ns", C.c_int64)]
 
 
 class RtSummary(C.Structure):

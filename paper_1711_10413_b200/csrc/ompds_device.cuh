@@ -97,6 +97,13 @@ __device__ __forceinline__ uint32_t lane_id() {
   return l;
 }
 
+// Device time for the event trace (ns since an arbitrary epoch).
+__device__ __forceinline__ int64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return static_cast<int64_t>(t);
+}
+
 //===----------------------------------------------------------------------===//
 // Team context
 //===----------------------------------------------------------------------===//
@@ -145,7 +152,7 @@ struct TeamCtx {
       return;
     uint32_t i = atomicAdd(&at<uint32_t>(Rt::kEvents), 1u);
     if (static_cast<int32_t>(i) < max_events)
-      events[i] = ompds_event{kind, fn, nargs, bytes};
+      events[i] = ompds_event{kind, fn, nargs, bytes, globaltimer_ns()};
   }
   // Reserves `n` consecutive event slots, returns the first (or -1 if off).
   __device__ __forceinline__ int64_t log_reserve(uint32_t n) const {
@@ -156,7 +163,7 @@ struct TeamCtx {
   __device__ __forceinline__ void log_at(int64_t i, int32_t kind, int32_t fn,
                                          int64_t nargs, int64_t bytes) const {
     if (i >= 0 && i < max_events)
-      events[i] = ompds_event{kind, fn, nargs, bytes};
+      events[i] = ompds_event{kind, fn, nargs, bytes, globaltimer_ns()};
   }
 
   // LIFO allocator over the team's global slab.  The reference heap never

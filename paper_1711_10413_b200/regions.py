@@ -103,7 +103,9 @@ class Outputs:
                           bool(s.depot_in_smem), s.n_events, s.depot_offset, s.smem_bytes)
                 for s in arr]
 
-    def team_events(self) -> List[List[tuple]]:
+    def team_events(self, times: bool = False) -> List[List[tuple]]:
+        """Per team: (kind, fn, nargs, bytes) in log order, the reference's
+        RuntimeEvent fields; times=True appends the device time (ns)."""
         if self.events is None:
             return [[] for _ in range(self.teams)]
         stats = self.team_stats()
@@ -113,7 +115,8 @@ class Outputs:
         for t in range(self.teams):
             n = min(stats[t].n_events, self.max_events)
             base = t * self.max_events
-            out.append([(L.EVENT_KIND_NAMES[e.kind], e.fn, e.nargs, e.bytes)
+            out.append([(L.EVENT_KIND_NAMES[e.kind], e.fn, e.nargs, e.bytes) +
+                        ((e.t_ns,) if times else ())
                         for e in arr[base:base + n]])
         return out
 

@@ -307,3 +307,33 @@ def test_team_grid_sharded_by_range_equals_one_launch(shards):
         want = np.zeros(teams * workers, dtype=np.float64 if elem else np.int32)
         O.lib().orc_regions(elem, teams, workers, regions, O.ptr(want))
         assert np.array_equal(a.cpu().numpy(), want)
+
+
+# --------------------------------------------------------------------------- trace
+
+@pytest.mark.parametrize("teams,workers", [(2, 32), (3, 96)])
+def test_event_trace_times_follow_the_handoff_barriers(teams, workers):
+    """The event log's device timestamps (ompds_event.t_ns, %globaltimer)
+    respect what the barriers guarantee: init <= prepare(r) <= every fetch of
+    r (release), every retire of r <= prepare(r+1) (join), last retire <=
+    deinit -- per team; fetch/retire order across warps is free."""
+    regions = 4
+    a = torch.zeros(teams * workers, dtype=torch.int32, device=DEV)
+    out = RG.run_regions(a, teams, workers, regions, max_events=2048)
+    for ev in out.team_events(times=True):
+        kinds = [e[0] for e in ev]
+        assert kinds[0] == "init" and kinds[-1] == "deinit"
+        t = [e[4] for e in ev]
+        assert all(x > 0 for x in t)
+        # split into regions at each prepare
+        starts = [i for i, k in enumerate(kinds) if k.startswith("prepare")]
+        assert len(starts) == regions
+        bounds = starts + [len(ev) - 1]
+        assert t[0] <= t[starts[0]]
+        for r in range(regions):
+            p, nxt = bounds[r], bounds[r + 1]
+            body = range(p + 1, nxt)
+            assert all(t[p] <= t[i] for i in body), r
+            assert all(t[i] <= t[nxt] for i in body), r
+            assert sum(1 for i in body if kinds[i] == "fetch") == workers
+            assert sum(1 for i in body if kinds[i] == "retire") == workers

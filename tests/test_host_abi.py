@@ -38,7 +38,7 @@ def test_struct_sizes_match_the_c_abi():
     # sizes implied by the header's field lists (natural alignment, x86-64)
     assert C.sizeof(P.RtCall) == 16
     assert C.sizeof(P.RtResult) == 32
-    assert C.sizeof(P.Event) == 24
+    assert C.sizeof(P.Event) == 32
     assert C.sizeof(P.FrameVar) == 32
     assert C.sizeof(P.DepotSlot) == 32
     assert C.sizeof(P.DepotLayout) == 32
