@@ -10,15 +10,20 @@
 //     thr = sum / n_team;                       // sequential code reads sum
 //     #pragma omp parallel                     // region 1 shares {thr, cnt}
 //     { long c = 0; for (i = mine) c += x[i] > thr;  #pragma omp atomic  cnt += c; }
-//     out[2*team] = sum; out[2*team+1] = cnt;
+//     long wsum[32], tot;                        // captured array + scalar
+//     #pragma omp parallel                     // region 2 shares {wsum, tot}
+//     { warp partial of x -> wsum[warp];  #pragma omp barrier
+//       if (omp_get_thread_num() == 0) tot = sum over wsum; }
+//     out[3*team] = sum; out[3*team+1] = cnt; out[3*team+2] = tot;
 //   }
 //
-// The three locals are implicitly shared: they live in the team's depot in
+// The locals are implicitly shared: they live in the team's depot in
 // shared memory, the workers reach them through get-shared-variables, and
 // their writes (the atomics) are what the master reads after each join --
 // the data-sharing semantics of arXiv 1711.10413 end to end.  Each team
 // reduces its own contiguous slice of x; the host checks every team's sum
-// and count against numpy (tests/test_example_region.py).
+// and count against numpy, and the barrier region's total against the first
+// region's sum (tests/test_example_region.py).
 //
 // Built by paper_1711_10413_b200/build.py into _build/libompds_example.so
 // against the runtime headers and libompds_b200.so.
@@ -32,7 +37,7 @@ struct ReductionProg {
   struct Args {
     const int32_t *x;
     int64_t n;
-    long long *out; // 2 per team: sum, count above the team's mean
+    long long *out; // 3 per team: sum, count above the team's mean, total
   };
   __device__ static void team_range(const Args &a, int64_t *lo, int64_t *hi) {
     *lo = a.n * blockIdx.x / gridDim.x;
@@ -57,10 +62,16 @@ struct ReductionProg {
     if (m.parallel_with(1, 2, [&](int j) -> void * { return m.cap(1 + j); }) !=
         OMPDS_OK) // shares {thr, cnt}
       return;
+    long long *wsum = reinterpret_cast<long long *>(m.cap(3));
+    if (m.parallel_with(2, 2, [&](int j) -> void * { return m.cap(3 + j); }) !=
+        OMPDS_OK) // shares {wsum, tot}
+      return;
     if (m.leader) {
-      a.out[2 * blockIdx.x] = *sum;
-      a.out[2 * blockIdx.x + 1] = *cnt;
+      a.out[3 * blockIdx.x] = *sum;
+      a.out[3 * blockIdx.x + 1] = *cnt;
+      a.out[3 * blockIdx.x + 2] = *reinterpret_cast<long long *>(m.cap(4));
     }
+    (void)wsum;
   }
   __device__ static void region(int32_t fn, const SharedVars &sv, Worker &w,
                                 const Args &a) {
@@ -69,6 +80,22 @@ struct ReductionProg {
     long long *s0 = static_cast<long long *>(sv.get(0));
     long long *s1 = static_cast<long long *>(sv.get(1));
     long long part = 0;
+    if (fn == 2) { // per-warp partials, an omp barrier, one worker totals them
+      for (int64_t i = lo + w.wid; w.mine && i < hi; i += w.workers)
+        part += a.x[i];
+      for (int o = 16; o > 0; o >>= 1)
+        part += __shfl_xor_sync(0xffffffffu, part, o);
+      if ((threadIdx.x & 31) == 0)
+        s0[w.warp] = part;
+      w.barrier();
+      if (w.wid == 0) {
+        long long tot = 0;
+        for (uint32_t k = 0; k < w.worker_threads / 32; ++k)
+          tot += s0[k];
+        *s1 = tot;
+      }
+      return;
+    }
     if (fn == 0) {
       for (int64_t i = lo + w.wid; w.mine && i < hi; i += w.workers)
         part += a.x[i];
@@ -93,10 +120,11 @@ extern "C" int32_t example_reduction(const ompds_launch *launch, const int32_t *
   if (!x || !out || n < 0)
     return OMPDS_ERR_INVALID;
   FixedLayout lay;
-  // kernel frame group: sum, thr, cnt (captured, 8 B each), then
-  // __omp_worker's wf.addr / args.addr -- 40 B, team footprint 249 B
-  const int32_t s = build_fixed_layout({8, 8, 8}, 0, &lay);
+  // kernel frame group: sum, thr, cnt (captured, 8 B each), wsum[32]
+  // (256 B), tot (8 B), then __omp_worker's wf.addr / args.addr -- 304 B,
+  // team footprint 513 B
+  const int32_t s = build_fixed_layout({8, 8, 8, 256, 8}, 0, &lay);
   if (s)
     return s;
-  return launch_generic<ReductionProg>(launch, lay, 3, {x, n, out}, stats, nullptr);
+  return launch_generic<ReductionProg>(launch, lay, 5, {x, n, out}, stats, nullptr);
 }

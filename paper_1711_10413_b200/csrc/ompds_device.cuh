@@ -38,6 +38,7 @@ namespace ompds {
 
 constexpr int kWarp = 32;
 constexpr uint32_t kBarHandoff = 1; // master <-> worker region handoff
+constexpr uint32_t kBarRegion = 2;  // `omp barrier` among a region's workers
 
 enum Phase : uint8_t { kUninit = 0, kIdle = 1, kStaged = 2, kTerminated = 3 };
 enum Role : int { kMaster = OMPDS_ROLE_MASTER, kWorker = OMPDS_ROLE_WORKER };

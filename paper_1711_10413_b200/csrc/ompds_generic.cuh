@@ -357,6 +357,14 @@ struct Worker {
   void **args;  // the fetched shared-args list
   int32_t nargs;
   int32_t region_index; // regions this warp ran before the current one
+  uint32_t worker_threads; // 32 x worker warps (padding lanes included)
+
+  // `#pragma omp barrier` inside the region: every worker of the team (the
+  // master warp is parked at the join and does not take part); all lanes of
+  // every worker warp must arrive, padding lanes included.
+  __device__ __forceinline__ void barrier() const {
+    bar_sync(kBarRegion, worker_threads);
+  }
 };
 
 template <class Prog>
@@ -391,6 +399,7 @@ __global__ void OMPDS_GENERIC_LB
     w.teams = p.total_teams;
     w.local_team = blockIdx.x;
     w.local_teams = gridDim.x;
+    w.worker_threads = static_cast<uint32_t>(worker_warps) * 32u;
     w.workers = p.workers;
     w.warp = warp;
     w.t = &t;

@@ -1,8 +1,10 @@
 """A user-defined region program (examples/reduction_region.cu) compiled
-against the runtime headers: two parallel regions per team share kernel
+against the runtime headers: three parallel regions per team share kernel
 locals by reference -- the workers' atomics on the shared `sum` / `cnt` are
-what the master reads after each join, and the master's write of `thr`
-between the regions is what the second region's workers read."""
+what the master reads after each join, the master's write of `thr` between
+the regions is what the second region's workers read, and the third region
+uses an `omp barrier` among its workers before one of them totals the
+per-warp partials in a shared array."""
 import ctypes as C
 import os
 
@@ -36,7 +38,7 @@ def _expected(x, teams):
         s = int(x[lo:hi].astype(np.int64).sum())
         c = hi - lo
         thr = 0 if c == 0 else (abs(s) // c) * (1 if s >= 0 else -1)  # C division
-        out += [s, int((x[lo:hi].astype(np.int64) > thr).sum())]
+        out += [s, int((x[lo:hi].astype(np.int64) > thr).sum()), s]
     return out
 
 
@@ -48,7 +50,7 @@ def test_example_region_program_matches_numpy(teams, workers, n):
     from paper_1711_10413_b200 import regions as RG
     x = torch.empty(n, dtype=torch.int32, device="cuda")
     RG.fill_uniform(x, 0x5eed01ab)
-    out = torch.zeros(2 * teams, dtype=torch.int64, device="cuda")
+    out = torch.zeros(3 * teams, dtype=torch.int64, device="cuda")
     res = RG.Outputs(teams, x.device, 0)
     launch = RG.make_launch(teams, workers)
     L.check(lib().example_reduction(C.byref(launch), C.c_void_p(x.data_ptr()), n,
@@ -57,7 +59,7 @@ def test_example_region_program_matches_numpy(teams, workers, n):
     torch.cuda.synchronize()
     assert out.cpu().tolist() == _expected(x.cpu().numpy(), teams)
     for st in res.team_stats():
-        # two regions: 4 master barriers, 5 releases; team region = the
-        # 40-byte depot + 160 B window + 49 B runtime span
-        assert (st.trap, st.master_barriers, st.barrier_releases, st.regions) == (0, 4, 5, 2)
-        assert st.smem_bytes == 40 + 160 + 49 and st.depot_in_smem
+        # three regions: 6 master barriers, 7 releases; team region = the
+        # 304-byte depot + 160 B window + 49 B runtime span
+        assert (st.trap, st.master_barriers, st.barrier_releases, st.regions) == (0, 6, 7, 3)
+        assert st.smem_bytes == 304 + 160 + 49 and st.depot_in_smem
