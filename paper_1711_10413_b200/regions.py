@@ -159,10 +159,13 @@ class WarpStack:
 
 
 def run_nested(a: torch.Tensor, teams: int, workers: int, regions: int,
-               warp_slot_bytes: int = 2048, warp_overflow_bytes: int = 4096, **kw):
+               warp_slot_bytes: int = 2048, warp_overflow_bytes: int = 4096,
+               collect: bool = True, **kw):
     """Config 3: nested regions (depth 3) on per-warp data-sharing stacks.
 
-    Returns (Outputs, per-team list of per-warp :class:`WarpStack`)."""
+    Returns (Outputs, per-team list of per-warp :class:`WarpStack`); with
+    collect=False the launch is only enqueued (no wait, stacks None) -- for
+    timing the kernel alone."""
     _require_cuda(a)
     max_events = kw.pop("max_events", 0)
     out = Outputs(teams, a.device, max_events)
@@ -176,6 +179,8 @@ def run_nested(a: torch.Tensor, teams: int, workers: int, regions: int,
                                      out.events_ptr()), "ompds_run_nested")
     out.used_on(kw.get("stream"))
     _used_on(kw.get("stream"), ws)
+    if not collect:
+        return out, None
     torch.cuda.synchronize(a.device)  # the launch may be on another stream
     raw = bytes(ws.cpu().numpy().tobytes())
     arr = (L.WarpStackStats * (teams * warps)).from_buffer_copy(raw)
