@@ -144,6 +144,26 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def device_ms(stream, launch, reps=3):
+    """Device time of what `launch()` enqueues on `stream` (median of
+    `reps`, after one untimed run): the GPU spins (~100 us) while the host
+    prepares each launch, so the host's argument marshalling never lands
+    between the two events."""
+    import torch
+    times = []
+    for i in range(reps + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(200_000)
+            e0.record(stream)
+            launch()
+            e1.record(stream)
+        e1.synchronize()
+        if i:
+            times.append(e0.elapsed_time(e1))
+    return statistics.median(times)
+
+
 def cpu_baseline(n_sample, threads):
     """The C oracle port (fp64, OpenMP over the host's cores) on a bounded sample."""
     import numpy as np
@@ -306,13 +326,8 @@ def main():
     a = torch.zeros(32, dtype=torch.float64, device=dev)
     RG.run_regions(a, 1, 32, 10, stream=stream)
     stream.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    RG.run_regions(a, 1, 32, R, stream=stream)
-    e1.record(stream)
-    e1.synchronize()
-    ns_per_region = e0.elapsed_time(e1) * 1e6 / R
+    ns_per_region = device_ms(stream, lambda: RG.run_regions(a, 1, 32, R, stream=stream)) \
+        * 1e6 / R
     # the same protocol on every SM: 16 teams/SM x 32 workers, 2000 regions
     # each (tools/agg_sweep.py: 8/SM 2.6, 16/SM 4.3 G regions/s; more teams
     # than the register limit's 19/SM run in two waves)
@@ -326,11 +341,8 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    e0.record(stream)
-    RG.run_regions(a2, teams2, 32, R2, stream=stream, **rng)
-    e1.record(stream)
-    e1.synchronize()
-    ms2 = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    ms2 = device_ms(stream, lambda: RG.run_regions(a2, teams2, 32, R2, stream=stream, **rng))
+    ms2 = torch.tensor([ms2], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
     agg_regions_per_s = world * teams2 * R2 / (float(ms2.item()) * 1e-3)
@@ -344,11 +356,8 @@ def main():
         for label, tm, rr in (("1team", 1, 2000), ("full", sms * 16, 200)):
             ap = torch.zeros(tm * 32, dtype=torch.float64, device=dev)
             RG.run_regions(ap, tm, 32, 10, prealloc_entries=pe, list_allocator=alloc, stream=stream)
-            e0.record(stream)
-            RG.run_regions(ap, tm, 32, rr, prealloc_entries=pe, list_allocator=alloc, stream=stream)
-            e1.record(stream)
-            e1.synchronize()
-            ms_p = e0.elapsed_time(e1)
+            ms_p = device_ms(stream, lambda: RG.run_regions(
+                ap, tm, 32, rr, prealloc_entries=pe, list_allocator=alloc, stream=stream))
             row[f"ns_per_region_{label}"] = round(ms_p * 1e6 / rr, 1)
             row[f"regions_per_s_{label}"] = round(tm * rr / (ms_p * 1e-3), 0)
         placement[name] = row
@@ -519,13 +528,9 @@ def other_configs(RG, dev, stream, sms):
                              ("config3_nested_1team_overflow", 1, 0)):
         a3 = torch.zeros(teams * 96, dtype=torch.float64, device=dev)
         _, stacks = RG.run_nested(a3, teams, 96, 10, warp_slot_bytes=slot, stream=stream)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
         # timed: the launch only (collecting the warp statistics is host work)
-        RG.run_nested(a3, teams, 96, R, warp_slot_bytes=slot, stream=stream, collect=False)
-        e1.record(stream)
-        e1.synchronize()
-        ms = e0.elapsed_time(e1)
+        ms = device_ms(stream, lambda: RG.run_nested(a3, teams, 96, R, warp_slot_bytes=slot,
+                                                     stream=stream, collect=False))
         out[key] = {"teams": teams, "workers": 96, "regions": R,
                     "ns_per_region": round(ms * 1e6 / R, 1),
                     "aggregate_regions_per_s": round(teams * R / (ms * 1e-3), 0),
