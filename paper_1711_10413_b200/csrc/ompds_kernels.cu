@@ -4,8 +4,12 @@
 // One CTA = one OpenMP team.  Worker warps [0, ceil(W/32)) run the worker
 // loop of proj/src/Codegen.cpp:403-513; the last warp is the reserved master
 // warp (Codegen.h:25-30): lane 0 is the master and commits every side effect
-// of the sequential region, lanes 1..31 execute it redundantly so the warp
-// stays converged for the aligned named barriers it must arrive at.
+// of the sequential region, lanes 1..31 execute it redundantly -- they must
+// stay resident and arrive at the handoff barriers (an exited thread never
+// arrives), and the warp evaluates the runtime's checks on broadcast loads.
+// The team kernel itself (Master, Worker, generic_mode_kernel) lives in
+// ompds_generic.cuh; this file holds the configs' region programs and the
+// C-ABI launchers.
 //
 // Per region the master pays exactly two handoff barriers (release, join --
 // Codegen.cpp:304-309) and the team sees 2R+1 releases including the
