@@ -227,6 +227,12 @@ typedef struct ompds_gpu_spec { /* GpuSpec Occupancy.h:24-31 */
   int32_t max_regs_per_thread;
   int64_t max_threads_per_sm;      /* 0 = unlimited (reference model)      */
   int64_t reserved_smem_per_block; /* 0 in the reference model; 1 KB B200  */
+  int32_t reg_alloc_unit;          /* registers per thread are allocated
+                                      per warp in multiples of this: 8 on
+                                      B200 (256 per warp, as ncu's
+                                      occupancy_limit_registers counts);
+                                      0 = exact (the reference model)     */
+  int32_t reserved0;
 } ompds_gpu_spec;
 
 typedef struct ompds_occupancy { /* OccupancyResult Occupancy.h:62-68 */

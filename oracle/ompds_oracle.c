@@ -336,6 +336,11 @@ static int64_t mn(int64_t a, int64_t b) { return a < b ? a : b; }
 int32_t orc_occupancy_for(const ompds_gpu_spec *g, int64_t fp, int32_t regs,
                           int32_t threads, ompds_occupancy *o) {
   int64_t per_team_regs = (int64_t)regs * threads;
+  if (g->reg_alloc_unit > 0) { /* per warp, regs rounded up to the unit */
+    int64_t u = g->reg_alloc_unit;
+    int64_t warps = ((int64_t)threads + g->warp_size - 1) / g->warp_size;
+    per_team_regs = (((int64_t)regs + u - 1) / u * u) * g->warp_size * warps;
+  }
   o->teams_by_regs = per_team_regs > 0 ? g->registers_per_sm / per_team_regs : 0;
   int64_t per = fp > 0 ? fp + g->reserved_smem_per_block : 0;
   o->teams_by_smem = per > 0 ? g->shared_bytes_per_sm / per : 0;
@@ -349,6 +354,11 @@ int32_t orc_occupancy_for(const ompds_gpu_spec *g, int64_t fp, int32_t regs,
 
 int64_t orc_max_regs_for_teams(const ompds_gpu_spec *g, int64_t teams, int32_t threads) {
   if (teams <= 0 || threads <= 0) return g->max_regs_per_thread;
+  if (g->reg_alloc_unit > 0) {
+    int64_t warps = ((int64_t)threads + g->warp_size - 1) / g->warp_size;
+    int64_t r = g->registers_per_sm / (teams * warps * g->warp_size);
+    return mn(r / g->reg_alloc_unit * g->reg_alloc_unit, g->max_regs_per_thread);
+  }
   return mn(g->registers_per_sm / (teams * threads), g->max_regs_per_thread);
 }
 

@@ -83,7 +83,8 @@ class GpuSpec(C.Structure):
     _fields_ = [("shared_bytes_per_sm", C.c_int64), ("registers_per_sm", C.c_int64),
                 ("max_blocks_per_sm", C.c_int64), ("warp_size", C.c_int32),
                 ("max_regs_per_thread", C.c_int32), ("max_threads_per_sm", C.c_int64),
-                ("reserved_smem_per_block", C.c_int64)]
+                ("reserved_smem_per_block", C.c_int64), ("reg_alloc_unit", C.c_int32),
+                ("reserved0", C.c_int32)]
 
 
 class Occupancy(C.Structure):

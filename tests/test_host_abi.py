@@ -185,6 +185,13 @@ def test_b200_occupancy_row():
     # 1024-thread teams: the 2048-threads/SM limit binds (2 teams/SM).
     o = occupancy.occupancy_for("b200", 289, 32, 1024)
     assert o.potential == 2 and o.actual == 2
+    # registers are allocated per warp, 8 per thread at a time: the
+    # config-1 kernel at 49 registers x 64 threads fits 18 teams per SM --
+    # ncu's launch__occupancy_limit_registers for it (profiles/r1d_regions_ncu.json);
+    # the config-4 kernel at 64 x 128 fits 8 (ncu: 8)
+    assert occupancy.occupancy_for("b200", 265, 49, 64).teams_by_regs == 18
+    assert occupancy.occupancy_for("b200", 289, 64, 128).teams_by_regs == 8
+    assert occupancy.max_regs_for_teams("b200", 18, 64) == 56
 
 
 def test_compute_entry_point_raises_ompds_error_without_gpu():
@@ -202,7 +209,9 @@ def test_b200_kernel_occupancy_table_from_ptxas_log():
     assert {r[0] for r in rows} >= {"RegionsProgIiE", "StreamProgIdE", "SharedArrayProgIdE"}
     for r in rows:
         regs, thr = int(r[2]), int(r[3])
-        assert int(r[5]) == 65536 // (regs * thr)  # teams_by_regs
+        # teams_by_regs: per-warp allocation, registers rounded up to 8
+        warps = (thr + 31) // 32
+        assert int(r[5]) == 65536 // (((regs + 7) // 8 * 8) * 32 * warps)
 
 
 @pytest.mark.parametrize("first,teams,total", [(-1, 2, 4), (3, 2, 4), (1, 2, 0), (0, 2, -1)])
