@@ -58,6 +58,10 @@ typedef enum ompds_status {
   OMPDS_TRAP_STACK_UNDERFLOW = 19, /* pop of a frame that is not the top */
   OMPDS_TRAP_OUT_OF_BOUNDS = 20,   /* region program: index outside its object
                                       (Simulator.cpp:313-377 "out-of-bounds") */
+  OMPDS_TRAP_STEP_LIMIT = 21,      /* region program: a thread executed more
+                                      than ompds_program.step_limit operations
+                                      (Simulator.cpp:819-822, "step limit
+                                      exceeded")                           */
   /* host-side errors */
   OMPDS_ERR_CUDA = 100,    /* no usable CUDA device / launch or copy failed */
   OMPDS_ERR_INVALID = 101, /* invalid argument */
@@ -391,6 +395,11 @@ typedef struct ompds_program {
   int64_t total_shared; /* kernel frame group depot (TotalShared)     */
   int64_t total_local;  /* its local mirror                            */
   int64_t priv_bytes;   /* largest outlined-function frame             */
+  int64_t step_limit;   /* operations one thread (the master's sequential
+                           code, or one worker's region body) may execute
+                           before the team traps OMPDS_TRAP_STEP_LIMIT;
+                           <= 0: 20,000,000 (SimOptions::StepLimit's
+                           default, Simulator.h:37)                     */
 } ompds_program;
 
 int32_t ompds_run_program(const ompds_launch *launch, const ompds_program *prog,

@@ -35,6 +35,7 @@ EVENT_KIND_NAMES = ["init", "prepare_prealloc", "prepare_dynamic", "fetch", "ret
 VAR_ESCAPES, VAR_PINNED = 1, 2
 PIPELINE_DEFAULT, PIPELINE_O0, PIPELINE_BAD_ORDER = range(3)
 ELEM_I32, ELEM_F64 = 0, 1
+TRAP_STACK_OVERFLOW, TRAP_STACK_UNDERFLOW, TRAP_OUT_OF_BOUNDS, TRAP_STEP_LIMIT = 18, 19, 20, 21
 LIST_SLAB, LIST_MALLOC = 0, 1
 
 
@@ -129,7 +130,8 @@ class Program(C.Structure):
                 ("regions", C.POINTER(ProgRegion)), ("captures", C.POINTER(C.c_int32)),
                 ("n_captures", C.c_int32), ("n_buffers", C.c_int32),
                 ("buffers", C.POINTER(C.c_void_p)), ("total_shared", C.c_int64),
-                ("total_local", C.c_int64), ("priv_bytes", C.c_int64)]
+                ("total_local", C.c_int64), ("priv_bytes", C.c_int64),
+                ("step_limit", C.c_int64)]
 
 
 # Every symbol include/ompds.h declares, with its signature.
@@ -206,3 +208,8 @@ def check(code: int, where: str) -> None:
 
 def exported_symbols():
     return list(_SIGS)
+
+
+def trap_reason(code: int) -> str:
+    """The trap string of a status code (1..17: the reference's, byte for byte)."""
+    return lib().ompds_trap_reason(code).decode()

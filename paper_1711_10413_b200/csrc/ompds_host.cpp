@@ -34,6 +34,7 @@ const char *const kTrapStrings[] = {
     "data-sharing stack overflow",
     "data-sharing stack underflow",
     "out-of-bounds access",
+    "step limit exceeded", // Simulator.cpp:820
 };
 
 int64_t roundUp8(int64_t n) { return (n + 7) & ~int64_t(7); }

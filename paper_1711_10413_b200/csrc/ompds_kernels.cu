@@ -437,6 +437,7 @@ constexpr int kVmPriv = 256;    // bytes of a worker's private frame
 constexpr int kVmCaps = 128;    // captures per region
 
 struct VmCtx {
+  int64_t steps_left; // operations this thread may still execute
   const int32_t *code;
   const ompds_prog_var *vars;
   void *const *bufs;
@@ -466,11 +467,13 @@ __device__ __forceinline__ int32_t *vm_addr(const VmCtx &c, int32_t v,
 
 // Runs from *pc until END (returns 0), PARALLEL (returns 1, region in *r)
 // or a trap (returns the trap code, negated).
-__device__ int32_t vm_run(const VmCtx &c, int32_t *pc_io, int32_t *r) {
+__device__ int32_t vm_run(VmCtx &c, int32_t *pc_io, int32_t *r) {
   int32_t st[kVmStack];
   int sp = 0;
   int32_t pc = *pc_io;
   for (;;) {
+    if (--c.steps_left < 0) // a runaway program (Simulator.cpp:819-822)
+      return -OMPDS_TRAP_STEP_LIMIT;
     const int32_t op = c.code[pc++];
     switch (op) {
     case OP_END:
@@ -541,13 +544,14 @@ struct ProgramProg {
     void *const *bufs;
     unsigned char *mlocal; // teams * total_local
     int64_t total_local;
+    int64_t step_limit;    // per thread (master code / one region body)
   };
   __device__ static void master(Master &m, const Args &a) {
     unsigned char *ml = a.mlocal + size_t(blockIdx.x) * a.total_local;
     for (int64_t i = lane_id() * 4; i < a.total_local; i += 128) // zero-filled frame
       *reinterpret_cast<int32_t *>(ml + i) = 0;
     __syncwarp();
-    VmCtx c{a.code, a.vars, a.bufs, m.depot.base, ml, nullptr, nullptr,
+    VmCtx c{a.step_limit, a.code, a.vars, a.bufs, m.depot.base, ml, nullptr, nullptr,
             0, m.p->first_team + static_cast<int32_t>(blockIdx.x), 1, m.p->total_teams};
     int32_t pc = 0;
     for (;;) {
@@ -581,7 +585,7 @@ struct ProgramProg {
     if (!w.mine)
       return;
     alignas(16) unsigned char priv[kVmPriv];
-    VmCtx c{a.code, a.vars, a.bufs, nullptr, nullptr, priv, caps,
+    VmCtx c{a.step_limit, a.code, a.vars, a.bufs, nullptr, nullptr, priv, caps,
             w.wid, w.team, w.workers, w.teams};
     int32_t pc = a.regions[fn].entry, r = 0;
     const int32_t ev = vm_run(c, &pc, &r);
@@ -965,7 +969,8 @@ int32_t ompds_run_program(const ompds_launch *launch, const ompds_program *pr,
                       reinterpret_cast<const ompds_prog_region *>(dev + o_regs),
                       reinterpret_cast<const int32_t *>(dev + o_caps),
                       reinterpret_cast<void *const *>(dev + o_bufs), mlocal,
-                      std::max<int64_t>(pr->total_local, 4)};
+                      std::max<int64_t>(pr->total_local, 4),
+                      pr->step_limit > 0 ? pr->step_limit : int64_t(20000000)};
   s = launch_generic<ProgramProg>(launch, lay, 0, a, stats, events);
   if (s)
     return s;

@@ -328,7 +328,8 @@ def compile_program(ast: dict, layouts: Sequence[dict], kernel_root: str, teams:
 def run_program(prog: Program, buffers, prealloc_entries: int = L.DEFAULT_PREALLOC_ENTRIES,
                 fail_dynamic_alloc: bool = False, depot_capacity: int = -1,
                 max_events: int = 0, stream=None, list_allocator: int = L.LIST_SLAB,
-                first_team: int = 0, total_teams: int = 0, teams: int = 0):
+                first_team: int = 0, total_teams: int = 0, teams: int = 0,
+                step_limit: int = 0):
     """Launches the program: `buffers` are int32 CUDA tensors, one per mapped
     array, in host declaration order.  Returns regions.Outputs."""
     import torch
@@ -352,7 +353,8 @@ def run_program(prog: Program, buffers, prealloc_entries: int = L.DEFAULT_PREALL
     desc = L.Program(code=code, n_code=len(prog.code), vars=vars_, n_vars=len(prog.vars),
                      n_regions=len(regs), regions=regs_a, captures=caps_a, n_captures=len(caps),
                      n_buffers=len(buffers), buffers=bufs, total_shared=prog.total_shared,
-                     total_local=prog.total_local, priv_bytes=prog.priv_bytes)
+                     total_local=prog.total_local, priv_bytes=prog.priv_bytes,
+                     step_limit=step_limit)
     out = RG.Outputs(teams or prog.teams, buffers[0].device if buffers else "cuda", max_events)
     launch = RG.make_launch(teams or prog.teams, prog.workers, prealloc_entries,
                             fail_dynamic_alloc, depot_capacity, max_events > 0, max_events,

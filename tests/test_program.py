@@ -366,3 +366,28 @@ def test_gpu_runtime_parameters_never_change_program_outputs():
             assert all(s.dynamic_allocs == 0 for s in stats), key
         checked += 1
     assert checked == 80
+
+
+@pytest.mark.gpu
+def test_gpu_runaway_programs_hit_the_step_limit():
+    """SimulatorTests.cpp:142-148 ("runaway launches hit the step limit"): a
+    program whose thread runs more operations than the limit traps with the
+    reference's string and the team still terminates; the default limit
+    (SimOptions::StepLimit, 20M) leaves the reference's outputs intact."""
+    import torch
+    from paper_1711_10413_b200 import _lib as L
+    p = next(x for x in G.load("corpus") if x["stem"] == "arrays_1")  # a 96-trip loop
+    t, w, run = launches(p)[0]
+    prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], t, w)
+    bufs = [torch.full((sz,), init, dtype=torch.int32, device="cuda")
+            for _, sz, init in prog.buffers]
+    out = PG.run_program(prog, bufs, step_limit=50)
+    st = out.team_stats()
+    assert all(s.trap == L.TRAP_STEP_LIMIT for s in st)
+    assert L.trap_reason(L.TRAP_STEP_LIMIT) == "step limit exceeded"
+    bufs = [torch.full((sz,), init, dtype=torch.int32, device="cuda")
+            for _, sz, init in prog.buffers]
+    out = PG.run_program(prog, bufs)
+    assert [s.trap for s in out.team_stats()] == [0] * t
+    for (name, _, _), b in zip(prog.buffers, bufs):
+        assert b.cpu().tolist() == run["sim"]["globals"][name]
