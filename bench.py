@@ -328,6 +328,9 @@ def main():
     stream.synchronize()
     ns_per_region = device_ms(stream, lambda: RG.run_regions(a, 1, 32, R, stream=stream)) \
         * 1e6 / R
+    # the reference's integer analog (4 int captures, int body) beside it
+    ai = torch.zeros(32, dtype=torch.int32, device=dev)
+    ns_int = device_ms(stream, lambda: RG.run_regions(ai, 1, 32, R, stream=stream)) * 1e6 / R
     # the same protocol on every SM: 16 teams/SM x 32 workers, 2000 regions
     # each (tools/agg_sweep.py: 8/SM 2.6, 16/SM 4.3 G regions/s; more teams
     # than the register limit's 19/SM run in two waves)
@@ -397,6 +400,7 @@ def main():
                    "l2": "inputs (2 x 8 B x n) larger than the 126 MB L2, no flush needed"},
         "roofline": roofline,
         "regions": {"ns_per_region": round(ns_per_region, 1),
+                    "ns_per_region_int_analog": round(ns_int, 1),
                     "regions_per_s": round(1e9 / ns_per_region, 1),
                     "workload": "config 1: 1 team x 32 workers, 4 shared scalars (2 int, 2 double), "
                                 f"{R} regions in a sequential loop",
