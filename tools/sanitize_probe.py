@@ -28,6 +28,13 @@ def main():
     y = torch.ones(5003, dtype=torch.float64, device=dev)
     RG.run_stream(x, y, [k / 8 for k in range(1, 9)], 4, 96, max_events=512)
     RG.run_stream(x, y, [k / 8 for k in range(1, 9)], 4, 96, prealloc_entries=2)
+    # args lists past the window: team slab and device malloc; team ranges
+    for alloc in (0, 1):
+        a = torch.zeros(2 * 40, dtype=torch.int32, device=dev)
+        RG.run_regions(a, 2, 40, 3, prealloc_entries=2, list_allocator=alloc)
+    a = torch.zeros(4 * 32, dtype=torch.int32, device=dev)
+    RG.run_regions(a, 2, 32, 2, first_team=0, total_teams=4)
+    RG.run_regions(a, 2, 32, 2, first_team=2, total_teams=4)
     for slot in (2048, 0):
         n = torch.zeros(2 * 72, dtype=torch.float64, device=dev)
         RG.run_nested(n, 2, 72, 2, warp_slot_bytes=slot)
@@ -41,6 +48,13 @@ def main():
         bufs = [torch.full((sz,), init, dtype=torch.int32, device=dev)
                 for _, sz, init in prog.buffers]
         PG.run_program(prog, bufs)
+    # a runaway program trapping at the step limit
+    p = next(x for x in G.load("corpus") if x["stem"] == "arrays_1")
+    t, w, _ = launches(p)[0]
+    prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], t, w)
+    bufs = [torch.full((sz,), init, dtype=torch.int32, device=dev)
+            for _, sz, init in prog.buffers]
+    PG.run_program(prog, bufs, step_limit=50)
     torch.cuda.synchronize()
     print("sanitize probe done")
 
