@@ -265,11 +265,12 @@ def main():
     lo, hi = sharding.shard_range(n_total, rank, world)
     n = hi - lo
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    # Tuned on B200 (tools/sweep.py, profiles/r1_sweep*.json): 128-thread
-    # teams (W=96 + the master warp), 8 teams per SM, 2 x 16-byte units of x
-    # and y in flight per thread; ~4 % faster than one wave of 1024-thread teams.
+    # Tuned on B200 (tools/stream_geom_ab.py): 128-thread teams (W = 96 +
+    # the master warp), 7 teams per SM, each thread streaming 2 consecutive
+    # 16-byte units of x and of y per iteration (6.88 TB/s; 8 teams/SM with
+    # the unit-cyclic schedule gave 6.70).
     workers = args.workers or 96
-    teams = args.teams or sms * 8
+    teams = args.teams or sms * 7
 
     x = torch.empty(n, dtype=torch.float64, device=dev)
     y = torch.empty(n, dtype=torch.float64, device=dev)

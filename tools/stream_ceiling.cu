@@ -43,6 +43,30 @@ __global__ void __launch_bounds__(1024) ldg(const double2 *__restrict__ x, doubl
   }
 }
 
+// K consecutive 16-byte units per thread (16K bytes contiguous per thread),
+// cyclic over threads: unit block b = gid + j * pool covers units [K*b, K*b+K)
+template <int K>
+__global__ void __launch_bounds__(1024) ldg_blk(const double2 *__restrict__ x,
+                                                double2 *__restrict__ y, int64_t units,
+                                                double c1, double s) {
+  const int64_t pool = int64_t(gridDim.x) * blockDim.x;
+  const int64_t blocks = units / K;
+  for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < blocks; b += pool) {
+    double2 xs[K], ys[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      xs[k] = __ldcs(x + b * K + k);
+      ys[k] = __ldcs(y + b * K + k);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      ys[k].x = op(c1, xs[k].x, ys[k].x, s);
+      ys[k].y = op(c1, xs[k].y, ys[k].y, s);
+      __stcs(y + b * K + k, ys[k]);
+    }
+  }
+}
+
 __device__ __forceinline__ uint32_t sa(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -150,6 +174,25 @@ int main() {
       timeit(nm, [&] { ldg<2><<<sms * bps, thr>>>((const double2 *)x, (double2 *)y, units, 0.125, 4.375); });
       snprintf(nm, sizeof nm, "ldg<4>  %d blocks/SM x %d", bps, thr);
       timeit(nm, [&] { ldg<4><<<sms * bps, thr>>>((const double2 *)x, (double2 *)y, units, 0.125, 4.375); });
+    }
+  }
+  // repeatability: the product geometry vs the best contiguous-block one
+  for (int rep = 0; rep < 4; ++rep) {
+    timeit("rep ldg<2> 1184 x 96 (product geometry)", [&] {
+      ldg<2><<<sms * 8, 96>>>((const double2 *)x, (double2 *)y, units, 0.125, 4.375); });
+    timeit("rep ldg_blk<4> 888 x 96", [&] {
+      ldg_blk<4><<<sms * 6, 96>>>((const double2 *)x, (double2 *)y, units, 0.125, 4.375); });
+    timeit("rep ldg_blk<2> 888 x 96", [&] {
+      ldg_blk<2><<<sms * 6, 96>>>((const double2 *)x, (double2 *)y, units, 0.125, 4.375); });
+  }
+  // contiguous per-thread blocks of K units
+  for (int k : {6, 8, 12, 16}) {
+    for (int thr : {96, 128, 256}) {
+      char nm[96];
+      snprintf(nm, sizeof nm, "ldg_blk<2> %d x %d", sms * k, thr);
+      timeit(nm, [&] { ldg_blk<2><<<sms * k, thr>>>((const double2 *)x, (double2 *)y, units, 0.125, 4.375); });
+      snprintf(nm, sizeof nm, "ldg_blk<4> %d x %d", sms * k, thr);
+      timeit(nm, [&] { ldg_blk<4><<<sms * k, thr>>>((const double2 *)x, (double2 *)y, units, 0.125, 4.375); });
     }
   }
   // pool-size sensitivity: the generic-mode kernel runs 96 workers per
