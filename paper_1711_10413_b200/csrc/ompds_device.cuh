@@ -462,12 +462,26 @@ struct WarpMask {
   uint32_t n;       // their count
   uint32_t leader;  // lowest participating lane (does the warp's bookkeeping)
   bool is_leader;
+  // Also loop-invariant for a team, so hoisted with the mask (of(t, mine)):
+  bool no_events;   // no event log: the fetch/retire fast paths apply
+  uint32_t win_off; // shared address of this lane's window entry (0: none)
   __device__ __forceinline__ static WarpMask of(bool mine) {
     WarpMask m;
     m.ballot = __ballot_sync(0xffffffffu, mine);
     m.n = __popc(m.ballot);
     m.leader = m.ballot ? __ffs(m.ballot) - 1 : 0;
     m.is_leader = m.ballot != 0 && lane_id() == m.leader;
+    m.no_events = false; // general paths only (still correct)
+    m.win_off = 0;
+    return m;
+  }
+  __device__ __forceinline__ static WarpMask of(const TeamCtx &t, bool mine) {
+    WarpMask m = of(mine);
+    m.no_events = t.events == nullptr;
+#if OMPDS_PREFETCH_WINDOW
+    if (static_cast<int32_t>(lane_id()) < t.prealloc)
+      m.win_off = static_cast<uint32_t>(__cvta_generic_to_shared(t.window)) + 8u * lane_id();
+#endif
     return m;
   }
 };
@@ -516,15 +530,11 @@ __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
                                                      const WarpMask &m,
                                                      bool mine) {
   Fetch f;
-  // Lane j's entry of the preallocated window is loaded alongside the team
-  // state (no dependency on the staged list pointer): when the region's list
-  // is the window, get-shared-variables needs no further load.
-  uint32_t win_off = 0;
-#if OMPDS_PREFETCH_WINDOW
-  if (static_cast<int32_t>(lane_id()) < t.prealloc)
-    win_off = static_cast<uint32_t>(__cvta_generic_to_shared(t.window)) + 8u * lane_id();
-#endif
-  const StagedState st = load_staged_state(t, win_off);
+  // Lane j's entry of the preallocated window (m.win_off) is loaded
+  // alongside the team state (no dependency on the staged list pointer):
+  // when the region's list is the window, get-shared-variables needs no
+  // further load.
+  const StagedState st = load_staged_state(t, m.win_off);
   const uint8_t ph = st.phase;
   f.win = st.win;
   f.workers = st.workers;
@@ -533,7 +543,7 @@ __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
   f.args = st.args;
   f.nargs = st.nargs;
   const uint32_t active = static_cast<uint32_t>(__cvta_generic_to_shared(&t.active_word()));
-  if (__builtin_expect(ph == kStaged && t.events == nullptr, 1)) {
+  if (__builtin_expect(ph == kStaged && m.no_events, 1)) {
     // The common case in one branch: a staged region and no event log.
     // Active += n: a plain store when this warp holds every participant
     // (Active is 0 between regions and no other warp fetches), otherwise
@@ -581,13 +591,16 @@ __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
 // What a worker warp needs to retire the region it fetched, packed in one
 // register so nothing else stays live across the region body: bit 0 = this
 // lane is the warp's leader, bit 1 = the warp holds all W participants,
-// bit 2 = the list is the window (nothing to free), bits 8.. = participants.
+// bit 2 = the list is the window (nothing to free), bit 3 = no event log,
+// bits 8.. = participants.
 __device__ __forceinline__ uint32_t retire_plan(const TeamCtx &t,
                                                 const WarpMask &m,
                                                 const Fetch &f) {
+  // the list is the window iff nargs <= PreallocEntries (the placement law
+  // of prepare_parallel, DeviceRuntime.cpp:61-74): a 32-bit compare
   return (m.n << 8) | (m.is_leader ? 1u : 0u) |
          (m.n == static_cast<uint32_t>(f.workers) ? 2u : 0u) |
-         (f.args == t.window || f.args == nullptr ? 4u : 0u);
+         (f.nargs <= t.prealloc ? 4u : 0u) | (m.no_events ? 8u : 0u);
 }
 
 // All 32 lanes of a worker warp call this when the region body is done.
@@ -600,7 +613,7 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
                                                   uint32_t plan) {
   const bool leader = plan & 1u;
   const uint32_t n = plan >> 8;
-  if (__builtin_expect((plan & 4u) && t.events == nullptr, 1)) {
+  if (__builtin_expect((plan & 12u) == 12u, 1)) { // window list, no event log
     if (plan & 2u) {
       // sole warp: it retires the last participant.  The __syncwarp orders
       // every lane's fetch reads before the leader's reset (lanes of one
@@ -730,7 +743,7 @@ __device__ __forceinline__ SharedVars get_shared_variables(void **args,
 __device__ __forceinline__ SharedVars get_shared_variables(const TeamCtx &t,
                                                            const Fetch &f) {
 #if OMPDS_PREFETCH_WINDOW
-  if (f.args == t.window) {
+  if (f.nargs <= t.prealloc && f.args != nullptr) { // the list is the window
     SharedVars v;
     v.mine = static_cast<int32_t>(lane_id()) < f.nargs ? f.win : nullptr;
     return v;

@@ -412,7 +412,7 @@ __global__ void OMPDS_GENERIC_LB
         p.warp_ovf ? p.warp_ovf + (size_t(blockIdx.x) * worker_warps + warp) * p.warp_ovf_bytes
                    : nullptr;
     w.ds.init(slot, p.warp_slot_bytes, ovf, p.warp_ovf ? p.warp_ovf_bytes : 0);
-    const WarpMask wm = WarpMask::of(w.mine); // loop-invariant participation
+    const WarpMask wm = WarpMask::of(t, w.mine); // loop-invariant participation
     for (int32_t rr = 0;; ++rr) {
       bar_sync(kBarHandoff, team_threads); // await.work
       OMPDS_TL(rr, 5);
