@@ -138,6 +138,8 @@ struct Master {
   const TeamParams *p;
   bool leader;
   bool join_completes; // completes_at_join(): several worker warps, no event log
+  int32_t fast_nargs;  // the fast prepare applies to nargs <= this: the
+                       // window size without an event log, -1 with one
   uint32_t team_threads;
   int32_t trap = 0;
   int32_t barriers = 0;
@@ -211,7 +213,7 @@ struct Master {
     // (traps, a global list, events) takes parallel_general.
     const PrepareState st = load_prepare_state(t);
     if (__builtin_expect(st.phase == kIdle && st.active == 0 && nargs >= 0 &&
-                             nargs <= t.prealloc && t.events == nullptr, 1)) {
+                             nargs <= fast_nargs, 1)) {
       __syncwarp(); // every lane has read the state before the master stages
       OMPDS_TL(regions, 1);
       stage_region_if(t, fn, nargs, t.window, leader);
@@ -443,6 +445,7 @@ __global__ void OMPDS_GENERIC_LB
     m.p = &p;
     m.leader = lane_id() == 0;
     m.join_completes = completes_at_join(t, p.workers);
+    m.fast_nargs = t.events == nullptr ? t.prealloc : -1;
     m.team_threads = team_threads;
     if (m.init() == OMPDS_OK && m.push_depot() == OMPDS_OK)
       Prog::master(m, a);
