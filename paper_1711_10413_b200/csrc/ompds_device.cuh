@@ -121,6 +121,8 @@ struct TeamCtx {
   ompds_event *events;     // per-team event log (nullptr: off)
   int32_t max_events;
   int32_t list_malloc;     // args lists past the window: 1 device malloc, 0 slab
+  uint32_t rt_s;           // shared-window addresses of rt / window (computed
+  uint32_t window_s;       // once: no address conversion on the region path)
 
   template <class T> __device__ __forceinline__ T &at(int off) const {
     return *reinterpret_cast<T *>(rt + off);
@@ -221,6 +223,8 @@ __device__ __forceinline__ TeamCtx make_team(unsigned char *smem,
   t.events = events;
   t.max_events = max_events;
   t.list_malloc = list_malloc;
+  t.rt_s = static_cast<uint32_t>(__cvta_generic_to_shared(t.rt));
+  t.window_s = static_cast<uint32_t>(__cvta_generic_to_shared(t.window));
   return t;
 }
 
@@ -232,7 +236,7 @@ struct PrepareState {
   int32_t active;
 };
 __device__ __forceinline__ PrepareState load_prepare_state(const TeamCtx &t) {
-  const uint32_t rt = static_cast<uint32_t>(__cvta_generic_to_shared(t.rt));
+  const uint32_t rt = t.rt_s;
   uint32_t ph, aw;
   asm volatile("ld.shared.u8 %0, [%2+48];\n\t"
                "ld.shared.u32 %1, [%2+20];"
@@ -253,7 +257,7 @@ struct StagedState {
 // `win_off`: shared address of this lane's window entry, 0 = none.
 __device__ __forceinline__ StagedState load_staged_state(const TeamCtx &t,
                                                          uint32_t win_off) {
-  const uint32_t rt = static_cast<uint32_t>(__cvta_generic_to_shared(t.rt));
+  const uint32_t rt = t.rt_s;
   uint32_t ph, fn, na, wk;
   unsigned long long args, win = 0;
   static_assert(Rt::kArgs == 0 && Rt::kWorkFn == 8 && Rt::kNArgs == 12 &&
@@ -480,7 +484,7 @@ struct WarpMask {
     m.no_events = t.events == nullptr;
 #if OMPDS_PREFETCH_WINDOW
     if (static_cast<int32_t>(lane_id()) < t.prealloc)
-      m.win_off = static_cast<uint32_t>(__cvta_generic_to_shared(t.window)) + 8u * lane_id();
+      m.win_off = t.window_s + 8u * lane_id();
 #endif
     return m;
   }
@@ -497,7 +501,7 @@ __device__ __forceinline__ void red_add_if(uint32_t saddr, uint32_t v, bool p) {
 // retire of a region whose list is the window: args = null, work_fn = -1,
 // nargs = 0, Active word = 0, phase = Idle (retire_last's window case).
 __device__ __forceinline__ void retire_window_if(const TeamCtx &t, bool p) {
-  const uint32_t rt = static_cast<uint32_t>(__cvta_generic_to_shared(t.rt));
+  const uint32_t rt = t.rt_s;
   static_assert(Rt::kArgs == 0 && Rt::kWorkFn == 8 && Rt::kNArgs == 12 &&
                     Rt::kActive == 20 && Rt::kPhase == 48, "rt layout");
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t"
@@ -512,7 +516,7 @@ __device__ __forceinline__ void retire_window_if(const TeamCtx &t, bool p) {
 // staging of a region (stage_region's stores), predicated on `p`.
 __device__ __forceinline__ void stage_region_if(const TeamCtx &t, int32_t fn,
                                                 int32_t nargs, void **list, bool p) {
-  const uint32_t rt = static_cast<uint32_t>(__cvta_generic_to_shared(t.rt));
+  const uint32_t rt = t.rt_s;
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t"
                "@q st.shared.u64 [%0], %2;\n\t"
                "@q st.shared.v2.u32 [%0+8], {%3, %4};\n\t"
@@ -542,7 +546,7 @@ __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
   f.fn = st.fn;
   f.args = st.args;
   f.nargs = st.nargs;
-  const uint32_t active = static_cast<uint32_t>(__cvta_generic_to_shared(&t.active_word()));
+  const uint32_t active = t.rt_s + Rt::kActive;
   if (__builtin_expect(ph == kStaged && m.no_events, 1)) {
     // The common case in one branch: a staged region and no event log.
     // Active += n: a plain store when this warp holds every participant
@@ -626,7 +630,7 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
       // Active -= n); the join barrier orders every retirement before the
       // master, which observes retired == W and completes the last
       // retirement (complete_region) -- no returning atomic on any worker.
-      red_add_if(static_cast<uint32_t>(__cvta_generic_to_shared(&t.active_word())),
+      red_add_if(t.rt_s + Rt::kActive,
                  (n << 16) - n, leader);
     }
     return;
@@ -663,7 +667,7 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
     uint32_t old;
     asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
                  : "=r"(old)
-                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(&t.active_word()))),
+                 : "r"(t.rt_s + Rt::kActive),
                    "r"((n << 16) - n)
                  : "memory");
     const uint32_t retired = (old >> 16) + n;

@@ -217,7 +217,7 @@ struct Master {
       __syncwarp(); // every lane has read the state before the master stages
       OMPDS_TL(regions, 1);
       stage_region_if(t, fn, nargs, t.window, leader);
-      const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(t.window));
+      const uint32_t sa = t.window_s;
       const int lane = static_cast<int>(lane_id());
       if (lane < nargs) // one predicated STS per lane for lists up to 32 entries
         asm volatile("st.shared.u64 [%0], %1;" ::"r"(sa + 8u * lane),
@@ -284,7 +284,7 @@ struct Master {
     // coalesced store per 32 entries) instead of nargs scalar stores.
     const int lane = static_cast<int>(lane_id());
     if (list == t.window) { // the smem window: STS, not generic stores
-      const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(t.window));
+      const uint32_t sa = t.window_s;
       for (int j = lane; ok && j < nargs; j += 32)
         asm volatile("st.shared.u64 [%0], %1;" ::"r"(sa + 8u * j),
                      "l"(reinterpret_cast<unsigned long long>(addr_of(j)))
