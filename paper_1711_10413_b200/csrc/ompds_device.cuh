@@ -530,37 +530,46 @@ __device__ __forceinline__ void stage_region_if(const TeamCtx &t, int32_t fn,
 
 // All 32 lanes of a worker warp call this after the release barrier.
 // `mine` = this lane is a requested worker (tid < W); `m` = WarpMask::of(mine).
-__device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
-                                                     const WarpMask &m,
-                                                     bool mine) {
+// Fetch from an already loaded team state (the loop issues the loads right
+// after the release barrier).  `fast` is the common case -- a staged region
+// and no event log -- decided by the caller.
+__device__ __forceinline__ Fetch fetch_from(const StagedState &st) {
   Fetch f;
-  // Lane j's entry of the preallocated window (m.win_off) is loaded
-  // alongside the team state (no dependency on the staged list pointer):
-  // when the region's list is the window, get-shared-variables needs no
-  // further load.
-  const StagedState st = load_staged_state(t, m.win_off);
-  const uint8_t ph = st.phase;
   f.win = st.win;
   f.workers = st.workers;
   f.status = OMPDS_OK;
   f.fn = st.fn;
   f.args = st.args;
   f.nargs = st.nargs;
-  const uint32_t active = t.rt_s + Rt::kActive;
-  if (__builtin_expect(ph == kStaged && m.no_events, 1)) {
-    // The common case in one branch: a staged region and no event log.
-    // Active += n: a plain store when this warp holds every participant
-    // (Active is 0 between regions and no other warp fetches), otherwise
-    // one fire-and-forget shared atomic.
-    if (m.n == static_cast<uint32_t>(st.workers))
-      asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
-                   "@q st.shared.u32 [%0], %1;\n\t}" ::"r"(active), "r"(m.n),
-                   "r"(static_cast<uint32_t>(m.is_leader))
-                   : "memory");
-    else
-      red_add_if(active, m.n, m.is_leader);
-    return f;
-  }
+  return f;
+}
+__device__ __forceinline__ bool fetch_is_fast(const StagedState &st,
+                                              const WarpMask &m) {
+  return st.phase == kStaged && m.no_events;
+}
+// The fast fetch's bookkeeping, branch-free: Active += n by the warp's
+// leader -- a plain store when this warp holds every participant (Active is
+// 0 between regions and no other warp fetches), otherwise one
+// fire-and-forget shared atomic.
+__device__ __forceinline__ void fetch_account_fast(const TeamCtx &t,
+                                                   const StagedState &st,
+                                                   const WarpMask &m) {
+  const bool sole = m.n == static_cast<uint32_t>(st.workers);
+  asm volatile("{\n\t.reg .pred qs, qm;\n\t"
+               "setp.ne.u32 qs, %2, 0;\n\t"
+               "setp.ne.u32 qm, %3, 0;\n\t"
+               "@qs st.shared.u32 [%0], %1;\n\t"
+               "@qm red.shared.add.u32 [%0], %1;\n\t}" ::"r"(t.rt_s + Rt::kActive),
+               "r"(m.n), "r"(static_cast<uint32_t>(m.is_leader && sole)),
+               "r"(static_cast<uint32_t>(m.is_leader && !sole))
+               : "memory");
+}
+// Every other case of the reference's kernel_parallel for a warp:
+// termination, a fetch with nothing staged (trap), and the event log.
+__device__ __forceinline__ Fetch fetch_general(const TeamCtx &t, const StagedState &st,
+                                            const WarpMask &m, bool mine) {
+  Fetch f = fetch_from(st);
+  const uint8_t ph = st.phase;
   if (ph == kTerminated) {
     f.fn = -1;
     f.args = nullptr;
@@ -574,6 +583,10 @@ __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
   }
   if (m.n == 0)
     return f;
+  if (!t.events) { // staged, no log, reached through a general mask
+    fetch_account_fast(t, st, m);
+    return f;
+  }
   // staged, event log on
   int64_t ev = -1;
   if (m.is_leader) {
@@ -586,6 +599,21 @@ __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
     t.log_at(ev + __popc(m.ballot & ((1u << lane) - 1u)), OMPDS_EV_FETCH, f.fn,
              0, 0);
   return f;
+}
+
+__device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
+                                                     const WarpMask &m,
+                                                     bool mine) {
+  // Lane j's entry of the preallocated window (m.win_off) is loaded
+  // alongside the team state (no dependency on the staged list pointer):
+  // when the region's list is the window, get-shared-variables needs no
+  // further load.
+  const StagedState st = load_staged_state(t, m.win_off);
+  if (__builtin_expect(fetch_is_fast(st, m), 1)) {
+    fetch_account_fast(t, st, m);
+    return fetch_from(st);
+  }
+  return fetch_general(t, st, m, mine);
 }
 __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
                                                      bool mine) {

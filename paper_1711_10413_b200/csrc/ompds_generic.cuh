@@ -418,14 +418,21 @@ __global__ void OMPDS_GENERIC_LB
     for (int32_t rr = 0;; ++rr) {
       bar_sync(kBarHandoff, team_threads); // await.work
       OMPDS_TL(rr, 5);
-      Fetch f = begin_parallel_warp(t, wm, w.mine);
-      OMPDS_TL(rr, 6);
-      if (f.fn < 0) {
-        if (f.status == OMPDS_OK)
-          break; // termination sentinel (wf == null)
-        bar_sync(kBarHandoff, team_threads); // trapped fetch: skip the region
-        continue;
+      const StagedState st = load_staged_state(t, wm.win_off);
+      Fetch f;
+      if (__builtin_expect(fetch_is_fast(st, wm), 1)) {
+        fetch_account_fast(t, st, wm); // a staged region, no event log
+        f = fetch_from(st);
+      } else {
+        f = fetch_general(t, st, wm, w.mine);
+        if (f.fn < 0) {
+          if (f.status == OMPDS_OK)
+            break; // termination sentinel (wf == null)
+          bar_sync(kBarHandoff, team_threads); // trapped fetch: skip the region
+          continue;
+        }
       }
+      OMPDS_TL(rr, 6);
       w.args = f.args;
       w.nargs = f.nargs;
       w.region_index = rr;
