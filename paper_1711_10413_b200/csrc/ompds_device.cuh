@@ -775,7 +775,9 @@ __device__ __forceinline__ SharedVars get_shared_variables(void **args,
 __device__ __forceinline__ SharedVars get_shared_variables(const TeamCtx &t,
                                                            const Fetch &f) {
 #if OMPDS_PREFETCH_WINDOW
-  if (f.nargs <= t.prealloc && f.args != nullptr) { // the list is the window
+  // the list is the window (placement law; a fetched region's list is never
+  // null -- terminated or trapped fetches never reach get-shared-variables)
+  if (f.nargs <= t.prealloc) {
     SharedVars v;
     v.mine = static_cast<int32_t>(lane_id()) < f.nargs ? f.win : nullptr;
     return v;

@@ -65,8 +65,9 @@ template <class T> struct RegionsProg {
     // get-shared-variables: lane j < 4 dereferences capture j once (slots
     // are 8-byte sized and aligned, so one 8-byte load covers an int or a
     // T slot), shuffles spread the four values.
+    // (the master published 4 entries: lanes 0..3 hold non-null pointers)
     unsigned long long raw = 0;
-    if (lane_id() < 4 && sv.mine)
+    if (lane_id() < 4)
       raw = *static_cast<const unsigned long long *>(sv.mine);
     const int32_t c1 = __shfl_sync(0xffffffffu, static_cast<int32_t>(raw), 0);
     const int32_t c2 = __shfl_sync(0xffffffffu, static_cast<int32_t>(raw), 1);
