@@ -397,7 +397,7 @@ def main():
         "config": {"workload": "config4_stream_region", "elements_per_gpu": n,
                    "elements_total": n_total, "teams": teams, "workers": workers,
                    "threads_per_team": ((workers + 31) // 32) * 32 + 32,
-                   "shared_scalars": 8, "parallelism": f"team-range shards x{world}",
+                   "shared_scalars": 8, "parallelism": f"element-range shards x{world}",
                    "l2": "inputs (2 x 8 B x n) larger than the 126 MB L2, no flush needed"},
         "roofline": roofline,
         "regions": {"ns_per_region": round(ns_per_region, 1),
@@ -416,6 +416,7 @@ def main():
         "occupancy": {"model": "b200 row of the reference occupancy model",
                       "teams_by_regs": occ.teams_by_regs, "teams_by_smem": occ.teams_by_smem,
                       "teams_per_sm": occ.actual, "threads_per_team": thr,
+                      "grid_teams_per_sm": round(teams / sms, 2),
                       "binding_limit": "registers" if occ.actual == occ.teams_by_regs
                       else "smem" if occ.actual == occ.teams_by_smem else "blocks/threads"},
         "checksum": f"{checksum:#018x}",
