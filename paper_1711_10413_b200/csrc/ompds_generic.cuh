@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -464,40 +465,39 @@ __global__ void OMPDS_GENERIC_LB
 // Host side: workspace, layouts for the fixed configs, launch helper.
 //===----------------------------------------------------------------------===//
 
-// Library-owned global memory reused across launches on a device: buffer 0
-// holds the teams' overflow slabs (args lists, master depot overflow),
-// buffer 1 the worker warps' data-sharing overflow chains, buffer 2 a region
-// program's tables, buffer 3 the masters' local depot mirrors.  Launches
-// that run concurrently on different streams must not share a device.
-struct Workspace {
-  std::mutex mu;
-  int device = -1;
+// Library-owned global memory reused across launches, one set per (device,
+// stream): buffer 0 holds the teams' overflow slabs (args lists, master
+// depot overflow), buffer 1 the worker warps' data-sharing overflow chains,
+// buffer 2 a region program's tables, buffer 3 the masters' local depot
+// mirrors.  Launches on one stream run in order, so they can share a set;
+// launches on different streams (or devices) get their own.
+struct WsBuffers {
   unsigned char *buf[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t bytes[4] = {0, 0, 0, 0};
 };
+struct Workspace {
+  std::mutex mu;
+  std::map<std::pair<int, void *>, WsBuffers> sets;
+};
 inline Workspace g_ws;
 
-inline int32_t ensure_buffer(int which, size_t bytes, unsigned char **out) {
+inline int32_t ensure_buffer(int which, size_t bytes, unsigned char **out,
+                             void *stream = nullptr) {
   std::lock_guard<std::mutex> lk(g_ws.mu);
   int dev = 0;
   OMPDS_CUDA(cudaGetDevice(&dev));
-  if (g_ws.device != dev) {
-    for (int i = 0; i < 4; ++i) { // leaked on device switch (bounded, rare)
-      g_ws.buf[i] = nullptr;
-      g_ws.bytes[i] = 0;
+  WsBuffers &w = g_ws.sets[{dev, stream}];
+  if (w.bytes[which] < bytes) {
+    if (w.buf[which]) { // earlier launches on this stream may still use it
+      OMPDS_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+      OMPDS_CUDA(cudaFree(w.buf[which]));
     }
-    g_ws.device = dev;
+    w.buf[which] = nullptr;
+    w.bytes[which] = 0;
+    OMPDS_CUDA(cudaMalloc(&w.buf[which], bytes));
+    w.bytes[which] = bytes;
   }
-  if (g_ws.bytes[which] < bytes) {
-    if (g_ws.buf[which]) {
-      OMPDS_CUDA(cudaDeviceSynchronize());
-      OMPDS_CUDA(cudaFree(g_ws.buf[which]));
-    }
-    g_ws.buf[which] = nullptr;
-    OMPDS_CUDA(cudaMalloc(&g_ws.buf[which], bytes));
-    g_ws.bytes[which] = bytes;
-  }
-  *out = g_ws.buf[which];
+  *out = w.buf[which];
   return OMPDS_OK;
 }
 
@@ -579,7 +579,7 @@ int32_t launch_generic(const ompds_launch *l, const FixedLayout &lay,
   p.aux_off = lay.aux_off;
   p.slab_bytes = std::max<uint32_t>(
       kSlabBytes, static_cast<uint32_t>(round_up(2 * lay.total_shared + 64, 256)));
-  s = ensure_buffer(0, size_t(p.slab_bytes) * l->teams, &p.slabs);
+  s = ensure_buffer(0, size_t(p.slab_bytes) * l->teams, &p.slabs, l->stream);
   if (s)
     return s;
   const int threads = static_cast<int>(round_up(l->workers, 32)) + 32;
@@ -587,7 +587,8 @@ int32_t launch_generic(const ompds_launch *l, const FixedLayout &lay,
   p.warp_slot_bytes = round_up(warp_slot_bytes, 16);
   p.warp_ovf_bytes = round_up(warp_ovf_bytes, 256);
   if (p.warp_ovf_bytes > 0) {
-    s = ensure_buffer(1, size_t(p.warp_ovf_bytes) * worker_warps * l->teams, &p.warp_ovf);
+    s = ensure_buffer(1, size_t(p.warp_ovf_bytes) * worker_warps * l->teams, &p.warp_ovf,
+                      l->stream);
     if (s)
       return s;
   }

@@ -961,10 +961,11 @@ int32_t ompds_run_program(const ompds_launch *launch, const ompds_program *pr,
   if (sz_caps) std::memcpy(host.data() + o_caps, pr->captures, sz_caps);
   if (sz_bufs) std::memcpy(host.data() + o_bufs, pr->buffers, sz_bufs);
   unsigned char *dev = nullptr, *mlocal = nullptr;
-  int32_t s = ensure_buffer(2, total, &dev);
+  int32_t s = ensure_buffer(2, total, &dev, launch->stream);
   if (s)
     return s;
-  s = ensure_buffer(3, size_t(std::max<int64_t>(pr->total_local, 4)) * launch->teams, &mlocal);
+  s = ensure_buffer(3, size_t(std::max<int64_t>(pr->total_local, 4)) * launch->teams, &mlocal,
+                    launch->stream);
   if (s)
     return s;
   cudaStream_t st = static_cast<cudaStream_t>(launch->stream);
