@@ -337,3 +337,26 @@ def test_event_trace_times_follow_the_handoff_barriers(teams, workers):
             assert all(t[i] <= t[nxt] for i in body), r
             assert sum(1 for i in body if kinds[i] == "fetch") == workers
             assert sum(1 for i in body if kinds[i] == "retire") == workers
+
+
+def test_concurrent_launches_on_two_streams_do_not_share_the_slab():
+    """Args lists past the window live in the per-team slab of a workspace
+    that is per (device, stream): two launches in flight on two streams,
+    both spilling every region's list, still produce the oracle's values."""
+    teams, workers, regions = 148, 64, 20
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    arrays = []
+    for st in streams:
+        a = torch.zeros(teams * workers, dtype=torch.int32, device=DEV)
+        arrays.append(a)
+    torch.cuda.synchronize()
+    for st, a in zip(streams, arrays):
+        outs.append(RG.run_regions(a, teams, workers, regions, prealloc_entries=2, stream=st))
+    torch.cuda.synchronize()
+    want = np.zeros(teams * workers, dtype=np.int32)
+    O.lib().orc_regions(0, teams, workers, regions, O.ptr(want))
+    for a, out in zip(arrays, outs):
+        assert np.array_equal(a.cpu().numpy(), want)
+        assert all((s.trap, s.dynamic_allocs, s.dynamic_frees) == (0, regions, regions)
+                   for s in out.team_stats())
