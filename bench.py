@@ -227,6 +227,9 @@ def run_reference(args):
     base["value"] = round(gbs, 6)
     base["ms_per_step"] = round(el / args.steps * 1e3, 3)
     base["config"]["elements_per_step"] = n
+    # same metric as our arm: config-4 elements processed per second x 24 B
+    # (the reference's i32 elements would move 12 B; counting 24 favours it)
+    base["config"]["bytes_counted_per_element"] = BYTES_PER_ELEM
     base["cpu_baseline"] = {"value": base["value"], "unit": "GB/s", "cores": threads,
                             "kind": "reference",
                             "sample": f"{nchunks} chunks x {chunk} int elements per step, "
