@@ -76,6 +76,12 @@ const char *ompds_last_error(void);
 uint32_t ompds_version(void);
 /* Number of usable CUDA devices (0 when none). */
 int32_t ompds_device_count(void);
+/* Frees the library's device workspace (stack overflow chains, args-list
+ * slabs, program tables) kept for `stream` (a cudaStream_t, NULL = the
+ * default stream) on the current device, after waiting for the stream's
+ * work.  Call it before destroying a stream the library launched on; the
+ * next launch on a stream reallocates on demand. */
+int32_t ompds_release_workspace(void *stream);
 
 /* ------------------------------------------------------------------------ */
 /* Team runtime protocol: omplab::TeamRuntime  (DeviceRuntime.h:81-119)     */

@@ -141,6 +141,7 @@ _SIGS = {
     "ompds_last_error": (C.c_char_p, []),
     "ompds_version": (C.c_uint32, []),
     "ompds_device_count": (C.c_int32, []),
+    "ompds_release_workspace": (C.c_int32, [C.c_void_p]),
     "ompds_rt_replay": (C.c_int32, [C.POINTER(RuntimeConfig), C.POINTER(RtCall), C.c_int32,
                                      C.POINTER(RtResult), C.POINTER(Event), C.c_int32,
                                      C.POINTER(RtSummary)]),

@@ -501,6 +501,24 @@ inline int32_t ensure_buffer(int which, size_t bytes, unsigned char **out,
   return OMPDS_OK;
 }
 
+inline int32_t release_workspace(void *stream) {
+  std::lock_guard<std::mutex> lk(g_ws.mu);
+  int dev = 0;
+  OMPDS_CUDA(cudaGetDevice(&dev));
+  auto it = g_ws.sets.find({dev, stream});
+  if (it == g_ws.sets.end())
+    return OMPDS_OK;
+  OMPDS_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  for (int k = 0; k < 4; ++k) {
+    unsigned char *b = it->second.buf[k];
+    it->second.buf[k] = nullptr;
+    it->second.bytes[k] = 0;
+    if (b)
+      OMPDS_CUDA(cudaFree(b));
+  }
+  g_ws.sets.erase(it);
+  return OMPDS_OK;
+}
 
 // Kernel frame group of a fixed config, in the reference's emission order:
 // captured locals, then sequential loop counters, then __omp_worker's

@@ -750,6 +750,8 @@ int32_t ompds_device_count(void) {
   return n;
 }
 
+int32_t ompds_release_workspace(void *stream) { return release_workspace(stream); }
+
 int64_t ompds_team_smem_bytes(int64_t depot_capacity, int32_t prealloc) {
   return team_region_bytes(round_up(depot_capacity, 8), prealloc);
 }

@@ -254,6 +254,13 @@ def fill_uniform(t: torch.Tensor, seed: int, first: int = 0,
                                        seed, first, C.c_void_p(s)), "ompds_fill_uniform")
 
 
+def release_workspace(stream: Optional[torch.cuda.Stream] = None) -> None:
+    """Frees the library's device workspace kept for `stream` on the current
+    device (waits for the stream first); the next launch reallocates."""
+    s = (stream or torch.cuda.current_stream()).cuda_stream
+    L.check(L.lib().ompds_release_workspace(C.c_void_p(s)), "ompds_release_workspace")
+
+
 def checksum(t: torch.Tensor, stream: Optional[torch.cuda.Stream] = None) -> int:
     """Sum of the elements' bit patterns mod 2^64 (order independent, exact)."""
     _require_cuda(t)

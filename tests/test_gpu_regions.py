@@ -360,3 +360,23 @@ def test_concurrent_launches_on_two_streams_do_not_share_the_slab():
         assert np.array_equal(a.cpu().numpy(), want)
         assert all((s.trap, s.dynamic_allocs, s.dynamic_frees) == (0, regions, regions)
                    for s in out.team_stats())
+
+
+@pytest.mark.gpu
+def test_release_workspace_then_relaunch_on_the_same_stream():
+    """ompds_release_workspace frees a stream's slabs and chains after its
+    work; the next launch on that stream reallocates and is exact, and
+    releasing a stream the library never used is a no-op."""
+    teams, workers, regions = 64, 40, 6
+    st = torch.cuda.Stream()
+    want = np.zeros(teams * workers, dtype=np.int32)
+    O.lib().orc_regions(0, teams, workers, regions, O.ptr(want))
+    for _ in range(2):
+        a = torch.zeros(teams * workers, dtype=torch.int32, device=DEV)
+        torch.cuda.synchronize()
+        out = RG.run_regions(a, teams, workers, regions, prealloc_entries=2, stream=st)
+        RG.release_workspace(st)
+        assert np.array_equal(a.cpu().numpy(), want)
+        assert all((s.trap, s.dynamic_allocs, s.dynamic_frees) == (0, regions, regions)
+                   for s in out.team_stats())
+    RG.release_workspace(torch.cuda.Stream())
