@@ -4,6 +4,8 @@ C ABI: integer analogs bit-exact against the reference's own simulator output
 kernels and the oracle use the same explicit fma / add order; the stated
 tolerance would be 1e-12 relative), runtime statistics against the
 reference's barrier / allocation laws."""
+import functools
+
 import numpy as np
 import pytest
 import torch
@@ -213,19 +215,25 @@ def test_config4_host_buffer_entry_point_matches_oracle():
     assert np.array_equal(yh.numpy().view(np.uint64), ys.view(np.uint64))
 
 
-def test_config4_full_size_checksum_vs_oracle():
-    n = 1 << 28
-    x, y = _f64_inputs(n)
-    RG.run_stream(x, y, COEF, 296, 992, stats=False)
-    torch.cuda.synchronize()
-    got = RG.checksum(y)
-    del x, y
+@functools.lru_cache(maxsize=None)
+def _full_size_oracle_checksum(n):
     xs = np.empty(n)
     ys = np.empty(n)
     O.lib().orc_fill(1, O.ptr(xs), n, 0x5eed01ab, 0)
     O.lib().orc_fill(1, O.ptr(ys), n, 0x5eed01ac, 0)
     O.lib().orc_stream(1, n, O.ptr(xs), O.ptr(ys), O.ptr(np.array(COEF)), 0)
-    assert got == O.lib().orc_checksum(1, O.ptr(ys), n)
+    return O.lib().orc_checksum(1, O.ptr(ys), n)
+
+
+@pytest.mark.parametrize("teams,workers", [(296, 992), (148 * 7, 96)])  # 2nd: bench.py's grid
+def test_config4_full_size_checksum_vs_oracle(teams, workers):
+    n = 1 << 28
+    x, y = _f64_inputs(n)
+    RG.run_stream(x, y, COEF, teams, workers, stats=False)
+    torch.cuda.synchronize()
+    got = RG.checksum(y)
+    del x, y
+    assert got == _full_size_oracle_checksum(n)
 
 
 # --------------------------------------------------------------------------- config 5
