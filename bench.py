@@ -368,6 +368,19 @@ def main():
             row[f"ns_per_region_{label}"] = round(ms_p * 1e6 / rr, 1)
             row[f"regions_per_s_{label}"] = round(tm * rr / (ms_p * 1e-3), 0)
         placement[name] = row
+    # north_star's "push/pop + handoff overhead in ns per parallel region":
+    # the building blocks timed alone on one SM (ompds_probe_overheads), and
+    # the config-1 region split into the bare handoff and the rest (runtime
+    # protocol + get-shared-variables + body)
+    ov = RG.probe_overheads(8192, stream=stream)
+    ov["config1_ns_per_region"] = round(ns_per_region, 1)
+    ov["config1_protocol_ns_per_region"] = round(ns_per_region - ov["handoff_ns"], 1)
+    # config 3: each worker warp pushes and pops 2 frames per nested region
+    ov["config3_push_pop_ns_per_region"] = round(2 * ov["push_pop_pair_slot_ns"], 2)
+    ov["how"] = ("one 2-warp CTA, clock64 and %globaltimer over 8192 iterations each; "
+                 "push_pop_pair_* = (push + store/load in a 40 B/lane frame + pop) - "
+                 "(the same store/load at a fixed smem address); handoff = release + "
+                 "join named barriers between the master and one worker warp")
     configs = other_configs(RG, dev, stream, sms) if rank == 0 else {}
     from paper_1711_10413_b200 import occupancy as OCC
     regs = ptxas_regs("StreamProgIdE") or 64
@@ -412,7 +425,8 @@ def main():
                     "aggregate_workload": f"{world * teams2} teams x 32 workers x {R2} regions"
                                           + (f", team grid sharded by range over {world} GPUs"
                                              if world > 1 else ""),
-                    "args_list_placement": placement},
+                    "args_list_placement": placement,
+                    "overheads": ov},
         "smem_bytes_per_cta": smem_bytes,
         "smem_layout": "depot 80 + args window 160 + runtime span 49 (reference footprint 289)",
         "regs_per_thread": regs,

@@ -428,6 +428,33 @@ int32_t ompds_fill_uniform(int32_t elem, void *out, int64_t n, uint64_t seed,
 int32_t ompds_checksum(int32_t elem, const void *data, int64_t n,
                        uint64_t *out_dev, void *stream);
 
+/* Cost of the runtime's building blocks on one SM (north_star: "push/pop +
+ * handoff overhead"), measured by one 2-warp CTA with clock64 and
+ * %globaltimer over `iterations` iterations each:
+ *   smem_access    a store + load at a fixed shared address (the baseline);
+ *   push_pop_slot  data-sharing stack push of a 40-byte-per-lane frame (the
+ *                  config-3 level-1 frame), the same store + load in it, pop
+ *                  -- frame in the warp's shared-memory slot;
+ *   push_pop_chain the same with the frame on the global overflow chain;
+ *   handoff        master warp <-> worker warp: the release and the join
+ *                  barrier of one region with nothing staged (named barrier
+ *                  1, non-aligned, as the team kernels use).
+ * Push/pop overhead per pair = push_pop_* - smem_access. */
+typedef struct ompds_overhead_probe {
+  int32_t iterations;
+  int32_t reserved0;
+  double sm_clock_mhz; /* clock64 cycles per %globaltimer microsecond */
+  double smem_access_cycles;
+  double push_pop_slot_cycles;
+  double push_pop_chain_cycles;
+  double handoff_cycles;
+} ompds_overhead_probe; /* 48 bytes */
+
+/* Runs the probe on the current device and `stream`; synchronises and
+ * writes `*out` (host memory).  iterations in [1, 1<<20]. */
+int32_t ompds_probe_overheads(int32_t iterations, ompds_overhead_probe *out,
+                              void *stream);
+
 /* Dynamic smem bytes per CTA the launchers request for a team region with
  * depot `total_shared` (== ompds_shared_footprint for the reference layout). */
 int64_t ompds_team_smem_bytes(int64_t depot_capacity, int32_t prealloc_entries);

@@ -101,6 +101,13 @@ class Launch(C.Structure):
                 ("total_teams", C.c_int32), ("reserved0", C.c_int32)]
 
 
+class OverheadProbe(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("reserved0", C.c_int32),
+                ("sm_clock_mhz", C.c_double), ("smem_access_cycles", C.c_double),
+                ("push_pop_slot_cycles", C.c_double), ("push_pop_chain_cycles", C.c_double),
+                ("handoff_cycles", C.c_double)]
+
+
 class TeamStats(C.Structure):
     _fields_ = [("trap", C.c_int32), ("master_barriers", C.c_int32),
                 ("barrier_releases", C.c_int32), ("regions", C.c_int32),
@@ -167,6 +174,7 @@ _SIGS = {
                                            _P, _P]),
     "ompds_fill_uniform": (C.c_int32, [C.c_int32, _P, C.c_int64, C.c_uint64, C.c_int64, _P]),
     "ompds_checksum": (C.c_int32, [C.c_int32, _P, C.c_int64, _P, _P]),
+    "ompds_probe_overheads": (C.c_int32, [C.c_int32, C.POINTER(OverheadProbe), _P]),
     "ompds_team_smem_bytes": (C.c_int64, [C.c_int64, C.c_int32]),
 }
 

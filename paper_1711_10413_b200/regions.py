@@ -254,6 +254,29 @@ def fill_uniform(t: torch.Tensor, seed: int, first: int = 0,
                                        seed, first, C.c_void_p(s)), "ompds_fill_uniform")
 
 
+def probe_overheads(iterations: int = 8192,
+                    stream: Optional[torch.cuda.Stream] = None) -> dict:
+    """The runtime's building blocks on one SM (ompds_probe_overheads):
+    cycles and ns per data-sharing stack push + pop pair (frame in the smem
+    slot / on the global chain, net of the store + load done in the frame)
+    and per bare region handoff (release + join barriers)."""
+    p = L.OverheadProbe()
+    s = (stream or torch.cuda.current_stream()).cuda_stream
+    L.check(L.lib().ompds_probe_overheads(iterations, C.byref(p), C.c_void_p(s)),
+            "ompds_probe_overheads")
+    ns = 1e3 / p.sm_clock_mhz if p.sm_clock_mhz > 0 else float("nan")
+    slot = p.push_pop_slot_cycles - p.smem_access_cycles
+    chain = p.push_pop_chain_cycles - p.smem_access_cycles
+    return {"iterations": p.iterations, "sm_clock_mhz": round(p.sm_clock_mhz, 1),
+            "smem_store_load_cycles": round(p.smem_access_cycles, 2),
+            "push_pop_pair_slot_cycles": round(slot, 2),
+            "push_pop_pair_slot_ns": round(slot * ns, 2),
+            "push_pop_pair_chain_cycles": round(chain, 2),
+            "push_pop_pair_chain_ns": round(chain * ns, 2),
+            "handoff_cycles": round(p.handoff_cycles, 2),
+            "handoff_ns": round(p.handoff_cycles * ns, 2)}
+
+
 def release_workspace(stream: Optional[torch.cuda.Stream] = None) -> None:
     """Frees the library's device workspace kept for `stream` on the current
     device (waits for the stream first); the next launch reallocates."""

@@ -44,6 +44,7 @@ def test_struct_sizes_match_the_c_abi():
     assert C.sizeof(P.DepotLayout) == 32
     assert C.sizeof(P.Launch) == 56
     assert C.sizeof(P.TeamStats) == 56
+    assert C.sizeof(P.OverheadProbe) == 48
 
 
 def test_trap_strings_are_the_reference_strings():
@@ -222,3 +223,13 @@ def test_team_range_outside_the_grid_is_rejected(first, teams, total):
     launch = P.Launch(teams, 32, 20, 0, -1, 0, 0, None, 0, first, total, 0)
     rc = P.lib().ompds_run_regions(C.byref(launch), 0, 1, C.c_void_p(16), None, None)
     assert rc == P.ERR_INVALID
+
+
+def test_overhead_probe_validates_before_touching_a_gpu():
+    import ctypes as C
+    p = P.OverheadProbe()
+    assert P.lib().ompds_probe_overheads(0, C.byref(p), None) == P.ERR_INVALID
+    assert P.lib().ompds_probe_overheads((1 << 20) + 1, C.byref(p), None) == P.ERR_INVALID
+    assert P.lib().ompds_probe_overheads(16, None, None) == P.ERR_INVALID
+    if P.lib().ompds_device_count() == 0:
+        assert P.lib().ompds_probe_overheads(16, C.byref(p), None) == P.ERR_CUDA
