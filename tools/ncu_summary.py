@@ -69,11 +69,12 @@ def summarise_rep(rep, algo_bytes):
         d = {"kernel": k.get("Kernel Name", ("?", ""))[0], "metrics": m,
              "stall_samples": stalls,
              "barrier_stall_fraction": round(stalls.get("barrier", 0) / total, 4) if total else None}
-        rd = num(k.get("dram__bytes_read.sum", ("0", ""))[0]) or 0
-        wr = num(k.get("dram__bytes_write.sum", ("0", ""))[0]) or 0
-        ur = k.get("dram__bytes_read.sum", ("", ""))[1]
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(ur, 1)
-        d["dram_bytes_per_launch"] = (rd + wr) * scale
+        units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+        def nbytes(key):
+            v, u = k.get(key, ("0", "byte"))
+            return (num(v) or 0) * units.get(u, 1)
+        d["dram_bytes_per_launch"] = nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum")
         if algo_bytes:
             d["algorithmic_bytes_per_launch"] = algo_bytes
             d["traffic_over_algorithmic"] = round(d["dram_bytes_per_launch"] / algo_bytes, 4)
