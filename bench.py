@@ -335,13 +335,17 @@ def main():
     # the reference's integer analog (4 int captures, int body) beside it
     ai = torch.zeros(32, dtype=torch.int32, device=dev)
     ns_int = device_ms(stream, lambda: RG.run_regions(ai, 1, 32, R, stream=stream)) * 1e6 / R
-    # the same protocol on every SM: 16 teams/SM x 32 workers, 2000 regions
-    # each (tools/agg_sweep.py: 8/SM 2.6, 16/SM 4.3 G regions/s; more teams
-    # than the register limit's 19/SM run in two waves)
+    # the same protocol on every SM: as many 64-thread teams per SM as the
+    # kernel's registers allow (one wave; 18/SM at 52 registers, the B200 row
+    # of the occupancy model = ncu's launch__occupancy_limit_registers),
+    # 2000 regions each (tools/regs_ab.py: 16/SM 4.32, 18/SM 4.51 G regions/s;
+    # 20/SM runs in two waves, 3.1)
     # With N ranks the team grid (N x 16 teams/SM) is sharded by range: rank r
     # launches teams [r*T, (r+1)*T) of the N*T grid (first_team/total_teams),
     # the whole-job rate is N*T*R2 over the slowest rank's time.
-    R2, teams2 = 2000, sms * 16
+    from paper_1711_10413_b200 import occupancy as OCC
+    per_sm1 = OCC.occupancy_for("b200", 265, ptxas_regs("RegionsProgIdE") or 52, 64).actual
+    R2, teams2 = 2000, sms * per_sm1
     a2 = torch.zeros(world * teams2 * 32, dtype=torch.float64, device=dev)
     rng = dict(first_team=rank * teams2, total_teams=world * teams2)
     RG.run_regions(a2, teams2, 32, 10, stream=stream, **rng)
@@ -360,7 +364,7 @@ def main():
     placement = {}
     for name, pe, alloc in (("window", 20, 0), ("global_slab", 2, 0), ("device_malloc", 2, 1)):
         row = {}
-        for label, tm, rr in (("1team", 1, 2000), ("full", sms * 16, 200)):
+        for label, tm, rr in (("1team", 1, 2000), ("full", teams2, 200)):
             ap = torch.zeros(tm * 32, dtype=torch.float64, device=dev)
             RG.run_regions(ap, tm, 32, 10, prealloc_entries=pe, list_allocator=alloc, stream=stream)
             ms_p = device_ms(stream, lambda: RG.run_regions(
@@ -382,7 +386,6 @@ def main():
                  "(the same store/load at a fixed smem address); handoff = release + "
                  "join named barriers between the master and one worker warp")
     configs = other_configs(RG, dev, stream, sms) if rank == 0 else {}
-    from paper_1711_10413_b200 import occupancy as OCC
     regs = ptxas_regs("StreamProgIdE") or 64
     thr = ((workers + 31) // 32) * 32 + 32
     occ = OCC.occupancy_for("b200", smem_bytes, regs, thr)
