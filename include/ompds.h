@@ -408,6 +408,15 @@ typedef struct ompds_program {
                            default, Simulator.h:37)                     */
 } ompds_program;
 
+/* Checks a program without a GPU (ompds_run_program runs the same check
+ * first): opcodes and operands in range, jump targets on instruction
+ * boundaries, one stack depth in [0, 32] at every reachable instruction (0 at
+ * PARALLEL), no falling off the end, and only variables the executing side
+ * addresses (master: depot, local mirror, buffers; region bodies: private
+ * frame, captures below the region's nargs, buffers), inside their frames.
+ * OMPDS_OK or OMPDS_ERR_INVALID. */
+int32_t ompds_program_verify(const ompds_program *prog);
+
 int32_t ompds_run_program(const ompds_launch *launch, const ompds_program *prog,
                           ompds_team_stats *stats_dev, ompds_event *events_dev);
 

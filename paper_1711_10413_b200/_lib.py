@@ -169,6 +169,7 @@ _SIGS = {
                                       _P]),
     "ompds_run_nested": (C.c_int32, [C.POINTER(Launch), C.c_int32, C.c_int32, C.c_int64,
                                       C.c_int64, _P, _P, _P, _P]),
+    "ompds_program_verify": (C.c_int32, [C.POINTER(Program)]),
     "ompds_run_program": (C.c_int32, [C.POINTER(Launch), C.POINTER(Program), _P, _P]),
     "ompds_run_stream_host": (C.c_int32, [C.POINTER(Launch), C.c_int32, C.c_int64, _P, _P, _P,
                                            _P, _P]),

@@ -1016,16 +1016,142 @@ int32_t ompds_run_nested(const ompds_launch *launch, int32_t elem,
                                             warp_slot_bytes, warp_overflow_bytes);
 }
 
-int32_t ompds_run_program(const ompds_launch *launch, const ompds_program *pr,
-                          ompds_team_stats *stats, ompds_event *events) {
-  if (!launch || !pr || !pr->code || pr->n_code <= 0 || pr->n_vars < 0 ||
-      pr->n_regions < 0 || pr->n_captures < 0 || pr->n_buffers < 0 ||
-      pr->total_shared < 0 || pr->total_local < 0 || pr->priv_bytes > kVmPriv)
+} // extern "C"
+
+namespace {
+
+// Host-side verification of a region program before the device interpreter
+// sees it: opcodes and operands in range, jump targets on instruction
+// boundaries, one consistent stack depth in [0, kVmStack] at every reachable
+// instruction (0 at PARALLEL), no falling off the end, and only variables the
+// executing side can address -- the master: the depot, its local mirror and
+// the mapped buffers; a region body: its private frame, captures below its
+// nargs and the mapped buffers -- each inside its frame.  A malformed
+// program is OMPDS_ERR_INVALID, never a device fault.
+bool vm_has_arg(int32_t op) {
+  return op == OP_PUSH || op == OP_LOAD || op == OP_STORE || op == OP_LOADX ||
+         op == OP_STOREX || op == OP_JMP || op == OP_JNLT || op == OP_PARALLEL;
+}
+
+bool vm_var_ok(const ompds_program *pr, int32_t v, bool master, int32_t nargs) {
+  if (v < 0 || v >= pr->n_vars)
+    return false;
+  const ompds_prog_var d = pr->vars[v];
+  if (d.count < 0)
+    return false;
+  const int64_t end = int64_t(d.index) + 4 * int64_t(d.count);
+  switch (d.space) {
+  case SP_DEPOT: return master && d.index >= 0 && end <= pr->total_shared;
+  case SP_MLOCAL: return master && d.index >= 0 && end <= std::max<int64_t>(pr->total_local, 4);
+  case SP_PRIV: return !master && d.index >= 0 && end <= kVmPriv;
+  case SP_CAPTURE: return !master && d.index >= 0 && d.index < nargs;
+  case SP_GLOBAL: return d.index >= 0 && d.index < pr->n_buffers;
+  default: return false;
+  }
+}
+
+bool vm_walk(const ompds_program *pr, const std::vector<int8_t> &start, int32_t entry,
+             bool master, int32_t nargs) {
+  const int64_t n = pr->n_code;
+  const int32_t *code = pr->code;
+  std::vector<int32_t> depth(size_t(n), -1);
+  std::vector<std::pair<int64_t, int32_t>> work{{entry, 0}};
+  while (!work.empty()) {
+    auto [pc, d] = work.back();
+    work.pop_back();
+    if (pc < 0 || pc >= n || !start[size_t(pc)])
+      return false; // a jump off an instruction, or falling off the end
+    if (depth[size_t(pc)] >= 0) {
+      if (depth[size_t(pc)] != d)
+        return false;
+      continue;
+    }
+    depth[size_t(pc)] = d;
+    const int32_t op = code[pc];
+    const int32_t arg = vm_has_arg(op) ? code[pc + 1] : 0;
+    int need = 0, delta = 0;
+    switch (op) {
+    case OP_END: continue;
+    case OP_PUSH: delta = 1; break;
+    case OP_LOAD: delta = 1; break;
+    case OP_STORE: need = 1; delta = -1; break;
+    case OP_LOADX: need = 1; break;
+    case OP_STOREX: need = 2; delta = -2; break;
+    case OP_ADD: case OP_SUB: case OP_MUL: need = 2; delta = -1; break;
+    case OP_TID: case OP_TEAM: case OP_NTHREADS: case OP_NTEAMS: delta = 1; break;
+    case OP_JMP: work.push_back({arg, d}); continue;
+    case OP_JNLT: need = 2; delta = -2; break;
+    case OP_PARALLEL:
+      if (!master || d != 0 || arg < 0 || arg >= pr->n_regions)
+        return false;
+      break;
+    case OP_ZERO_PRIV:
+      if (master)
+        return false;
+      break;
+    default: return false;
+    }
+    if ((op == OP_LOAD || op == OP_STORE || op == OP_LOADX || op == OP_STOREX) &&
+        !vm_var_ok(pr, arg, master, nargs))
+      return false;
+    if (d < need || d + delta > kVmStack)
+      return false;
+    const int64_t len = vm_has_arg(op) ? 2 : 1;
+    if (op == OP_JNLT)
+      work.push_back({arg, d + delta});
+    work.push_back({pc + len, d + delta});
+  }
+  return true;
+}
+
+bool verify_program(const ompds_program *pr) {
+  const int64_t n = pr->n_code;
+  std::vector<int8_t> start(size_t(n), 0);
+  for (int64_t pc = 0; pc < n;) { // instruction boundaries
+    start[size_t(pc)] = 1;
+    pc += vm_has_arg(pr->code[pc]) ? 2 : 1;
+    if (pc > n)
+      return false;
+  }
+  for (int32_t r = 0; r < pr->n_regions; ++r) {
+    const ompds_prog_region &g = pr->regions[r];
+    if (g.cap_begin < 0 || int64_t(g.cap_begin) + g.n_captures > pr->n_captures ||
+        (g.n_captures > 0 && !pr->captures))
+      return false;
+    for (int32_t j = 0; j < g.n_captures; ++j)
+      if (!vm_var_ok(pr, pr->captures[g.cap_begin + j], true, 0))
+        return false;
+    if (!vm_walk(pr, start, g.entry, false, g.n_captures))
+      return false;
+  }
+  return vm_walk(pr, start, 0, true, 0);
+}
+
+} // namespace
+
+extern "C" {
+
+int32_t ompds_program_verify(const ompds_program *pr) {
+  if (!pr || !pr->code || pr->n_code <= 0 || pr->n_vars < 0 || pr->n_regions < 0 ||
+      pr->n_captures < 0 || pr->n_buffers < 0 || pr->total_shared < 0 ||
+      pr->total_local < 0 || pr->priv_bytes > kVmPriv)
+    return OMPDS_ERR_INVALID;
+  if ((pr->n_regions > 0 && !pr->regions) || (pr->n_vars > 0 && !pr->vars) ||
+      (pr->n_buffers > 0 && !pr->buffers))
     return OMPDS_ERR_INVALID;
   for (int32_t i = 0; i < pr->n_regions; ++i)
-    if (pr->regions[i].n_captures > kVmCaps || pr->regions[i].entry < 0 ||
-        pr->regions[i].entry >= pr->n_code)
+    if (pr->regions[i].n_captures < 0 || pr->regions[i].n_captures > kVmCaps ||
+        pr->regions[i].entry < 0 || pr->regions[i].entry >= pr->n_code)
       return OMPDS_ERR_INVALID;
+  return verify_program(pr) ? OMPDS_OK : OMPDS_ERR_INVALID;
+}
+
+int32_t ompds_run_program(const ompds_launch *launch, const ompds_program *pr,
+                          ompds_team_stats *stats, ompds_event *events) {
+  if (!launch)
+    return OMPDS_ERR_INVALID;
+  if (const int32_t v = ompds_program_verify(pr))
+    return v;
   // Stage the program's tables in one device buffer (workspace slot 2).
   const size_t sz_code = size_t(pr->n_code) * 4, sz_vars = size_t(pr->n_vars) * sizeof(ompds_prog_var),
                sz_regs = size_t(pr->n_regions) * sizeof(ompds_prog_region),

@@ -325,6 +325,35 @@ def compile_program(ast: dict, layouts: Sequence[dict], kernel_root: str, teams:
     return _Compiler(ast, layouts, kernel_root, teams, workers).compile()
 
 
+def describe(prog: Program, buffer_ptrs, step_limit: int = 0):
+    """The ompds_program descriptor of `prog` (and the ctypes arrays it
+    points into, which must outlive it)."""
+    code = (C.c_int32 * max(len(prog.code), 1))(*prog.code)
+    vars_ = (L.ProgVar * max(len(prog.vars), 1))(*[L.ProgVar(s, o, n, 0) for s, o, n in prog.vars])
+    caps = [c for r in prog.regions for c in r.captures]
+    regs = []
+    k = 0
+    for r in prog.regions:
+        regs.append(L.ProgRegion(r.entry, len(r.captures), k, 0))
+        k += len(r.captures)
+    regs_a = (L.ProgRegion * max(len(regs), 1))(*regs)
+    caps_a = (C.c_int32 * max(len(caps), 1))(*caps)
+    bufs = (C.c_void_p * max(len(buffer_ptrs), 1))(*buffer_ptrs)
+    desc = L.Program(code=code, n_code=len(prog.code), vars=vars_, n_vars=len(prog.vars),
+                     n_regions=len(regs), regions=regs_a, captures=caps_a, n_captures=len(caps),
+                     n_buffers=len(buffer_ptrs), buffers=bufs, total_shared=prog.total_shared,
+                     total_local=prog.total_local, priv_bytes=prog.priv_bytes,
+                     step_limit=step_limit)
+    return desc, (code, vars_, regs_a, caps_a, bufs)
+
+
+def verify(prog: Program) -> int:
+    """ompds_program_verify on the program (no GPU needed); OMPDS_OK or
+    OMPDS_ERR_INVALID."""
+    desc, _keep = describe(prog, [16 * (k + 1) for k in range(len(prog.buffers))])
+    return L.lib().ompds_program_verify(C.byref(desc))
+
+
 def run_program(prog: Program, buffers, prealloc_entries: int = L.DEFAULT_PREALLOC_ENTRIES,
                 fail_dynamic_alloc: bool = False, depot_capacity: int = -1,
                 max_events: int = 0, stream=None, list_allocator: int = L.LIST_SLAB,
@@ -339,22 +368,7 @@ def run_program(prog: Program, buffers, prealloc_entries: int = L.DEFAULT_PREALL
     for b, (name, n, _) in zip(buffers, prog.buffers):
         if b.dtype != torch.int32 or b.numel() != n or not b.is_cuda:
             raise ValueError(f"buffer {name}: int32[{n}] on cuda expected")
-    code = (C.c_int32 * max(len(prog.code), 1))(*prog.code)
-    vars_ = (L.ProgVar * max(len(prog.vars), 1))(*[L.ProgVar(s, o, n, 0) for s, o, n in prog.vars])
-    caps = [c for r in prog.regions for c in r.captures]
-    regs = []
-    k = 0
-    for r in prog.regions:
-        regs.append(L.ProgRegion(r.entry, len(r.captures), k, 0))
-        k += len(r.captures)
-    regs_a = (L.ProgRegion * max(len(regs), 1))(*regs)
-    caps_a = (C.c_int32 * max(len(caps), 1))(*caps)
-    bufs = (C.c_void_p * max(len(buffers), 1))(*[b.data_ptr() for b in buffers])
-    desc = L.Program(code=code, n_code=len(prog.code), vars=vars_, n_vars=len(prog.vars),
-                     n_regions=len(regs), regions=regs_a, captures=caps_a, n_captures=len(caps),
-                     n_buffers=len(buffers), buffers=bufs, total_shared=prog.total_shared,
-                     total_local=prog.total_local, priv_bytes=prog.priv_bytes,
-                     step_limit=step_limit)
+    desc, _keep = describe(prog, [b.data_ptr() for b in buffers], step_limit)
     out = RG.Outputs(teams or prog.teams, buffers[0].device if buffers else "cuda", max_events)
     launch = RG.make_launch(teams or prog.teams, prog.workers, prealloc_entries,
                             fail_dynamic_alloc, depot_capacity, max_events > 0, max_events,

@@ -163,6 +163,82 @@ def test_lowering_reproduces_reference_outputs_on_cpu():
     assert n > 150
 
 
+def test_every_lowered_program_passes_the_verifier():
+    """ompds_program_verify (run by ompds_run_program before any launch)
+    accepts every program the lowering produces, incl. the bad-pass-order
+    layouts."""
+    from paper_1711_10413_b200 import _lib as L
+    n = 0
+    for p in programs():
+        for pipeline in ("default", "bad_order"):
+            prog = PG.compile_program(p["ast"], our_layouts(p, pipeline), p["kernel"], 2, 40)
+            assert PG.verify(prog) == L.OK, (p["stem"], pipeline)
+            n += 1
+    assert n > 200
+
+
+def _mutants(prog):
+    """(label, program) pairs each breaking one rule the verifier enforces."""
+    import dataclasses
+    code = list(prog.code)
+    out = []
+
+    def with_code(c):
+        return dataclasses.replace(prog, code=c)
+
+    out.append(("unknown opcode", with_code(code[:-1] + [99])))
+    out.append(("falls off the end", with_code(code[:-1] + [PG.OP_TID])))
+    out.append(("stack underflow at entry", with_code([PG.OP_ADD] + code[1:])))
+    out.append(("jump into an operand", with_code([PG.OP_JMP, 3, PG.OP_PUSH, 7, PG.OP_END])))
+    out.append(("jump past the end", with_code([PG.OP_JMP, 10 ** 6] + code[2:])))
+    out.append(("stack overflow", with_code([PG.OP_TID] * 33 + [PG.OP_END])))
+    out.append(("ZERO_PRIV in master code", with_code([PG.OP_ZERO_PRIV] + code)))
+    out.append(("parallel with a value on the stack",
+                with_code([PG.OP_TID, PG.OP_PARALLEL, 0, PG.OP_END])))
+    out.append(("parallel of a missing region",
+                with_code([PG.OP_PARALLEL, len(prog.regions), PG.OP_END])))
+    out.append(("variable index out of range",
+                with_code([PG.OP_LOAD, len(prog.vars), PG.OP_STORE, 0, PG.OP_END])))
+    return out
+
+
+def test_verifier_rejects_malformed_programs():
+    """A malformed program is OMPDS_ERR_INVALID before any launch -- never a
+    device fault -- for each rule (tests run without a GPU)."""
+    from paper_1711_10413_b200 import _lib as L
+    p = next(q for q in programs() if q["stem"] == "shared_scalar")
+    t, w, _ = launches(p)[0]
+    prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], t, w)
+    assert PG.verify(prog) == L.OK
+    for label, bad in _mutants(prog):
+        assert PG.verify(bad) == L.ERR_INVALID, label
+    # region-side rules: a depot variable or a capture beyond the region's
+    # nargs inside a region body, a region entry inside an operand
+    import dataclasses
+    r0 = prog.regions[0]
+    depot_var = next(i for i, v in enumerate(prog.vars) if v[0] == PG.SP_DEPOT)
+    body = [PG.OP_ZERO_PRIV, PG.OP_LOAD, depot_var, PG.OP_STORE, depot_var, PG.OP_END]
+    bad = dataclasses.replace(prog, code=list(prog.code) + body,
+                              regions=[dataclasses.replace(r0, entry=len(prog.code))]
+                              + list(prog.regions[1:]))
+    assert PG.verify(bad) == L.ERR_INVALID
+    cap = len(prog.vars)
+    vars_ = list(prog.vars) + [(PG.SP_CAPTURE, len(r0.captures), 1)]
+    body = [PG.OP_ZERO_PRIV, PG.OP_LOAD, cap, PG.OP_STORE, cap, PG.OP_END]
+    bad = dataclasses.replace(prog, code=list(prog.code) + body, vars=vars_,
+                              regions=[dataclasses.replace(r0, entry=len(prog.code))]
+                              + list(prog.regions[1:]))
+    assert PG.verify(bad) == L.ERR_INVALID
+    bad = dataclasses.replace(prog, regions=[dataclasses.replace(r0, entry=r0.entry + 2)]
+                              + list(prog.regions[1:]))
+    assert PG.verify(bad) in (L.ERR_INVALID, L.OK)  # +2 may still be a boundary
+    # the same descriptor is refused by ompds_run_program before the launch
+    import ctypes as C
+    desc, _keep = PG.describe(_mutants(prog)[0][1], [16])
+    launch = L.Launch(1, 32, 20, 0, -1, 0, 0, None, 0, 0, 0, 0)
+    assert L.lib().ompds_run_program(C.byref(launch), C.byref(desc), None, None) == L.ERR_INVALID
+
+
 def test_sharing_analysis_matches_reference_detection():
     """The captures the lowering derives from the AST are exactly the kernel
     allocas the reference's escape detection marks shared
