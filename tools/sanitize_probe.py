@@ -55,6 +55,16 @@ def main():
     bufs = [torch.full((sz,), init, dtype=torch.int32, device=dev)
             for _, sz, init in prog.buffers]
     PG.run_program(prog, bufs, step_limit=50)
+    # two streams with spilled lists at once; the overhead probe
+    sts = [torch.cuda.Stream(), torch.cuda.Stream()]
+    arrs = [torch.zeros(8 * 40, dtype=torch.int32, device=dev) for _ in sts]
+    torch.cuda.synchronize()
+    for st, a in zip(sts, arrs):
+        RG.run_regions(a, 8, 40, 4, prealloc_entries=2, stream=st)
+    torch.cuda.synchronize()
+    for st in sts:
+        RG.release_workspace(st)
+    RG.probe_overheads(64)
     torch.cuda.synchronize()
     print("sanitize probe done")
 
