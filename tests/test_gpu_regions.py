@@ -388,3 +388,37 @@ def test_release_workspace_then_relaunch_on_the_same_stream():
         assert all((s.trap, s.dynamic_allocs, s.dynamic_frees) == (0, regions, regions)
                    for s in out.team_stats())
     RG.release_workspace(torch.cuda.Stream())
+
+
+@pytest.mark.gpu
+def test_region_launches_replay_from_a_cuda_graph():
+    """After one eager launch on a stream (which sizes the stream's
+    workspace), the config-4 region and a config-1 grid with spilled args
+    lists can be captured into a CUDA graph and replayed: every replay is one
+    more region pass, bit-exact against the oracle."""
+    n, teams, workers, replays = (1 << 18) + 3, 148, 96, 3
+    x, y = _f64_inputs(n)
+    s = torch.cuda.Stream()
+    a = torch.zeros(8 * 40, dtype=torch.int32, device=DEV)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        RG.run_stream(x, y, COEF, teams, workers, stats=False, stream=s)  # eager warm-up
+        RG.run_regions(a, 8, 40, 3, prealloc_entries=2, stream=s)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        RG.run_stream(x, y, COEF, teams, workers, stats=False, stream=s)
+        RG.run_regions(a, 8, 40, 3, prealloc_entries=2, stream=s)
+    for _ in range(replays):
+        g.replay()
+    torch.cuda.synchronize()
+    xs = np.empty(n)
+    ys = np.empty(n)
+    O.lib().orc_fill(1, O.ptr(xs), n, 0x5eed01ab, 0)
+    O.lib().orc_fill(1, O.ptr(ys), n, 0x5eed01ac, 0)
+    for _ in range(1 + replays):
+        O.lib().orc_stream(1, n, O.ptr(xs), O.ptr(ys), O.ptr(np.array(COEF)), 0)
+    assert np.array_equal(y.cpu().numpy().view(np.uint64), ys.view(np.uint64))
+    want = np.zeros(8 * 40, dtype=np.int32)
+    O.lib().orc_regions(0, 8, 40, 3, O.ptr(want))
+    assert np.array_equal(a.cpu().numpy(), want * (1 + replays))
