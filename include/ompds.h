@@ -330,7 +330,9 @@ int32_t ompds_run_regions(const ompds_launch *launch, int32_t elem,
  * cp.async.bulk from `d_init` (device, 256 elems) when non-NULL, else by
  * the master's own loop -- then `parallel for i<n: a[i] += d[i & 255]`
  * on the cyclic schedule (AstLowering.cpp:429-462).
- * elem: 0 = int32, 1 = float64. */
+ * elem: 0 = int32, 1 = float64.  Pointers must be aligned to the element;
+ * a 16-byte aligned `a` gets the vectorised body, any other the
+ * element-wise one (same results). */
 int32_t ompds_run_shared_array(const ompds_launch *launch, int32_t elem,
                                int64_t n, void *a, const void *d_init,
                                ompds_team_stats *stats_dev,
@@ -340,7 +342,9 @@ int32_t ompds_run_shared_array(const ompds_launch *launch, int32_t elem,
  * c_k (k=1..8) on the cyclic schedule over elements [0, n):
  *   float64: y[i] = fma(c1, x[i], y[i]) + s,  s = ((((((c2+c3)+c4)+c5)+c6)+c7)+c8)
  *   int32  : y[i] = y[i] + (c1*x[i] + c2 + ... + c8)   (wrapping int32)
- * `coef` (host, 8 values of elem type) are the master's initial values. */
+ * `coef` (host, 8 values of elem type) are the master's initial values.
+ * x, y aligned to the element; both 16-byte aligned gets the vectorised
+ * body, otherwise the element-wise one (same results). */
 int32_t ompds_run_stream(const ompds_launch *launch, int32_t elem, int64_t n,
                          const void *x, void *y, const void *coef_host,
                          ompds_team_stats *stats_dev, ompds_event *events_dev);

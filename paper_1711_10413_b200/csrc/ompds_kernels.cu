@@ -225,6 +225,33 @@ template <class T> struct SharedArrayProg {
   }
 };
 
+// a[] not 16-byte aligned: element-wise cyclic loop, 4 elements in flight.
+template <class T> struct SharedArrayProgUnaligned : SharedArrayProg<T> {
+  using Args = typename SharedArrayProg<T>::Args;
+  static constexpr int kLen = SharedArrayProg<T>::kLen;
+  __device__ static void region(int32_t, const SharedVars &sv, const Worker &w,
+                                const Args &a) {
+    const T *d = static_cast<const T *>(sv.get(0));
+    if (!w.mine)
+      return;
+    const int64_t gid = int64_t(w.local_team) * w.workers + w.wid;
+    const int64_t pool = int64_t(w.local_teams) * w.workers;
+    constexpr int U = 4;
+    int64_t i = gid;
+    for (; i + (U - 1) * pool < a.n; i += U * pool) {
+      T v[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        v[k] = a.a[i + k * pool];
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        a.a[i + k * pool] = v[k] + d[(i + k * pool) & (kLen - 1)];
+    }
+    for (; i < a.n; i += pool)
+      a.a[i] = a.a[i] + d[i & (kLen - 1)];
+  }
+};
+
 //===----------------------------------------------------------------------===//
 // Config 4/5: streaming region, 8 implicitly shared scalars.
 //===----------------------------------------------------------------------===//
@@ -255,10 +282,10 @@ template <class T> struct StreamProg {
     __syncwarp();
     m.parallel(0, 8);
   }
-  __device__ static void region(int32_t, const SharedVars &sv, const Worker &w,
-                                const Args &a) {
-    // get-shared-variables: lane j dereferences capture j, shuffles spread
-    // the values; every lane folds c2..c8 in the same order.
+  // get-shared-variables: lane j dereferences capture j, shuffles spread
+  // the values; every lane folds c2..c8 in the same order.
+  __device__ static __forceinline__ void captures(const SharedVars &sv, T *c1_out,
+                                                  T *s_out) {
     T v{};
     if (lane_id() < 8 && sv.mine)
       v = *static_cast<const T *>(sv.mine);
@@ -272,6 +299,13 @@ template <class T> struct StreamProg {
       else
         s = static_cast<T>(static_cast<uint32_t>(s) + static_cast<uint32_t>(ck));
     }
+    *c1_out = c1;
+    *s_out = s;
+  }
+  __device__ static void region(int32_t, const SharedVars &sv, const Worker &w,
+                                const Args &a) {
+    T c1, s;
+    captures(sv, &c1, &s);
     if (!w.mine)
       return;
     constexpr int V = 16 / sizeof(T);
@@ -321,6 +355,37 @@ template <class T> struct StreamProg {
       st_stream(yv + u, ys);
     }
     for (int64_t i = units * V + gid; i < a.n; i += pool)
+      a.y[i] = stream_op(c1, a.x[i], a.y[i], s);
+  }
+};
+
+// x or y not 16-byte aligned (a view starting mid-vector): the same region
+// with the element-wise cyclic loop of AstLowering.cpp:429-462, 4 elements
+// of x and y in flight per thread.
+template <class T> struct StreamProgUnaligned : StreamProg<T> {
+  using Args = typename StreamProg<T>::Args;
+  __device__ static void region(int32_t, const SharedVars &sv, const Worker &w,
+                                const Args &a) {
+    T c1, s;
+    StreamProg<T>::captures(sv, &c1, &s);
+    if (!w.mine)
+      return;
+    const int64_t gid = int64_t(w.local_team) * w.workers + w.wid;
+    const int64_t pool = int64_t(w.local_teams) * w.workers;
+    constexpr int U = 4;
+    int64_t i = gid;
+    for (; i + (U - 1) * pool < a.n; i += U * pool) {
+      T xs[U], ys[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        xs[k] = a.x[i + k * pool];
+        ys[k] = a.y[i + k * pool];
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        a.y[i + k * pool] = stream_op(c1, xs[k], ys[k], s);
+    }
+    for (; i < a.n; i += pool)
       a.y[i] = stream_op(c1, a.x[i], a.y[i], s);
   }
 };
@@ -917,32 +982,41 @@ int32_t ompds_run_regions(const ompds_launch *launch, int32_t elem,
 int32_t ompds_run_shared_array(const ompds_launch *launch, int32_t elem,
                                int64_t n, void *a, const void *d_init,
                                ompds_team_stats *stats, ompds_event *events) {
+  const int64_t esz = elem ? 8 : 4;
   if (!a || n < 0 || (elem != 0 && elem != 1) ||
-      (reinterpret_cast<uintptr_t>(a) & 15))
+      (reinterpret_cast<uintptr_t>(a) & (esz - 1)) ||
+      (reinterpret_cast<uintptr_t>(d_init) & (esz - 1)))
     return OMPDS_ERR_INVALID;
   FixedLayout lay;
-  const int64_t esz = elem ? 8 : 4;
   int32_t s = build_fixed_layout({256 * esz}, 4, &lay);
   if (s)
     return s;
-  if (elem == 0)
-    return launch_generic<SharedArrayProg<int32_t>>(
-        launch, lay, 1,
-        {static_cast<int32_t *>(a), n, static_cast<const int32_t *>(d_init)},
-        stats, events);
-  return launch_generic<SharedArrayProg<double>>(
-      launch, lay, 1,
-      {static_cast<double *>(a), n, static_cast<const double *>(d_init)}, stats,
-      events);
+  // 16-byte vectors when a[] allows them, else the element-wise loop
+  const bool vec = (reinterpret_cast<uintptr_t>(a) & 15) == 0;
+  if (elem == 0) {
+    SharedArrayProg<int32_t>::Args args{static_cast<int32_t *>(a), n,
+                                        static_cast<const int32_t *>(d_init)};
+    return vec ? launch_generic<SharedArrayProg<int32_t>>(launch, lay, 1, args, stats, events)
+               : launch_generic<SharedArrayProgUnaligned<int32_t>>(launch, lay, 1, args, stats,
+                                                                   events);
+  }
+  SharedArrayProg<double>::Args args{static_cast<double *>(a), n,
+                                     static_cast<const double *>(d_init)};
+  return vec ? launch_generic<SharedArrayProg<double>>(launch, lay, 1, args, stats, events)
+             : launch_generic<SharedArrayProgUnaligned<double>>(launch, lay, 1, args, stats,
+                                                                events);
 }
 
 int32_t ompds_run_stream(const ompds_launch *launch, int32_t elem, int64_t n,
                          const void *x, void *y, const void *coef_host,
                          ompds_team_stats *stats, ompds_event *events) {
+  const uintptr_t esz = elem ? 8 : 4;
   if (!x || !y || !coef_host || n < 0 || (elem != 0 && elem != 1) ||
-      (reinterpret_cast<uintptr_t>(x) & 15) ||
-      (reinterpret_cast<uintptr_t>(y) & 15))
+      (reinterpret_cast<uintptr_t>(x) & (esz - 1)) ||
+      (reinterpret_cast<uintptr_t>(y) & (esz - 1)))
     return OMPDS_ERR_INVALID;
+  // 16-byte vectors when both arrays allow them, else the element-wise loop
+  const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
   static FixedLayout lay8;
   static std::once_flag once;
   static int32_t lay_status = 0;
@@ -955,13 +1029,15 @@ int32_t ompds_run_stream(const ompds_launch *launch, int32_t elem, int64_t n,
     StreamProg<int32_t>::Args a{static_cast<const int32_t *>(x),
                                 static_cast<int32_t *>(y), n, {}};
     std::memcpy(a.coef, coef_host, sizeof(a.coef));
-    return launch_generic<StreamProg<int32_t>>(launch, lay8, 8, a, stats,
-                                               events);
+    return vec ? launch_generic<StreamProg<int32_t>>(launch, lay8, 8, a, stats, events)
+               : launch_generic<StreamProgUnaligned<int32_t>>(launch, lay8, 8, a, stats,
+                                                              events);
   }
   StreamProg<double>::Args a{static_cast<const double *>(x),
                              static_cast<double *>(y), n, {}};
   std::memcpy(a.coef, coef_host, sizeof(a.coef));
-  return launch_generic<StreamProg<double>>(launch, lay8, 8, a, stats, events);
+  return vec ? launch_generic<StreamProg<double>>(launch, lay8, 8, a, stats, events)
+             : launch_generic<StreamProgUnaligned<double>>(launch, lay8, 8, a, stats, events);
 }
 
 int32_t ompds_run_nested(const ompds_launch *launch, int32_t elem,

@@ -220,6 +220,8 @@ def run_stream(x: torch.Tensor, y: torch.Tensor, coef, teams: int, workers: int,
                stats: bool = True, **kw) -> Optional[Outputs]:
     """Config 4: ``y = fma(c1, x, y) + (c2+...+c8)`` over all elements."""
     _require_cuda(x, y)
+    if x.dtype != y.dtype or x.numel() != y.numel():
+        raise ValueError("x and y: same dtype and length")
     max_events = kw.pop("max_events", 0)
     out = Outputs(teams, x.device, max_events) if stats else None
     launch = make_launch(teams, workers, log_events=max_events > 0, max_events=max_events, **kw)

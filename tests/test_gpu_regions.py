@@ -422,3 +422,54 @@ def test_region_launches_replay_from_a_cuda_graph():
     want = np.zeros(8 * 40, dtype=np.int32)
     O.lib().orc_regions(0, 8, 40, 3, O.ptr(want))
     assert np.array_equal(a.cpu().numpy(), want * (1 + replays))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,ox,oy", [(torch.float64, 1, 1), (torch.float64, 1, 0),
+                                         (torch.float64, 0, 1), (torch.int32, 1, 1),
+                                         (torch.int32, 2, 3), (torch.int32, 3, 0)])
+def test_config4_views_not_16_byte_aligned(dtype, ox, oy):
+    """Views starting mid-vector (x[1:], ...) take the element-wise variant
+    of the region; results equal the oracle and the neighbours of the view
+    are untouched."""
+    n = 100_003
+    elem = 1 if dtype == torch.float64 else 0
+    bx = torch.empty(n + 4, dtype=dtype, device=DEV)
+    by = torch.empty(n + 4, dtype=dtype, device=DEV)
+    RG.fill_uniform(bx, 0x5eed01ab)
+    RG.fill_uniform(by, 0x5eed01ac)
+    before = by.cpu().numpy().copy()
+    x, y = bx[ox:ox + n], by[oy:oy + n]
+    coef = COEF if elem else [k + 1 for k in range(8)]
+    out = RG.run_stream(x, y, coef, 148, 96)
+    torch.cuda.synchronize()
+    xs = bx.cpu().numpy()[ox:ox + n].copy()
+    ys = before[oy:oy + n].copy()
+    cf = np.array(coef, dtype=np.float64 if elem else np.int32)
+    O.lib().orc_stream(elem, n, O.ptr(xs), O.ptr(ys), O.ptr(cf), 0)
+    got = by.cpu().numpy()
+    view = np.uint64 if elem else np.uint32
+    assert np.array_equal(got[oy:oy + n].view(view), ys.view(view))
+    assert np.array_equal(got[:oy], before[:oy]) and np.array_equal(got[oy + n:], before[oy + n:])
+    assert all(s.trap == 0 and s.regions == 1 for s in out.team_stats())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,off", [(torch.float64, 1), (torch.int32, 1), (torch.int32, 2)])
+def test_config2_view_not_16_byte_aligned(dtype, off):
+    n = 70_001
+    base = torch.empty(n + 4, dtype=dtype, device=DEV)
+    RG.fill_uniform(base, 0x5eed01ac)
+    before = base.cpu().numpy().copy()
+    d_init = torch.arange(256, dtype=dtype, device=DEV) * 3 + 1
+    RG.run_shared_array(base[off:off + n], 37, 64, d_init=d_init)
+    torch.cuda.synchronize()
+    d = d_init.cpu().numpy()
+    want = before.copy()
+    if dtype == torch.float64:
+        want[off:off + n] = before[off:off + n] + d[np.arange(n) & 255]
+    else:
+        want[off:off + n] = (before[off:off + n].astype(np.int64)
+                             + d[np.arange(n) & 255]).astype(np.int32)
+    got = base.cpu().numpy()
+    assert np.array_equal(got, want)

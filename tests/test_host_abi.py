@@ -233,3 +233,17 @@ def test_overhead_probe_validates_before_touching_a_gpu():
     assert P.lib().ompds_probe_overheads(16, None, None) == P.ERR_INVALID
     if P.lib().ompds_device_count() == 0:
         assert P.lib().ompds_probe_overheads(16, C.byref(p), None) == P.ERR_CUDA
+
+
+def test_element_misaligned_pointers_are_rejected_before_a_gpu():
+    """16-byte-unaligned views are served (element-wise variant); pointers
+    not aligned to the element itself are invalid."""
+    import ctypes as C
+    launch = P.Launch(2, 32, 20, 0, -1, 0, 0, None, 0, 0, 0, 0)
+    coef = (C.c_double * 8)()
+    rc = P.lib().ompds_run_stream(C.byref(launch), 1, 10, C.c_void_p(4100), C.c_void_p(8192),
+                                  coef, None, None)
+    assert rc == P.ERR_INVALID
+    rc = P.lib().ompds_run_shared_array(C.byref(launch), 0, 10, C.c_void_p(4098), None, None,
+                                        None)
+    assert rc == P.ERR_INVALID
