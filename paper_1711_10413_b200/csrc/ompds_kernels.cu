@@ -225,7 +225,7 @@ template <class T> struct SharedArrayProg {
   }
 };
 
-// a[] not 16-byte aligned: element-wise cyclic loop, 4 elements in flight.
+// a[] not 16-byte aligned: element-wise cyclic loop, 8 elements in flight.
 template <class T> struct SharedArrayProgUnaligned : SharedArrayProg<T> {
   using Args = typename SharedArrayProg<T>::Args;
   static constexpr int kLen = SharedArrayProg<T>::kLen;
@@ -236,7 +236,7 @@ template <class T> struct SharedArrayProgUnaligned : SharedArrayProg<T> {
       return;
     const int64_t gid = int64_t(w.local_team) * w.workers + w.wid;
     const int64_t pool = int64_t(w.local_teams) * w.workers;
-    constexpr int U = 4;
+    constexpr int U = 8;
     int64_t i = gid;
     for (; i + (U - 1) * pool < a.n; i += U * pool) {
       T v[U];
@@ -360,7 +360,7 @@ template <class T> struct StreamProg {
 };
 
 // x or y not 16-byte aligned (a view starting mid-vector): the same region
-// with the element-wise cyclic loop of AstLowering.cpp:429-462, 4 elements
+// with the element-wise cyclic loop of AstLowering.cpp:429-462, 8 elements
 // of x and y in flight per thread.
 template <class T> struct StreamProgUnaligned : StreamProg<T> {
   using Args = typename StreamProg<T>::Args;
@@ -372,7 +372,7 @@ template <class T> struct StreamProgUnaligned : StreamProg<T> {
       return;
     const int64_t gid = int64_t(w.local_team) * w.workers + w.wid;
     const int64_t pool = int64_t(w.local_teams) * w.workers;
-    constexpr int U = 4;
+    constexpr int U = 8;
     int64_t i = gid;
     for (; i + (U - 1) * pool < a.n; i += U * pool) {
       T xs[U], ys[U];
