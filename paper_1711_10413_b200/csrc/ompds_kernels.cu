@@ -962,7 +962,8 @@ int32_t ompds_rt_replay(const ompds_runtime_config *config,
 int32_t ompds_run_regions(const ompds_launch *launch, int32_t elem,
                           int32_t regions, void *a, ompds_team_stats *stats,
                           ompds_event *events) {
-  if (!a || regions < 0 || (elem != 0 && elem != 1))
+  if (!a || regions < 0 || (elem != 0 && elem != 1) ||
+      (reinterpret_cast<uintptr_t>(a) & (elem ? 7 : 3)))
     return OMPDS_ERR_INVALID;
   FixedLayout lay;
   // c1, c2 (int), c3, c4 (elem) and -- when the region sits in a sequential
@@ -1047,6 +1048,7 @@ int32_t ompds_run_nested(const ompds_launch *launch, int32_t elem,
                          ompds_warp_stack_stats *warp_stats,
                          ompds_event *events) {
   if (!a || regions < 0 || (elem != 0 && elem != 1) || warp_slot_bytes < 0 ||
+      (reinterpret_cast<uintptr_t>(a) & (elem ? 7 : 3)) ||
       warp_overflow_bytes < 0)
     return OMPDS_ERR_INVALID;
   const int64_t esz = elem ? 8 : 4;

@@ -247,3 +247,5 @@ def test_element_misaligned_pointers_are_rejected_before_a_gpu():
     rc = P.lib().ompds_run_shared_array(C.byref(launch), 0, 10, C.c_void_p(4098), None, None,
                                         None)
     assert rc == P.ERR_INVALID
+    assert P.lib().ompds_run_regions(C.byref(launch), 1, 2, C.c_void_p(4100), None,
+                                     None) == P.ERR_INVALID
