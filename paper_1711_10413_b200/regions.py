@@ -121,9 +121,18 @@ class Outputs:
         return out
 
 
+def _require_team_array(a: torch.Tensor, teams: int, workers: int, kw) -> None:
+    """a[] is indexed by the grid's team number: one element per worker of
+    every team of the grid (total_teams when the launch is a team range)."""
+    grid = max(kw.get("total_teams") or 0, kw.get("first_team", 0) + teams, teams)
+    if a.numel() < grid * workers:
+        raise ValueError(f"a needs {grid} x {workers} elements, has {a.numel()}")
+
+
 def run_regions(a: torch.Tensor, teams: int, workers: int, regions: int, **kw) -> Outputs:
     """Config 1: ``regions`` parallel regions sharing 4 scalars per team."""
     _require_cuda(a)
+    _require_team_array(a, teams, workers, kw)
     max_events = kw.pop("max_events", 0)
     out = Outputs(teams, a.device, max_events)
     launch = make_launch(teams, workers, log_events=max_events > 0, max_events=max_events, **kw)
@@ -138,6 +147,10 @@ def run_shared_array(a: torch.Tensor, teams: int, workers: int,
                      d_init: Optional[torch.Tensor] = None, **kw) -> Outputs:
     """Config 2: d[256] in the depot, ``parallel for i: a[i] += d[i & 255]``."""
     _require_cuda(a)
+    if d_init is not None:
+        _require_cuda(d_init)
+        if d_init.dtype != a.dtype or d_init.numel() != 256:
+            raise ValueError("d_init: 256 elements of a's dtype")
     max_events = kw.pop("max_events", 0)
     out = Outputs(teams, a.device, max_events)
     launch = make_launch(teams, workers, log_events=max_events > 0, max_events=max_events, **kw)
@@ -167,6 +180,7 @@ def run_nested(a: torch.Tensor, teams: int, workers: int, regions: int,
     collect=False the launch is only enqueued (no wait, stacks None) -- for
     timing the kernel alone."""
     _require_cuda(a)
+    _require_team_array(a, teams, workers, kw)
     max_events = kw.pop("max_events", 0)
     out = Outputs(teams, a.device, max_events)
     warps = (workers + 31) // 32
