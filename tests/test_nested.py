@@ -105,3 +105,23 @@ def test_gpu_nested_stack_statistics_on_a_side_stream():
     for ws in stacks[0]:
         assert ws.status == 0 and ws.max_depth == md == 2
         assert ws.frame_in_smem == [bool(x) for x in ins] and ws.frame_offset == off
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("elem", [0, 1])
+def test_gpu_nested_whole_gpu_grid_matches_oracle(elem):
+    """The bench's config-3 grid (8 teams per SM x 96 workers) for 20 nested
+    regions: every element equals the oracle, every warp's stack matches."""
+    import torch
+    from paper_1711_10413_b200 import regions as RG
+    teams = torch.cuda.get_device_properties(0).multi_processor_count * 8
+    workers, regions = 96, 20
+    dt = torch.float64 if elem else torch.int32
+    a = torch.zeros(teams * workers, dtype=dt, device="cuda")
+    out, stacks = RG.run_nested(a, teams, workers, regions)
+    want = np.zeros(teams * workers, dtype=np.float64 if elem else np.int32)
+    O.lib().orc_nested(elem, teams, workers, regions, O.ptr(want))
+    assert np.array_equal(a.cpu().numpy(), want)
+    assert all(ws.status == 0 and ws.frame_in_smem == [True, True]
+               for t in stacks for ws in t)
+    assert all(s.trap == 0 and s.regions == regions for s in out.team_stats())
