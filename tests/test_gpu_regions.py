@@ -474,3 +474,20 @@ def test_config2_view_not_16_byte_aligned(dtype, off):
                              + d[np.arange(n) & 255]).astype(np.int32)
     got = base.cpu().numpy()
     assert np.array_equal(got, want)
+
+
+@pytest.mark.gpu
+def test_config2_bench_grid_full_size_matches_oracle():
+    """Config 2 as the bench runs it: 296 teams x 480 workers, 2^24 doubles,
+    d[] staged by TMA."""
+    n = 1 << 24
+    a = torch.empty(n, dtype=torch.float64, device=DEV)
+    RG.fill_uniform(a, 0x5eed01ac)
+    d_init = torch.arange(256, dtype=torch.float64, device=DEV) * 3 + 1
+    out = RG.run_shared_array(a, 296, 480, d_init=d_init)
+    want = np.empty(n)
+    O.lib().orc_fill(1, O.ptr(want), n, 0x5eed01ac, 0)
+    O.lib().orc_shared_array(1, n, O.ptr(want))
+    assert np.array_equal(a.cpu().numpy(), want)
+    assert all(s.trap == 0 and s.depot_in_smem and s.smem_bytes == 2281
+               for s in out.team_stats())
