@@ -36,6 +36,12 @@
 
 namespace ompds {
 
+// The general (trap / event-log / global-list) paths of prepare and fetch
+// are inlined: as calls they cost 3 % of config-4 bandwidth (the whole
+// kernel's register allocation changes).  Overridable for experiments.
+#ifndef OMPDS_GENERAL_INLINE
+#define OMPDS_GENERAL_INLINE __forceinline__
+#endif
 constexpr int kWarp = 32;
 constexpr uint32_t kBarHandoff = 1; // master <-> worker region handoff
 constexpr uint32_t kBarRegion = 2;  // `omp barrier` among a region's workers
@@ -566,7 +572,7 @@ __device__ __forceinline__ void fetch_account_fast(const TeamCtx &t,
 }
 // Every other case of the reference's kernel_parallel for a warp:
 // termination, a fetch with nothing staged (trap), and the event log.
-__device__ __forceinline__ Fetch fetch_general(const TeamCtx &t, const StagedState &st,
+__device__ OMPDS_GENERAL_INLINE Fetch fetch_general(const TeamCtx &t, const StagedState &st,
                                             const WarpMask &m, bool mine) {
   Fetch f = fetch_from(st);
   const uint8_t ph = st.phase;

@@ -244,7 +244,7 @@ struct Master {
   }
 
   template <class AddrOf>
-  __device__ __forceinline__ int32_t parallel_general(int32_t fn, int32_t nargs,
+  __device__ OMPDS_GENERAL_INLINE int32_t parallel_general(int32_t fn, int32_t nargs,
                                                    AddrOf addr_of) {
     void **list = nullptr;
     unsigned long long packed = 0;
