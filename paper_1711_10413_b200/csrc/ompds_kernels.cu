@@ -1105,7 +1105,9 @@ namespace {
 // executing side can address -- the master: the depot, its local mirror and
 // the mapped buffers; a region body: its private frame, captures below its
 // nargs and the mapped buffers -- each inside its frame.  A malformed
-// program is OMPDS_ERR_INVALID, never a device fault.
+// program is OMPDS_ERR_INVALID, never a device fault (the counterpart of the
+// reference validating a module before it simulates it, Verifier.cpp:323).
+// Lowered programs always pass (tests/test_program.py).
 bool vm_has_arg(int32_t op) {
   return op == OP_PUSH || op == OP_LOAD || op == OP_STORE || op == OP_LOADX ||
          op == OP_STOREX || op == OP_JMP || op == OP_JNLT || op == OP_PARALLEL;
