@@ -290,12 +290,6 @@ __device__ __forceinline__ StagedState load_staged_state(const TeamCtx &t,
                      reinterpret_cast<void **>(args), reinterpret_cast<void *>(win)};
 }
 
-__device__ __forceinline__ void rt_zero(const TeamCtx &t) {
-  for (int i = 0; i < Rt::kBytes; ++i)
-    t.rt[i] = 0;
-  t.work_fn() = -1;
-}
-
 //===----------------------------------------------------------------------===//
 // Team runtime protocol -- single-caller semantics, identical to
 // omplab::TeamRuntime (DeviceRuntime.cpp:33-143), trap order included.
@@ -900,7 +894,13 @@ struct DsStack {
 };
 
 //===----------------------------------------------------------------------===//
-// Reference / LLVM-runtime entry-point names.
+// Reference / LLVM-runtime entry-point names.  Like omplab::TeamRuntime
+// (DeviceRuntime.h:81-119: "one instance per team, not thread-safe") these
+// are single-caller: one thread of the team at a time, e.g. a code
+// generator's master thread, or the protocol replay kernel.  Concurrent
+// workers use the warp-level paths behind Master / Worker in
+// ompds_generic.cuh (fetch_is_fast / fetch_account_fast / end_parallel_warp),
+// which keep the same state, statistics and event log.
 //===----------------------------------------------------------------------===//
 
 __device__ __forceinline__ int32_t __kmpc_kernel_init(const TeamCtx &t,
