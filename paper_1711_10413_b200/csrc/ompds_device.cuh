@@ -895,8 +895,8 @@ struct DsStack {
 
 //===----------------------------------------------------------------------===//
 // Reference / LLVM-runtime entry-point names.  Like omplab::TeamRuntime
-// (DeviceRuntime.h:81-119: "one instance per team, not thread-safe") these
-// are single-caller: one thread of the team at a time, e.g. a code
+// (DeviceRuntime.h:81-119; one instance per team, calls serialised by the
+// simulator, not thread-safe) these are single-caller: one thread of the team at a time, e.g. a code
 // generator's master thread, or the protocol replay kernel.  Concurrent
 // workers use the warp-level paths behind Master / Worker in
 // ompds_generic.cuh (fetch_is_fast / fetch_account_fast / end_parallel_warp),
