@@ -494,15 +494,17 @@ def test_config2_bench_grid_full_size_matches_oracle():
 
 
 @pytest.mark.gpu
-def test_config4_past_2_pow_31_elements_checksum_vs_oracle():
-    """Maximum-size edge: 2^31 + 5 int32 elements (64-bit element, unit and
+@pytest.mark.parametrize("elem", [0, 1])
+def test_config4_past_2_pow_31_elements_checksum_vs_oracle(elem):
+    """Maximum-size edge: 2^31 + 5 elements (64-bit element, unit and
     block indices in the parallel-for), the bench grid; the oracle's
     checksum is accumulated over 2^26-element chunks regenerated from the
     same counter-based inputs, so host memory stays small."""
     n = (1 << 31) + 5
-    coef = [k + 1 for k in range(8)]
-    x = torch.empty(n, dtype=torch.int32, device=DEV)
-    y = torch.empty(n, dtype=torch.int32, device=DEV)
+    dt, npdt = (torch.float64, np.float64) if elem else (torch.int32, np.int32)
+    coef = COEF if elem else [k + 1 for k in range(8)]
+    x = torch.empty(n, dtype=dt, device=DEV)
+    y = torch.empty(n, dtype=dt, device=DEV)
     RG.fill_uniform(x, 0x5eed01ab)
     RG.fill_uniform(y, 0x5eed01ac)
     RG.run_stream(x, y, coef, 148 * 7, 96, stats=False)
@@ -511,13 +513,13 @@ def test_config4_past_2_pow_31_elements_checksum_vs_oracle():
     del x, y
     torch.cuda.empty_cache()
     want, chunk = 0, 1 << 26
-    xs = np.empty(chunk, dtype=np.int32)
-    ys = np.empty(chunk, dtype=np.int32)
-    cf = np.array(coef, dtype=np.int32)
+    xs = np.empty(chunk, dtype=npdt)
+    ys = np.empty(chunk, dtype=npdt)
+    cf = np.array(coef, dtype=npdt)
     for lo in range(0, n, chunk):
         m = min(chunk, n - lo)
-        O.lib().orc_fill(0, O.ptr(xs), m, 0x5eed01ab, lo)
-        O.lib().orc_fill(0, O.ptr(ys), m, 0x5eed01ac, lo)
-        O.lib().orc_stream(0, m, O.ptr(xs), O.ptr(ys), O.ptr(cf), 0)
-        want = (want + O.lib().orc_checksum(0, O.ptr(ys), m)) & ((1 << 64) - 1)
+        O.lib().orc_fill(elem, O.ptr(xs), m, 0x5eed01ab, lo)
+        O.lib().orc_fill(elem, O.ptr(ys), m, 0x5eed01ac, lo)
+        O.lib().orc_stream(elem, m, O.ptr(xs), O.ptr(ys), O.ptr(cf), 0)
+        want = (want + O.lib().orc_checksum(elem, O.ptr(ys), m)) & ((1 << 64) - 1)
     assert got == want
