@@ -343,8 +343,9 @@ int32_t ompds_run_shared_array(const ompds_launch *launch, int32_t elem,
  *   float64: y[i] = fma(c1, x[i], y[i]) + s,  s = ((((((c2+c3)+c4)+c5)+c6)+c7)+c8)
  *   int32  : y[i] = y[i] + (c1*x[i] + c2 + ... + c8)   (wrapping int32)
  * `coef` (host, 8 values of elem type) are the master's initial values.
- * x, y aligned to the element; both 16-byte aligned gets the vectorised
- * body, otherwise the element-wise one (same results). */
+ * x, y aligned to the element (may be NULL when n == 0: the region still
+ * runs); both 16-byte aligned gets the vectorised body, otherwise the
+ * element-wise one (same results). */
 int32_t ompds_run_stream(const ompds_launch *launch, int32_t elem, int64_t n,
                          const void *x, void *y, const void *coef_host,
                          ompds_team_stats *stats_dev, ompds_event *events_dev);

@@ -984,7 +984,7 @@ int32_t ompds_run_shared_array(const ompds_launch *launch, int32_t elem,
                                int64_t n, void *a, const void *d_init,
                                ompds_team_stats *stats, ompds_event *events) {
   const int64_t esz = elem ? 8 : 4;
-  if (!a || n < 0 || (elem != 0 && elem != 1) ||
+  if ((!a && n > 0) || n < 0 || (elem != 0 && elem != 1) ||
       (reinterpret_cast<uintptr_t>(a) & (esz - 1)) ||
       (reinterpret_cast<uintptr_t>(d_init) & (esz - 1)))
     return OMPDS_ERR_INVALID;
@@ -1012,7 +1012,7 @@ int32_t ompds_run_stream(const ompds_launch *launch, int32_t elem, int64_t n,
                          const void *x, void *y, const void *coef_host,
                          ompds_team_stats *stats, ompds_event *events) {
   const uintptr_t esz = elem ? 8 : 4;
-  if (!x || !y || !coef_host || n < 0 || (elem != 0 && elem != 1) ||
+  if (((!x || !y) && n > 0) || !coef_host || n < 0 || (elem != 0 && elem != 1) ||
       (reinterpret_cast<uintptr_t>(x) & (esz - 1)) ||
       (reinterpret_cast<uintptr_t>(y) & (esz - 1)))
     return OMPDS_ERR_INVALID;
@@ -1328,7 +1328,7 @@ int32_t ompds_run_stream_host(const ompds_launch *launch, int32_t elem,
 
 int32_t ompds_fill_uniform(int32_t elem, void *out, int64_t n, uint64_t seed,
                            int64_t first, void *stream) {
-  if (!out || n < 0 || (elem != 0 && elem != 1))
+  if ((!out && n > 0) || n < 0 || (elem != 0 && elem != 1))
     return OMPDS_ERR_INVALID;
   if (n == 0)
     return OMPDS_OK;
@@ -1380,7 +1380,7 @@ int32_t ompds_probe_overheads(int32_t iterations, ompds_overhead_probe *out,
 
 int32_t ompds_checksum(int32_t elem, const void *data, int64_t n,
                        uint64_t *out_dev, void *stream) {
-  if (!data || !out_dev || n < 0 || (elem != 0 && elem != 1))
+  if ((!data && n > 0) || !out_dev || n < 0 || (elem != 0 && elem != 1))
     return OMPDS_ERR_INVALID;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   OMPDS_CUDA(cudaMemsetAsync(out_dev, 0, 8, st));

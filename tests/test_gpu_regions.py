@@ -523,3 +523,28 @@ def test_config4_past_2_pow_31_elements_checksum_vs_oracle(elem):
         O.lib().orc_stream(elem, m, O.ptr(xs), O.ptr(ys), O.ptr(cf), 0)
         want = (want + O.lib().orc_checksum(elem, O.ptr(ys), m)) & ((1 << 64) - 1)
     assert got == want
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 17, 1023])
+def test_config2_and_4_tiny_and_empty_ranges(n):
+    """Empty and tiny element ranges (fewer elements than one warp, than the
+    vector width): the region still runs once per team, the elements that
+    exist equal the oracle."""
+    x, y = _f64_inputs(n)
+    out = RG.run_stream(x, y, COEF, 37, 96)
+    xs = np.empty(n)
+    ys = np.empty(n)
+    O.lib().orc_fill(1, O.ptr(xs), n, 0x5eed01ab, 0)
+    O.lib().orc_fill(1, O.ptr(ys), n, 0x5eed01ac, 0)
+    O.lib().orc_stream(1, n, O.ptr(xs), O.ptr(ys), O.ptr(np.array(COEF)), 0)
+    assert np.array_equal(y.cpu().numpy().view(np.uint64), ys.view(np.uint64))
+    assert all(s.trap == 0 and s.regions == 1 for s in out.team_stats())
+    a = torch.empty(n, dtype=torch.float64, device=DEV)
+    RG.fill_uniform(a, 0x5eed01ac)
+    out = RG.run_shared_array(a, 5, 64)
+    want = np.empty(n)
+    O.lib().orc_fill(1, O.ptr(want), n, 0x5eed01ac, 0)
+    O.lib().orc_shared_array(1, n, O.ptr(want))
+    assert np.array_equal(a.cpu().numpy(), want)
+    assert all(s.trap == 0 and s.regions == 1 for s in out.team_stats())
