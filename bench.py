@@ -330,11 +330,19 @@ def main():
     a = torch.zeros(32, dtype=torch.float64, device=dev)
     RG.run_regions(a, 1, 32, 10, stream=stream)
     stream.synchronize()
+    # A latency-bound region on one SM runs at whatever clock the GPU is at:
+    # right after the power-capped config-4 run that is still below max for
+    # a while (config 1 measured 407-444 ns across back-to-back runs, flat
+    # 407.6 in isolation, tools/cfg1_variance.py).  Let the clock recover,
+    # and report the SM clock the probe sees on either side.
+    time.sleep(1.0)
+    clk_before = RG.probe_overheads(1024, stream=stream)["sm_clock_mhz"]
     ns_per_region = device_ms(stream, lambda: RG.run_regions(a, 1, 32, R, stream=stream)) \
         * 1e6 / R
     # the reference's integer analog (4 int captures, int body) beside it
     ai = torch.zeros(32, dtype=torch.int32, device=dev)
     ns_int = device_ms(stream, lambda: RG.run_regions(ai, 1, 32, R, stream=stream)) * 1e6 / R
+    clk_after = RG.probe_overheads(1024, stream=stream)["sm_clock_mhz"]
     # the same protocol on every SM: as many 64-thread teams per SM as the
     # kernel's registers allow (one wave; 18/SM at 52 registers, the B200 row
     # of the occupancy model = ncu's launch__occupancy_limit_registers),
@@ -422,6 +430,7 @@ def main():
         "regions": {"ns_per_region": round(ns_per_region, 1),
                     "ns_per_region_int_analog": round(ns_int, 1),
                     "regions_per_s": round(1e9 / ns_per_region, 1),
+                    "sm_clock_mhz_around": [clk_before, clk_after],
                     "workload": "config 1: 1 team x 32 workers, 4 shared scalars (2 int, 2 double), "
                                 f"{R} regions in a sequential loop",
                     "aggregate_regions_per_s": round(agg_regions_per_s, 0),
