@@ -328,7 +328,7 @@ def main():
     # config 1 shares 2 int and 2 double scalars (RegionsProg<double>: c1, c2
     # int, c3, c4 and a[] double)
     a = torch.zeros(32, dtype=torch.float64, device=dev)
-    RG.run_regions(a, 1, 32, 10, stream=stream)
+    smem1 = RG.run_regions(a, 1, 32, 10, stream=stream).team_stats()[0].smem_bytes
     stream.synchronize()
     # A latency-bound region on one SM runs at whatever clock the GPU is at:
     # right after the power-capped config-4 run that is still below max for
@@ -431,6 +431,9 @@ def main():
                     "ns_per_region_int_analog": round(ns_int, 1),
                     "regions_per_s": round(1e9 / ns_per_region, 1),
                     "sm_clock_mhz_around": [clk_before, clk_after],
+                    "smem_bytes_per_cta": smem1,
+                    "teams_per_sm": per_sm1,
+                    "regs_per_thread": ptxas_regs("RegionsProgIdE"),
                     "workload": "config 1: 1 team x 32 workers, 4 shared scalars (2 int, 2 double), "
                                 f"{R} regions in a sequential loop",
                     "aggregate_regions_per_s": round(agg_regions_per_s, 0),
