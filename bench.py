@@ -551,8 +551,9 @@ def other_configs(RG, dev, stream, sms):
         "GBps_queued": round(16 * n2 / ms_queued / 1e6, 1),
         "timing": "ms: median of 10 launches, each after an L2 eviction and bracketed by "
                   f"CUDA events; ms_queued: {K} x [L2 evict; region] minus {K} x [L2 evict], "
-                  "queued back to back (ncu's kernel duration: 42.6 us)",
+                  "queued back to back (ncu's kernel duration: 42.6-43.2 us)",
         "smem_bytes_per_cta": st.smem_bytes, "depot_in_smem": st.depot_in_smem,
+        "regs_per_thread": ptxas_regs("SharedArrayProgIdE"),
         "staging": "cp.async.bulk (TMA) of d[256] into the depot slot",
         "roofline_frac": None,
         "l2": "evicted before every launch by reading a 256 MB buffer"}
@@ -565,7 +566,7 @@ def other_configs(RG, dev, stream, sms):
                              ("config3_nested_full", sms * 8, 2048),
                              ("config3_nested_1team_overflow", 1, 0)):
         a3 = torch.zeros(teams * 96, dtype=torch.float64, device=dev)
-        _, stacks = RG.run_nested(a3, teams, 96, 10, warp_slot_bytes=slot, stream=stream)
+        o3, stacks = RG.run_nested(a3, teams, 96, 10, warp_slot_bytes=slot, stream=stream)
         # timed: the launch only (collecting the warp statistics is host work)
         ms = device_ms(stream, lambda: RG.run_nested(a3, teams, 96, R, warp_slot_bytes=slot,
                                                      stream=stream, collect=False))
@@ -574,7 +575,9 @@ def other_configs(RG, dev, stream, sms):
                     "aggregate_regions_per_s": round(teams * R / (ms * 1e-3), 0),
                     "stack_depth": stacks[0][0].max_depth,
                     "frames_in_smem": stacks[0][0].frame_in_smem,
-                    "warp_slot_bytes": slot}
+                    "warp_slot_bytes": slot,
+                    "smem_bytes_per_cta": o3.team_stats()[0].smem_bytes,
+                    "regs_per_thread": ptxas_regs("NestedProgIdE")}
     return out
 
 
