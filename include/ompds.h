@@ -422,6 +422,9 @@ typedef struct ompds_program {
  * OMPDS_OK or OMPDS_ERR_INVALID. */
 int32_t ompds_program_verify(const ompds_program *prog);
 
+/* Runs a verified program (asynchronous on launch->stream; the descriptor
+ * and its arrays may be freed when the call returns).  Not capturable into
+ * a CUDA graph: the tables are staged from pageable host memory. */
 int32_t ompds_run_program(const ompds_launch *launch, const ompds_program *prog,
                           ompds_team_stats *stats_dev, ompds_event *events_dev);
 

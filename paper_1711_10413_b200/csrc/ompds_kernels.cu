@@ -1264,12 +1264,11 @@ int32_t ompds_run_program(const ompds_launch *launch, const ompds_program *pr,
                       reinterpret_cast<void *const *>(dev + o_bufs), mlocal,
                       std::max<int64_t>(pr->total_local, 4),
                       pr->step_limit > 0 ? pr->step_limit : int64_t(20000000)};
-  s = launch_generic<ProgramProg>(launch, lay, 0, a, stats, events);
-  if (s)
-    return s;
-  // the staging buffer is reused by the next launch: finish this one first
-  OMPDS_CUDA(cudaStreamSynchronize(st));
-  return OMPDS_OK;
+  // Asynchronous like the other launchers: the tables were copied out of
+  // `host` (pageable) before cudaMemcpyAsync returned, and the next launch's
+  // copy into the same workspace buffer is ordered behind this kernel by the
+  // stream (ensure_buffer synchronizes the stream before it ever frees it).
+  return launch_generic<ProgramProg>(launch, lay, 0, a, stats, events);
 }
 
 int32_t ompds_run_stream_host(const ompds_launch *launch, int32_t elem,

@@ -286,6 +286,28 @@ def test_gpu_runs_reference_programs_bit_exact():
 
 
 @pytest.mark.gpu
+def test_gpu_programs_queued_back_to_back_without_a_sync():
+    """ompds_run_program is asynchronous: every corpus/generated program is
+    enqueued on one stream with no synchronisation in between (each launch
+    restages its tables into the stream's workspace behind the previous
+    kernel), then all outputs are checked at once."""
+    import torch
+    pending = []
+    for p in programs()[:60]:
+        t, w, run = launches(p)[0]
+        prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], t, w)
+        bufs = [torch.full((sz,), init, dtype=torch.int32, device="cuda")
+                for _, sz, init in prog.buffers]
+        pending.append((p["stem"], prog, bufs, run, PG.run_program(prog, bufs)))
+    torch.cuda.synchronize()
+    assert len(pending) >= 40
+    for stem, prog, bufs, run, out in pending:
+        for (name, _, _), b in zip(prog.buffers, bufs):
+            assert b.cpu().tolist() == run["sim"]["globals"][name], (stem, name)
+        assert all(s.trap == 0 for s in out.team_stats()), stem
+
+
+@pytest.mark.gpu
 def test_gpu_reproduces_the_pass_order_miscompile():
     """SimulatorTests.cpp:150-173: bad pass order merges master-private t into
     the shared slot of c; unguarded, workers read 7 instead of 1."""
