@@ -236,6 +236,18 @@ def run_reference(args):
                                       "omplab simulate() (Simulator.cpp) per chunk"}
     base["e2e"] = {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}
+    # the other half of the metric, parallel regions/s: the config-1 analog
+    # (1 team x 32 workers, 4 shared int scalars) through the same simulator
+    L.omplab_ref_regions.argtypes = [C.c_int, C.c_int, C.c_int]
+    L.omplab_ref_regions.restype = C.c_double
+    R = 200
+    sec = L.omplab_ref_regions(0, 32, R)
+    if sec > 0:
+        base["regions"] = {"ns_per_region": round(sec * 1e9, 1),
+                           "regions_per_s": round(1 / sec, 1),
+                           "workload": f"config-1 analog: 1 team x 32 workers, 4 shared int "
+                                       f"scalars, {R} regions in a sequential loop, omplab "
+                                       "simulate() on one host thread"}
     print(json.dumps(base))
 
 
