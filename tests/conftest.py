@@ -18,3 +18,20 @@ def _built():
     build.build()
     from oracle import oracle
     oracle.build()
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _sanitizer_stack():
+    """OMPDS_TEST_CUDA_STACK=<bytes>: raise the per-thread stack limit for
+    runs under compute-sanitizer memcheck, whose device-heap checking runs
+    its malloc/free instrumentation on the stack of the calling kernel (the
+    region-program interpreter already uses 1.4 KB; with the default limit
+    the instrumented malloc overruns it).  Never set for normal runs."""
+    size = os.environ.get("OMPDS_TEST_CUDA_STACK")
+    if size:
+        import ctypes
+        import torch
+        if torch.cuda.is_available():
+            torch.zeros(1, device="cuda")
+            rt = ctypes.CDLL("libcudart.so.12")
+            assert rt.cudaDeviceSetLimit(0, ctypes.c_size_t(int(size))) == 0
