@@ -80,7 +80,9 @@ int32_t ompds_device_count(void);
  * slabs, program tables) kept for `stream` (a cudaStream_t, NULL = the
  * default stream) on the current device, after waiting for the stream's
  * work.  Call it before destroying a stream the library launched on; the
- * next launch on a stream reallocates on demand. */
+ * next launch on a stream reallocates on demand.  Buffers a larger launch
+ * superseded are kept until this call (CUDA graphs captured from earlier
+ * launches still point at them), so it invalidates such graphs. */
 int32_t ompds_release_workspace(void *stream);
 
 /* ------------------------------------------------------------------------ */

@@ -745,8 +745,14 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t, bool mine,
 //===----------------------------------------------------------------------===//
 
 struct SharedVars {
-  void *mine; // this lane's entry (lane j holds entry j)
+  void *mine;   // this lane's entry (lane j holds entry j)
+  void **list;  // the list itself: entries past the first 32 are read here
+  // Entry j of the list.  j < 32: a register shuffle (every lane of the warp
+  // must call it, with the same j); j >= 32: a load from the list (shared
+  // window or global block), since a shuffle source lane wraps modulo 32.
   __device__ __forceinline__ void *get(int j) const {
+    if (j >= kWarp)
+      return list[j];
     return reinterpret_cast<void *>(__shfl_sync(
         0xffffffffu, reinterpret_cast<unsigned long long>(mine), j));
   }
@@ -757,6 +763,7 @@ __device__ __forceinline__ SharedVars get_shared_variables(void **args,
   SharedVars v;
   const uint32_t lane = lane_id();
   v.mine = nullptr;
+  v.list = args;
   if (args != nullptr && static_cast<int32_t>(lane) < nargs) {
     if (__isShared(args)) { // the preallocated window: a plain LDS
       const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(args));
@@ -780,6 +787,7 @@ __device__ __forceinline__ SharedVars get_shared_variables(const TeamCtx &t,
   if (f.nargs <= t.prealloc) {
     SharedVars v;
     v.mine = static_cast<int32_t>(lane_id()) < f.nargs ? f.win : nullptr;
+    v.list = t.window;
     return v;
   }
 #endif

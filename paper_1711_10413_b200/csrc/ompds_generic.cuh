@@ -199,10 +199,13 @@ struct Master {
   }
 
   // prepare_parallel + publish &capture_j into the list + release + join.
+  // The captures are the layout's first kMaxCaptures depot slots
+  // (TeamParams::cap_off); a region with more captures publishes its own
+  // addresses through parallel_with.
   __device__ __forceinline__ int32_t parallel(int32_t fn, int32_t nargs) {
-    return parallel_with(fn, nargs, [this](int j) -> void * {
-      return cap(j < kMaxCaptures ? j : 0);
-    });
+    if (nargs > kMaxCaptures)
+      return sync_status(OMPDS_ERR_INVALID);
+    return parallel_with(fn, nargs, [this](int j) -> void * { return cap(j); });
   }
 
   template <class AddrOf>
@@ -471,9 +474,15 @@ __global__ void OMPDS_GENERIC_LB
 // buffer 2 a region program's tables, buffer 3 the masters' local depot
 // mirrors.  Launches on one stream run in order, so they can share a set;
 // launches on different streams (or devices) get their own.
+// A buffer that a larger launch supersedes is retired, not freed: a CUDA
+// graph captured from an earlier launch on the stream keeps pointing at it,
+// so it stays allocated until ompds_release_workspace (which therefore
+// invalidates graphs captured from launches on that stream).  Buffers grow by
+// at least 1.5x, so a stream retires O(log size) of them.
 struct WsBuffers {
   unsigned char *buf[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t bytes[4] = {0, 0, 0, 0};
+  std::vector<unsigned char *> retired;
 };
 struct Workspace {
   std::mutex mu;
@@ -488,14 +497,13 @@ inline int32_t ensure_buffer(int which, size_t bytes, unsigned char **out,
   OMPDS_CUDA(cudaGetDevice(&dev));
   WsBuffers &w = g_ws.sets[{dev, stream}];
   if (w.bytes[which] < bytes) {
-    if (w.buf[which]) { // earlier launches on this stream may still use it
-      OMPDS_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
-      OMPDS_CUDA(cudaFree(w.buf[which]));
-    }
-    w.buf[which] = nullptr;
-    w.bytes[which] = 0;
-    OMPDS_CUDA(cudaMalloc(&w.buf[which], bytes));
-    w.bytes[which] = bytes;
+    const size_t grow = std::max(bytes, w.bytes[which] + w.bytes[which] / 2);
+    unsigned char *fresh = nullptr;
+    OMPDS_CUDA(cudaMalloc(&fresh, grow));
+    if (w.buf[which]) // earlier launches (or captured graphs) may still use it
+      w.retired.push_back(w.buf[which]);
+    w.buf[which] = fresh;
+    w.bytes[which] = grow;
   }
   *out = w.buf[which];
   return OMPDS_OK;
@@ -509,6 +517,9 @@ inline int32_t release_workspace(void *stream) {
   if (it == g_ws.sets.end())
     return OMPDS_OK;
   OMPDS_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  for (unsigned char *b : it->second.retired)
+    OMPDS_CUDA(cudaFree(b));
+  it->second.retired.clear();
   for (int k = 0; k < 4; ++k) {
     unsigned char *b = it->second.buf[k];
     it->second.buf[k] = nullptr;
@@ -576,8 +587,6 @@ int32_t launch_generic(const ompds_launch *l, const FixedLayout &lay,
   int32_t s = validate_launch(l);
   if (s)
     return s;
-  int ndev = 0;
-  OMPDS_CUDA(cudaGetDeviceCount(&ndev));
   TeamParams p{};
   p.workers = l->workers;
   p.prealloc = l->prealloc_entries;

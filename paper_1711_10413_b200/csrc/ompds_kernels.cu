@@ -150,7 +150,11 @@ template <class T> struct SharedArrayProg {
   __device__ static void master(Master &m, const Args &a) {
     T *d = reinterpret_cast<T *>(m.cap(0));
     constexpr uint32_t bytes = kLen * sizeof(T);
-    if (a.d_init != nullptr && m.depot.in_smem) {
+    // cp.async.bulk needs a 16-byte aligned global source (and destination:
+    // the depot slot is 16-aligned in smem); any other d_init view is copied
+    // by the reserved warp like the overflow case below.
+    const bool tma_ok = (reinterpret_cast<uintptr_t>(a.d_init) & 15u) == 0;
+    if (a.d_init != nullptr && m.depot.in_smem && tma_ok) {
       // TMA staging: the args window is idle until the first prepare, so
       // its first 8 bytes host the transfer's mbarrier -- no extra smem.
       uint64_t *bar = reinterpret_cast<uint64_t *>(m.t.window);
@@ -165,7 +169,8 @@ template <class T> struct SharedArrayProg {
       }
       __syncwarp();
     } else if (a.d_init != nullptr) {
-      // depot on the global overflow chain: the reserved warp copies.
+      // depot on the global overflow chain, or a source view that is not
+      // 16-byte aligned: the reserved warp copies.
       for (int k = lane_id(); k < kLen; k += 32)
         d[k] = a.d_init[k];
       __syncwarp();
@@ -647,13 +652,11 @@ struct ProgramProg {
   __device__ static void region(int32_t fn, const SharedVars &sv, Worker &w,
                                 const Args &a) {
     // get-shared-variables: the first 32 entries come from the warp-shuffle
-    // broadcast, further ones straight from the list.
+    // broadcast, further ones straight from the list (SharedVars::get).
     void *caps[kVmCaps];
     const int32_t n = w.nargs < kVmCaps ? w.nargs : kVmCaps;
-    for (int j = 0; j < 32 && j < n; ++j)
+    for (int j = 0; j < n; ++j)
       caps[j] = sv.get(j);
-    for (int j = 32; j < n; ++j)
-      caps[j] = w.args[j];
     if (!w.mine)
       return;
     alignas(16) unsigned char priv[kVmPriv];
@@ -1113,25 +1116,41 @@ bool vm_has_arg(int32_t op) {
          op == OP_STOREX || op == OP_JMP || op == OP_JNLT || op == OP_PARALLEL;
 }
 
-bool vm_var_ok(const ompds_program *pr, int32_t v, bool master, int32_t nargs) {
+// `reg`: the region whose body addresses the variable (nullptr: the
+// master's sequential code).
+bool vm_var_ok(const ompds_program *pr, int32_t v, bool master,
+               const ompds_prog_region *reg) {
   if (v < 0 || v >= pr->n_vars)
     return false;
   const ompds_prog_var d = pr->vars[v];
-  if (d.count < 0)
+  if (d.count < 0 || d.index < 0)
+    return false;
+  // frame variables are int32 elements at 4-byte aligned offsets
+  const bool framed = d.space == SP_DEPOT || d.space == SP_MLOCAL || d.space == SP_PRIV;
+  if (framed && (d.index & 3))
     return false;
   const int64_t end = int64_t(d.index) + 4 * int64_t(d.count);
   switch (d.space) {
-  case SP_DEPOT: return master && d.index >= 0 && end <= pr->total_shared;
-  case SP_MLOCAL: return master && d.index >= 0 && end <= std::max<int64_t>(pr->total_local, 4);
-  case SP_PRIV: return !master && d.index >= 0 && end <= kVmPriv;
-  case SP_CAPTURE: return !master && d.index >= 0 && d.index < nargs;
-  case SP_GLOBAL: return d.index >= 0 && d.index < pr->n_buffers;
+  case SP_DEPOT: return master && end <= pr->total_shared;
+  case SP_MLOCAL: return master && end <= std::max<int64_t>(pr->total_local, 4);
+  case SP_PRIV: return !master && end <= kVmPriv;
+  case SP_CAPTURE: {
+    // capture j of the region: it aliases the master variable the region
+    // publishes as entry j, so it may not extend past that variable
+    if (master || reg == nullptr || d.index >= reg->n_captures)
+      return false;
+    const int32_t src = pr->captures[reg->cap_begin + d.index];
+    if (src < 0 || src >= pr->n_vars || pr->vars[src].space == SP_CAPTURE)
+      return false;
+    return d.count <= pr->vars[src].count;
+  }
+  case SP_GLOBAL: return d.index < pr->n_buffers;
   default: return false;
   }
 }
 
 bool vm_walk(const ompds_program *pr, const std::vector<int8_t> &start, int32_t entry,
-             bool master, int32_t nargs) {
+             bool master, const ompds_prog_region *reg) {
   const int64_t n = pr->n_code;
   const int32_t *code = pr->code;
   std::vector<int32_t> depth(size_t(n), -1);
@@ -1172,7 +1191,7 @@ bool vm_walk(const ompds_program *pr, const std::vector<int8_t> &start, int32_t 
     default: return false;
     }
     if ((op == OP_LOAD || op == OP_STORE || op == OP_LOADX || op == OP_STOREX) &&
-        !vm_var_ok(pr, arg, master, nargs))
+        !vm_var_ok(pr, arg, master, reg))
       return false;
     if (d < need || d + delta > kVmStack)
       return false;
@@ -1199,12 +1218,12 @@ bool verify_program(const ompds_program *pr) {
         (g.n_captures > 0 && !pr->captures))
       return false;
     for (int32_t j = 0; j < g.n_captures; ++j)
-      if (!vm_var_ok(pr, pr->captures[g.cap_begin + j], true, 0))
+      if (!vm_var_ok(pr, pr->captures[g.cap_begin + j], true, nullptr))
         return false;
-    if (!vm_walk(pr, start, g.entry, false, g.n_captures))
+    if (!vm_walk(pr, start, g.entry, false, &g))
       return false;
   }
-  return vm_walk(pr, start, 0, true, 0);
+  return vm_walk(pr, start, 0, true, nullptr);
 }
 
 } // namespace
@@ -1214,6 +1233,8 @@ extern "C" {
 int32_t ompds_program_verify(const ompds_program *pr) {
   if (!pr || !pr->code || pr->n_code <= 0 || pr->n_vars < 0 || pr->n_regions < 0 ||
       pr->n_captures < 0 || pr->n_buffers < 0 || pr->total_shared < 0 ||
+      (pr->total_shared & 7) != 0 || /* the args window and runtime span follow
+                                        the depot at 8-byte aligned offsets */
       pr->total_local < 0 || pr->priv_bytes > kVmPriv)
     return OMPDS_ERR_INVALID;
   if ((pr->n_regions > 0 && !pr->regions) || (pr->n_vars > 0 && !pr->vars) ||

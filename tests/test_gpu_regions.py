@@ -548,3 +548,57 @@ def test_config2_and_4_tiny_and_empty_ranges(n):
     O.lib().orc_shared_array(1, n, O.ptr(want))
     assert np.array_equal(a.cpu().numpy(), want)
     assert all(s.trap == 0 and s.regions == 1 for s in out.team_stats())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,off", [(torch.float64, 1), (torch.int32, 1), (torch.int32, 3)])
+def test_config2_d_init_view_not_16_byte_aligned(dtype, off):
+    """d_init = base[off:off+256] is aligned to its element but not to 16
+    bytes: the TMA bulk copy needs a 16-byte aligned source, so the reserved
+    warp copies it instead; results equal the staged-by-TMA run."""
+    n = 50_003
+    base = torch.arange(300, dtype=dtype, device=DEV) * 3 + 1
+    d_init = base[off:off + 256]
+    assert d_init.data_ptr() % 16 != 0
+    a = torch.zeros(n, dtype=dtype, device=DEV)
+    out = RG.run_shared_array(a, 37, 64, d_init=d_init)
+    torch.cuda.synchronize()
+    d = d_init.cpu().numpy()
+    want = d[np.arange(n) & 255]
+    assert np.array_equal(a.cpu().numpy(), want)
+    st = out.team_stats()
+    assert all(s.trap == 0 and s.depot_in_smem for s in st)
+
+
+@pytest.mark.gpu
+def test_graph_survives_a_larger_eager_launch():
+    """A graph captured after one eager launch keeps replaying correctly after
+    a later, larger eager launch on the same stream grew the workspace: the
+    superseded buffers are retired, not freed."""
+    s = torch.cuda.Stream()
+    a = torch.zeros(4 * 40, dtype=torch.int32, device=DEV)
+    with torch.cuda.stream(s):
+        RG.run_regions(a, 4, 40, 3, prealloc_entries=2, stream=s)  # sizes the slabs
+    s.synchronize()
+    a.zero_()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        RG.run_regions(a, 4, 40, 3, prealloc_entries=2, stream=s)
+    # a much larger grid on the same stream: the team slabs grow
+    big = torch.zeros(4096 * 40, dtype=torch.int32, device=DEV)
+    with torch.cuda.stream(s):
+        RG.run_regions(big, 4096, 40, 3, prealloc_entries=2, stream=s)
+    s.synchronize()
+    junk = [torch.full((1 << 20,), -1, dtype=torch.int32, device=DEV) for _ in range(8)]
+    torch.cuda.synchronize()
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    want = np.zeros(4 * 40, dtype=np.int32)
+    O.lib().orc_regions(0, 4, 40, 3, O.ptr(want))
+    assert np.array_equal(a.cpu().numpy(), want * 2)
+    want_big = np.zeros(4096 * 40, dtype=np.int32)
+    O.lib().orc_regions(0, 4096, 40, 3, O.ptr(want_big))
+    assert np.array_equal(big.cpu().numpy(), want_big)
+    del junk

@@ -232,6 +232,22 @@ def test_verifier_rejects_malformed_programs():
     bad = dataclasses.replace(prog, regions=[dataclasses.replace(r0, entry=r0.entry + 2)]
                               + list(prog.regions[1:]))
     assert PG.verify(bad) in (L.ERR_INVALID, L.OK)  # +2 may still be a boundary
+    # layout rules: a depot that would misalign the args window
+    # and runtime span; a frame variable at an offset that is not a multiple
+    # of 4; a region-side capture larger than the master variable it aliases
+    assert PG.verify(dataclasses.replace(prog, total_shared=prog.total_shared + 4)) == \
+        L.ERR_INVALID
+    sp, off, cnt = prog.vars[depot_var]
+    vars_ = list(prog.vars)
+    vars_[depot_var] = (sp, off + 2, cnt)
+    assert PG.verify(dataclasses.replace(prog, vars=vars_, total_shared=prog.total_shared + 8)) \
+        == L.ERR_INVALID
+    cap_vars = [i for i, v in enumerate(prog.vars) if v[0] == PG.SP_CAPTURE]
+    assert cap_vars, "shared_scalar's region reads a capture"
+    vars_ = list(prog.vars)
+    sp, j, cnt = vars_[cap_vars[0]]
+    vars_[cap_vars[0]] = (sp, j, cnt + 1)
+    assert PG.verify(dataclasses.replace(prog, vars=vars_)) == L.ERR_INVALID
     # the same descriptor is refused by ompds_run_program before the launch
     import ctypes as C
     desc, _keep = PG.describe(_mutants(prog)[0][1], [16])
