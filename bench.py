@@ -17,9 +17,15 @@ occupancy are reported alongside.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Multi-GPU (torchrun, one process per GPU): every rank runs the same region on
-its own element range (weak scaling: 2^28 elements per GPU, no data-path
-collective); the checksum of y is all-reduced once after timing.
+Multi-GPU (torchrun, one process per GPU; BASELINE config 5): strong scaling
+by default -- 2^28 elements in total, rank r owns [r*N/G, (r+1)*N/G) and its
+own teams, no data-path collective (``--scaling weak``: 2^28 per GPU).  The
+K steps are timed twice: CUDA events on each rank's stream (max over ranks =
+``value``) and a barrier-bracketed wall-clock window (``wall_window``).
+Correctness gate at every N: after timing the inputs are regenerated, one
+region pass runs, the per-rank checksums of y are all-reduced and compared
+with the whole range's expected checksum (tests/golden/config5_checksums.json,
+from the C oracle); ``checksum_ok`` is in the line and a mismatch exits 1.
 """
 from __future__ import annotations
 
@@ -49,7 +55,11 @@ def parse():
     ap.add_argument("--elements", type=int, default=1 << 28, help="elements per GPU (weak) or in total (strong)")
     ap.add_argument("--teams", type=int, default=0, help="0: 148 x teams-per-SM")
     ap.add_argument("--workers", type=int, default=0, help="W (0: tuned default)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (BASELINE config 5): --elements in total, split over the "
+                         "GPUs; weak: --elements per GPU")
+    ap.add_argument("--only-stream", action="store_true",
+                    help="only the headline stream region (skip configs 1-3 and overheads)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
@@ -164,6 +174,16 @@ def device_ms(stream, launch, reps=3):
     return statistics.median(times)
 
 
+def cpu_model():
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(n_sample, threads):
     """The C oracle port (fp64, OpenMP over the host's cores) on a bounded sample."""
     import numpy as np
@@ -184,6 +204,7 @@ def cpu_baseline(n_sample, threads):
             break
     gbs = BYTES_PER_ELEM * n_sample * reps / el / 1e9
     return {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"{n_sample} fp64 elements x {reps} passes of the config-4 body "
                       f"(oracle/ompds_oracle.c orc_stream, OpenMP {threads} threads)"}
 
@@ -231,7 +252,7 @@ def run_reference(args):
     # (the reference's i32 elements would move 12 B; counting 24 favours it)
     base["config"]["bytes_counted_per_element"] = BYTES_PER_ELEM
     base["cpu_baseline"] = {"value": base["value"], "unit": "GB/s", "cores": threads,
-                            "kind": "reference",
+                            "kind": "reference", "cpu_model": cpu_model(),
                             "sample": f"{nchunks} chunks x {chunk} int elements per step, "
                                       "omplab simulate() (Simulator.cpp) per chunk"}
     base["e2e"] = {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
@@ -251,6 +272,28 @@ def run_reference(args):
     print(json.dumps(base))
 
 
+def expected_checksum(n_total, rank):
+    """The checksum y must have after one region pass over [0, n_total):
+    the committed fixture (tests/golden/config5_checksums.json, generated by
+    the C oracle) when it lists n_total, else the oracle checker computed on
+    rank 0 (orc_stream_checksum: regenerates the inputs, no buffers)."""
+    fx = os.path.join(ROOT, "tests", "golden", "config5_checksums.json")
+    try:
+        d = json.load(open(fx))
+        if d["seed_x"] == SEED_X and d["seed_y"] == SEED_Y and d["coef"] == COEF and \
+                str(n_total) in d["checksums"]:
+            return int(d["checksums"][str(n_total)], 16), "tests/golden/config5_checksums.json"
+    except (OSError, ValueError, KeyError):
+        pass
+    if rank != 0:
+        return None, "oracle (rank 0)"
+    import numpy as np
+    from oracle import oracle as O  # the checker only
+    cf = np.array(COEF)
+    v = O.lib().orc_stream_checksum(1, 0, n_total, SEED_X, SEED_Y, O.ptr(cf), 0)
+    return int(v), "oracle/ompds_oracle.c orc_stream_checksum (checker)"
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -259,7 +302,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_1711_10413_b200 import _lib as PL
+    from paper_1711_10413_b200 import _lib as PL  # noqa: F401  (loads the .so: fails loudly)
     from paper_1711_10413_b200 import regions as RG
 
     rank, world, local = dist_env()
@@ -276,6 +319,8 @@ def main():
         else:
             dist.init_process_group(backend)
     from paper_1711_10413_b200 import sharding
+    # strong scaling (default, BASELINE config 5): 2^28 elements in total,
+    # rank r owns [r*N/G, (r+1)*N/G); weak: 2^28 per GPU
     n_total = args.elements * world if args.scaling == "weak" else args.elements
     lo, hi = sharding.shard_range(n_total, rank, world)
     n = hi - lo
@@ -290,19 +335,23 @@ def main():
     x = torch.empty(n, dtype=torch.float64, device=dev)
     y = torch.empty(n, dtype=torch.float64, device=dev)
     stream = torch.cuda.Stream(device=dev)
-    with torch.cuda.stream(stream):
+
+    def fill():
+        # each rank generates its own slice of the global counter-based inputs
         RG.fill_uniform(x, SEED_X, lo, stream=stream)
         RG.fill_uniform(y, SEED_Y, lo, stream=stream)
+
+    fill()
     stream.synchronize()
 
     def step():
         RG.run_stream(x, y, COEF, teams, workers, stats=False, stream=stream)
 
-    # parity of the first launch against the oracle on a slice (cheap, size-independent)
+    # runtime statistics of one launch (every team: no trap, one region)
     stats_out = RG.run_stream(x, y, COEF, teams, workers, stream=stream)
     stream.synchronize()
     st = stats_out.team_stats()
-    assert all(s.trap == 0 and s.regions == 1 for s in st)
+    assert all(s.trap == 0 and s.regions == 1 for s in st), "stream region trapped"
     smem_bytes = st[0].smem_bytes
 
     for _ in range(args.warmup):
@@ -313,8 +362,13 @@ def main():
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
+    # Two clocks over the same K steps: CUDA events on the launching stream
+    # (device time, max over ranks = `value`), and a wall-clock window
+    # bracketed by barriers on every rank -- if ranks did not actually run
+    # concurrently (e.g. several ranks sharing one GPU) the window shows it.
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
     ev0.record(stream)
     for _ in range(args.steps):
         step()
@@ -323,18 +377,144 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    wall_ms = (time.perf_counter() - w0) * 1e3
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    # every rank's (event ms, wall ms): a [world, 2] table filled row by row
+    # and summed (all_reduce works on CUDA tensors under nccl and gloo alike)
+    table = torch.zeros(world, 2, dtype=torch.float64, device=dev)
+    table[rank, 0], table[rank, 1] = ms, wall_ms
     if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+        dist.all_reduce(table)
+    gathered = table.cpu().tolist()
+    rank_ms = [float(g[0]) for g in gathered]
+    ms_max = max(rank_ms)
+    wall_max = max(float(g[1]) for g in gathered)
     ms_per_step = ms_max / args.steps
     value = BYTES_PER_ELEM * n_total / (ms_per_step * 1e-3) / 1e9
+    per_gpu = [round(BYTES_PER_ELEM * (sharding.shard_range(n_total, r, world)[1]
+                                       - sharding.shard_range(n_total, r, world)[0])
+                     / (rank_ms[r] / args.steps * 1e-3) / 1e9, 1) for r in range(world)]
+    value_wall = BYTES_PER_ELEM * n_total * args.steps / (wall_max * 1e-3) / 1e9
 
-    # checksum gather (once, outside the timed region)
+    # Correctness gate (every N): regenerate the inputs, one region pass,
+    # all-reduce the per-rank checksums and compare with the whole range's
+    # expected checksum (fixture or oracle checker).
+    fill()
+    step()
+    stream.synchronize()
     checksum = sharding.allreduce_checksum(RG.checksum(y, stream=stream), device=dev)
+    want, want_src = expected_checksum(n_total, rank)
+    if world > 1:  # rank 0's expectation (the oracle checker runs there only)
+        wt = torch.tensor(list(sharding.split64(want or 0)) + [int(want is not None)],
+                          dtype=torch.int64, device=dev)
+        dist.broadcast(wt, 0)
+        want = sharding.join64(int(wt[0]), int(wt[1])) if int(wt[2]) else None
+    checksum_ok = want is not None and checksum == want
+    gate = {"checksum": f"{checksum:#018x}",
+            "expected": f"{want:#018x}" if want is not None else None,
+            "checksum_ok": checksum_ok, "expected_from": want_src,
+            "what": f"sum of y's fp64 bit patterns mod 2^64 after one region pass over "
+                    f"[0, {n_total}) with regenerated inputs, per-rank element ranges "
+                    f"all-reduced over {world} rank(s)"}
 
+    from paper_1711_10413_b200 import occupancy as OCC
+    regions = {} if args.only_stream else regions_section(RG, torch, dist, dev, stream, sms,
+                                                          rank, world)
+    configs = other_configs(RG, dev, stream, sms) if rank == 0 and not args.only_stream \
+        else {}
+    regs = ptxas_regs("StreamProgIdE") or 64
+    thr = ((workers + 31) // 32) * 32 + 32
+    occ = OCC.occupancy_for("b200", smem_bytes, regs, thr)
+
+    peak, peak_src = measured_peaks()
+    if "config2_shared_array" in configs:
+        # from the queued steady-state time: it includes the write-back of
+        # the dirty lines a single launch leaves in L2
+        c2 = configs["config2_shared_array"]
+        c2["roofline_frac"] = round(c2["GBps_queued"] / peak, 4)
+        c2["roofline_frac_single_launch"] = round(c2["GBps"] / peak, 4)
+    roofline = {"bound": "hbm", "achieved": round(value / world, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(value / world / peak, 4), "traffic": None,
+                "peak_source": peak_src, "peak_nominal": 8000.0,
+                "frac_nominal": round(value / world / 8000.0, 4),
+                "algorithmic_bytes_per_launch": BYTES_PER_ELEM * n}
+    # DRAM bytes per launch from the committed `ncu --set full` capture, used
+    # only when it was taken on this exact build (sources hash) and size.
+    tr = os.path.join(ROOT, "profiles", "traffic.json")
+    roofline["traffic_source"] = None
+    if os.path.exists(tr):
+        try:
+            from paper_1711_10413_b200.build import sources_sha256
+            t = json.load(open(tr))
+            if t.get("n") == n and t.get("sources_sha256") == sources_sha256():
+                roofline["traffic"] = t["dram_bytes_per_launch"]
+                roofline["traffic_source"] = (f"profiles/{t['source']}.json (ncu, this build: "
+                                              f"sources {t['sources_sha256']})")
+                roofline["traffic_over_algorithmic"] = round(
+                    t["dram_bytes_per_launch"] / (BYTES_PER_ELEM * n), 4)
+            else:
+                roofline["traffic_source"] = ("profiles/traffic.json was captured for another "
+                                              "build or size: not reported")
+        except (OSError, ValueError, KeyError):
+            pass
+
+    line = {
+        "metric": "stream region body GB/s (config 4, 24 B/elem)",
+        "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config4_stream_region", "elements_per_gpu": n,
+                   "elements_total": n_total, "teams": teams, "workers": workers,
+                   "threads_per_team": ((workers + 31) // 32) * 32 + 32,
+                   "shared_scalars": 8, "parallelism": f"element-range shards x{world}",
+                   "l2": "inputs (2 x 8 B x n) larger than the 126 MB L2, no flush needed"},
+        "roofline": roofline,
+        "regions": regions,
+        "smem_bytes_per_cta": smem_bytes,
+        "smem_layout": "depot 80 + args window 160 + runtime span 49 (reference footprint 289)",
+        "regs_per_thread": regs,
+        "occupancy": {"model": "b200 row of the reference occupancy model",
+                      "teams_by_regs": occ.teams_by_regs, "teams_by_smem": occ.teams_by_smem,
+                      "teams_per_sm": occ.actual, "threads_per_team": thr,
+                      "grid_teams_per_sm": round(teams / sms, 2),
+                      "binding_limit": "registers" if occ.actual == occ.teams_by_regs
+                      else "smem" if occ.actual == occ.teams_by_smem else "blocks/threads"},
+        "checksum": f"{checksum:#018x}",
+        "checksum_ok": checksum_ok,
+        "correctness_gate": gate,
+        "per_gpu_GBps": per_gpu,
+        "aggregate_GBps": round(value, 1),
+        "wall_window": {"ms": round(wall_max, 3), "GBps": round(value_wall, 1),
+                        "how": "barrier-bracketed host wall clock around the same K steps "
+                               "on every rank, max over ranks (the events time each rank's "
+                               "own stream; this window also catches ranks that did not "
+                               "overlap)"},
+        "configs": configs,
+        "gpu_launches": args.steps,
+        "clocks": clk,
+    }
+    if not args.no_e2e:
+        e = e2e(args, teams, workers, n, dev, world)
+        if rank == 0:
+            line["e2e"] = e
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(1 << 26, os.cpu_count() or 1)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line))
+        sys.stdout.flush()
+    if not checksum_ok:
+        sys.stderr.write(f"bench: checksum mismatch on rank {rank}: {gate}\n")
+        sys.exit(1)
+
+
+def regions_section(RG, torch, dist, dev, stream, sms, rank, world):
+    """Config 1 (ns per region, whole-GPU regions/s), the args-list placement
+    study and the runtime building blocks' overheads."""
+    from paper_1711_10413_b200 import occupancy as OCC
     # config-1 latency: 1 team x 32 workers, R regions in a loop, 4 shared scalars
     R = 10_000
     # config 1 shares 2 int and 2 double scalars (RegionsProg<double>: c1, c2
@@ -405,80 +585,21 @@ def main():
                  "push_pop_pair_* = (push + store/load in a 40 B/lane frame + pop) - "
                  "(the same store/load at a fixed smem address); handoff = release + "
                  "join named barriers between the master and one worker warp")
-    configs = other_configs(RG, dev, stream, sms) if rank == 0 else {}
-    regs = ptxas_regs("StreamProgIdE") or 64
-    thr = ((workers + 31) // 32) * 32 + 32
-    occ = OCC.occupancy_for("b200", smem_bytes, regs, thr)
-
-    peak, peak_src = measured_peaks()
-    if "config2_shared_array" in configs:
-        c2 = configs["config2_shared_array"]
-        c2["roofline_frac"] = round(c2["GBps"] / peak, 4)
-    roofline = {"bound": "hbm", "achieved": round(value / world, 1), "peak": peak,
-                "unit": "GB/s", "frac": round(value / world / peak, 4), "traffic": None,
-                "peak_source": peak_src, "peak_nominal": 8000.0,
-                "frac_nominal": round(value / world / 8000.0, 4),
-                "algorithmic_bytes_per_launch": BYTES_PER_ELEM * n}
-    tr = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tr):
-        try:
-            t = json.load(open(tr))
-            if t.get("n") == n:
-                roofline["traffic"] = t["dram_bytes_per_launch"]
-        except (OSError, ValueError, KeyError):
-            pass
-
-    line = {
-        "metric": "stream region body GB/s (config 4, 24 B/elem)",
-        "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config4_stream_region", "elements_per_gpu": n,
-                   "elements_total": n_total, "teams": teams, "workers": workers,
-                   "threads_per_team": ((workers + 31) // 32) * 32 + 32,
-                   "shared_scalars": 8, "parallelism": f"element-range shards x{world}",
-                   "l2": "inputs (2 x 8 B x n) larger than the 126 MB L2, no flush needed"},
-        "roofline": roofline,
-        "regions": {"ns_per_region": round(ns_per_region, 1),
-                    "ns_per_region_int_analog": round(ns_int, 1),
-                    "regions_per_s": round(1e9 / ns_per_region, 1),
-                    "sm_clock_mhz_around": [clk_before, clk_after],
-                    "smem_bytes_per_cta": smem1,
-                    "teams_per_sm": per_sm1,
-                    "regs_per_thread": ptxas_regs("RegionsProgIdE"),
-                    "workload": "config 1: 1 team x 32 workers, 4 shared scalars (2 int, 2 double), "
-                                f"{R} regions in a sequential loop",
-                    "aggregate_regions_per_s": round(agg_regions_per_s, 0),
-                    "aggregate_workload": f"{world * teams2} teams x 32 workers x {R2} regions"
-                                          + (f", team grid sharded by range over {world} GPUs"
-                                             if world > 1 else ""),
-                    "args_list_placement": placement,
-                    "overheads": ov},
-        "smem_bytes_per_cta": smem_bytes,
-        "smem_layout": "depot 80 + args window 160 + runtime span 49 (reference footprint 289)",
-        "regs_per_thread": regs,
-        "occupancy": {"model": "b200 row of the reference occupancy model",
-                      "teams_by_regs": occ.teams_by_regs, "teams_by_smem": occ.teams_by_smem,
-                      "teams_per_sm": occ.actual, "threads_per_team": thr,
-                      "grid_teams_per_sm": round(teams / sms, 2),
-                      "binding_limit": "registers" if occ.actual == occ.teams_by_regs
-                      else "smem" if occ.actual == occ.teams_by_smem else "blocks/threads"},
-        "checksum": f"{checksum:#018x}",
-        "configs": configs,
-        "gpu_launches": args.steps,
-        "clocks": clk,
-    }
-    if not args.no_e2e:
-        e = e2e(args, teams, workers, n, dev, world)
-        if rank == 0:
-            line["e2e"] = e
-    if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(1 << 26, os.cpu_count() or 1)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
-    if rank == 0:
-        print(json.dumps(line))
+    return {"ns_per_region": round(ns_per_region, 1),
+            "ns_per_region_int_analog": round(ns_int, 1),
+            "regions_per_s": round(1e9 / ns_per_region, 1),
+            "sm_clock_mhz_around": [clk_before, clk_after],
+            "smem_bytes_per_cta": smem1,
+            "teams_per_sm": per_sm1,
+            "regs_per_thread": ptxas_regs("RegionsProgIdE"),
+            "workload": "config 1: 1 team x 32 workers, 4 shared scalars (2 int, 2 double), "
+                        f"{R} regions in a sequential loop",
+            "aggregate_regions_per_s": round(agg_regions_per_s, 0),
+            "aggregate_workload": f"{world * teams2} teams x 32 workers x {R2} regions"
+                                  + (f", team grid sharded by range over {world} GPUs"
+                                     if world > 1 else ""),
+            "args_list_placement": placement,
+            "overheads": ov}
 
 
 def other_configs(RG, dev, stream, sms):

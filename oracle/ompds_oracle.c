@@ -483,6 +483,48 @@ void orc_stream(int32_t elem, int64_t n, const void *x, void *y, const void *coe
   }
 }
 
+/* Config 4/5 checker over the element range [lo, hi) without materialising
+ * x or y: each element is regenerated from the counter-based inputs
+ * (orc_fill's formula), run through the region body once (orc_stream's
+ * formula) and its bit pattern summed mod 2^64 (orc_checksum's), OpenMP over
+ * `threads` (<= 0: all).  Equal to fill + stream + checksum of the range. */
+uint64_t orc_stream_checksum(int32_t elem, int64_t lo, int64_t hi, uint64_t seed_x,
+                             uint64_t seed_y, const void *coef, int32_t threads) {
+#ifdef _OPENMP
+  if (threads <= 0) threads = omp_get_max_threads();
+#else
+  (void)threads;
+#endif
+  uint64_t acc = 0;
+  if (elem) {
+    const double *c = (const double *)coef;
+    double s = c[1];
+    for (int k = 2; k < 8; ++k) s = s + c[k];
+    const double c1 = c[0];
+#pragma omp parallel for reduction(+ : acc) schedule(static) num_threads(threads)
+    for (int64_t i = lo; i < hi; ++i) {
+      const double x = (double)(orc_splitmix64(seed_x + (uint64_t)i) >> 11) * 0x1p-52 - 1.0;
+      const double y = (double)(orc_splitmix64(seed_y + (uint64_t)i) >> 11) * 0x1p-52 - 1.0;
+      const double r = fma(c1, x, y) + s;
+      uint64_t b;
+      memcpy(&b, &r, 8);
+      acc += b;
+    }
+  } else {
+    const int32_t *c = (const int32_t *)coef;
+    int32_t s = c[1];
+    for (int k = 2; k < 8; ++k) s = wrap_add(s, c[k]);
+    const int32_t c1 = c[0];
+#pragma omp parallel for reduction(+ : acc) schedule(static) num_threads(threads)
+    for (int64_t i = lo; i < hi; ++i) {
+      const int32_t x = (int32_t)(orc_splitmix64(seed_x + (uint64_t)i) % 201) - 100;
+      const int32_t y = (int32_t)(orc_splitmix64(seed_y + (uint64_t)i) % 201) - 100;
+      acc += (uint64_t)(int64_t)wrap_add(y, wrap_add(wrap_mul(c1, x), s));
+    }
+  }
+  return acc;
+}
+
 void orc_nested(int32_t elem, int32_t teams, int32_t workers, int32_t regions, void *a) {
   for (int32_t t = 0; t < teams; ++t) {
     int32_t c = 1;

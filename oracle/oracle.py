@@ -54,6 +54,9 @@ def lib():
         L.orc_stream.argtypes = [C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_int32]
         L.orc_max_threads.restype = C.c_int32
+        L.orc_stream_checksum.argtypes = [C.c_int32, C.c_int64, C.c_int64, C.c_uint64,
+                                          C.c_uint64, C.c_void_p, C.c_int32]
+        L.orc_stream_checksum.restype = C.c_uint64
         L.orc_nested.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]
         L.orc_ds_stack.argtypes = [C.c_int64, C.c_int64, C.POINTER(C.c_int64),
                                    C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32),

@@ -36,6 +36,17 @@ def nvcc() -> str:
     return "nvcc"
 
 
+def sources_sha256() -> str:
+    """Hash of the device/host sources the library is built from: stamps
+    measurements (ncu traffic captures) with the build they were taken on."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in SOURCES + HEADERS:
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True

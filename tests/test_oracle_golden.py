@@ -201,3 +201,41 @@ def test_ds_stack_placement_rules():
     assert list(ins)[:4] == [1, 1, 0, 0] and list(off)[:4] == [0, 16, 0, 48]
     assert ins[6] == 1 and off[6] == 32  # after popping the chain, back in the slot
     assert md.value == 4 and hw.value == 32 + 56
+
+
+def test_stream_checksum_equals_fill_stream_checksum_and_pins_the_fixture():
+    """orc_stream_checksum (the config-5 checker: fill + one region pass +
+    checksum of a range, no buffers) equals orc_fill + orc_stream +
+    orc_checksum on the same range, for both element types and an offset
+    range; and reproduces the committed fixture bench.py gates on."""
+    import json
+    import os
+    import numpy as np
+    from oracle import oracle as O
+    L = O.lib()
+    for elem, coef in ((1, np.array([k / 8 for k in range(1, 9)])),
+                       (0, np.arange(1, 9, dtype=np.int32))):
+        dt = np.float64 if elem else np.int32
+        lo, n = 12_345, 100_003
+        x, y = np.empty(n, dt), np.empty(n, dt)
+        L.orc_fill(elem, O.ptr(x), n, 0x5eed01ab, lo)
+        L.orc_fill(elem, O.ptr(y), n, 0x5eed01ac, lo)
+        L.orc_stream(elem, n, O.ptr(x), O.ptr(y), O.ptr(coef), 0)
+        assert L.orc_checksum(elem, O.ptr(y), n) == L.orc_stream_checksum(
+            elem, lo, lo + n, 0x5eed01ab, 0x5eed01ac, O.ptr(coef), 0)
+    fx = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                     "config5_checksums.json")))
+    cf = np.array(fx["coef"])
+    for n in (1 << 20, 1 << 22):
+        got = L.orc_stream_checksum(1, 0, n, fx["seed_x"], fx["seed_y"], O.ptr(cf), 0)
+        assert "%#018x" % got == fx["checksums"][str(n)]
+    # shards gather to the whole range (sum mod 2^64 over element ranges)
+    n = 1 << 22
+    from paper_1711_10413_b200 import sharding
+    for world in (2, 3, 8):
+        acc = 0
+        for r in range(world):
+            a, b = sharding.shard_range(n, r, world)
+            acc = (acc + L.orc_stream_checksum(1, a, b, fx["seed_x"], fx["seed_y"],
+                                               O.ptr(cf), 0)) & ((1 << 64) - 1)
+        assert "%#018x" % acc == fx["checksums"][str(n)]

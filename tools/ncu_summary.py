@@ -115,8 +115,10 @@ def main():
             json.dump(s, f, indent=1)
         if a.traffic_n:
             with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as f:
+                sys.path.insert(0, ROOT)
+                from paper_1711_10413_b200.build import sources_sha256
                 json.dump({"n": a.traffic_n, "dram_bytes_per_launch": s[0]["dram_bytes_per_launch"],
-                           "source": a.name}, f, indent=1)
+                           "source": a.name, "sources_sha256": sources_sha256()}, f, indent=1)
         json.dump(s, sys.stdout, indent=1)
     if a.launches:
         s = summarise_launches(a.launches)
