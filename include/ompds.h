@@ -160,6 +160,56 @@ int32_t ompds_rt_replay(const ompds_runtime_config *config,
                         ompds_rt_result *results, ompds_event *events,
                         int32_t max_events, ompds_rt_summary *summary);
 
+/* ------------------------------------------------------------------------ */
+/* Team runtime handle: one omplab::TeamRuntime instance                   */
+/* (DeviceRuntime.h:81-119, constructed per team at Simulator.cpp:290-292). */
+/*                                                                          */
+/* State lives on the device between calls; each call runs the same        */
+/* __device__ protocol function the generic-mode kernels inline, O(1) per  */
+/* call (one launch + one stream synchronisation).  Like the reference     */
+/* class it is not thread-safe: one caller per handle.  Every operation    */
+/* returns 0 or the reference trap code (1..17, ompds_trap_reason), or     */
+/* OMPDS_ERR_*; a trap leaves the state, counters and event log unchanged. */
+/* ------------------------------------------------------------------------ */
+typedef struct ompds_team ompds_team; /* opaque */
+/* SharedArgsAllocator (DeviceRuntime.h:46-52): allocate returns the block
+ * address or 0 when the heap is exhausted; release gets back exactly the
+ * address allocate returned.  The runtime only stores and compares list
+ * addresses, so any non-zero integers are valid. */
+typedef uint64_t (*ompds_alloc_fn)(int64_t bytes, void *user);
+typedef void (*ompds_release_fn)(uint64_t addr, void *user);
+
+/* TeamRuntime(RuntimeConfig, PreallocBase, SharedArgsAllocator&): `alloc`
+ * and `release` both set or both NULL (NULL: every list past the window is
+ * shared-args-alloc-failed).  Binds the handle to the current device. */
+int32_t ompds_team_create(const ompds_runtime_config *config, uint64_t prealloc_base,
+                          ompds_alloc_fn alloc, ompds_release_fn release, void *user,
+                          ompds_team **out);
+int32_t ompds_team_destroy(ompds_team *team);
+/* TeamRuntime::kernelInit (DeviceRuntime.cpp:33-44) */
+int32_t ompds_team_kernel_init(ompds_team *team, int32_t role, int32_t workers);
+/* TeamRuntime::prepareParallel (:46-79); `fn` names the work function (an
+ * id >= 0; the C++ adapter interns the reference's strings).  *args_addr =
+ * prealloc_base for the window, else the allocator's block. */
+int32_t ompds_team_prepare_parallel(ompds_team *team, int32_t role, int32_t fn,
+                                    int64_t nargs, uint64_t *args_addr);
+/* TeamRuntime::kernelParallel (:81-100); after deinit: *fn = -1,
+ * *args_addr = 0, *participate = 0 (the termination sentinel). */
+int32_t ompds_team_kernel_parallel(ompds_team *team, int32_t role, int32_t *fn,
+                                   uint64_t *args_addr, int32_t *participate);
+/* TeamRuntime::endParallel (:102-128); the last retirement of a region with
+ * a heap list calls release(addr). */
+int32_t ompds_team_end_parallel(ompds_team *team, int32_t role);
+/* TeamRuntime::kernelDeinit (:130-143) */
+int32_t ompds_team_kernel_deinit(ompds_team *team, int32_t role);
+/* workerCount / dynamicAllocs / dynamicFrees / leakedBlocks / terminated */
+int32_t ompds_team_summary(const ompds_team *team, ompds_rt_summary *out);
+/* events(): copies events [first, first + max_events) of the log to `out`
+ * and sets *n_events = the total logged so far (OMPDS_ERR_CAPACITY when
+ * events past the copied ones remain; the handle keeps every event). */
+int32_t ompds_team_events(const ompds_team *team, int32_t first, ompds_event *out,
+                          int32_t max_events, int32_t *n_events);
+
 /* Capacity law dynamicArgsBytes (DeviceRuntime.h:35-38). */
 int64_t ompds_dynamic_args_bytes(int64_t nargs, int32_t prealloc_entries);
 

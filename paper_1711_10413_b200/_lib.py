@@ -141,6 +141,9 @@ class Program(C.Structure):
                 ("step_limit", C.c_int64)]
 
 
+AllocFn = C.CFUNCTYPE(C.c_uint64, C.c_int64, C.c_void_p)   # ompds_alloc_fn
+ReleaseFn = C.CFUNCTYPE(None, C.c_uint64, C.c_void_p)        # ompds_release_fn
+
 # Every symbol include/ompds.h declares, with its signature.
 _P = C.c_void_p
 _SIGS = {
@@ -152,6 +155,19 @@ _SIGS = {
     "ompds_rt_replay": (C.c_int32, [C.POINTER(RuntimeConfig), C.POINTER(RtCall), C.c_int32,
                                      C.POINTER(RtResult), C.POINTER(Event), C.c_int32,
                                      C.POINTER(RtSummary)]),
+    "ompds_team_create": (C.c_int32, [C.POINTER(RuntimeConfig), C.c_uint64, AllocFn, ReleaseFn,
+                                       C.c_void_p, C.POINTER(C.c_void_p)]),
+    "ompds_team_destroy": (C.c_int32, [C.c_void_p]),
+    "ompds_team_kernel_init": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32]),
+    "ompds_team_prepare_parallel": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64,
+                                                 C.POINTER(C.c_uint64)]),
+    "ompds_team_kernel_parallel": (C.c_int32, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32),
+                                                C.POINTER(C.c_uint64), C.POINTER(C.c_int32)]),
+    "ompds_team_end_parallel": (C.c_int32, [C.c_void_p, C.c_int32]),
+    "ompds_team_kernel_deinit": (C.c_int32, [C.c_void_p, C.c_int32]),
+    "ompds_team_summary": (C.c_int32, [C.c_void_p, C.POINTER(RtSummary)]),
+    "ompds_team_events": (C.c_int32, [C.c_void_p, C.c_int32, C.POINTER(Event), C.c_int32,
+                                       C.POINTER(C.c_int32)]),
     "ompds_dynamic_args_bytes": (C.c_int64, [C.c_int64, C.c_int32]),
     "ompds_layout_build": (C.c_int32, [C.POINTER(FrameVar), C.c_int32, C.c_int32, C.c_int32,
                                         C.POINTER(DepotLayout), C.POINTER(DepotSlot), C.c_int32,

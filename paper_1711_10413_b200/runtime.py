@@ -3,10 +3,13 @@
 Same names, argument meaning and error behaviour as the reference class:
 every operation returns an :class:`RtResult` (``ok`` / ``trap_reason`` with the
 reference's exact strings), nothing raises on a protocol violation.  The
-operations execute on the GPU: each call replays the team's call history
-through ``ompds_rt_replay`` -- the same ``__device__`` state machine the
-generic-mode kernels inline (csrc/ompds_device.cuh) -- so this class is a
-thin, synchronous view of the device runtime, not a host re-implementation.
+operations execute on the GPU: each instance owns one team handle
+(``ompds_team_create``) whose state lives in device memory, and each call
+runs the team's ``__device__`` protocol function once -- the same state
+machine the generic-mode kernels inline (csrc/ompds_device.cuh) -- so this
+class is a thin, synchronous view of the device runtime, not a host
+re-implementation.  ``replay`` runs a whole call script in one launch
+(``ompds_rt_replay``), for the recorded-script parity tests.
 """
 from __future__ import annotations
 
@@ -95,92 +98,154 @@ def replay(calls: Sequence[Tuple[int, int, int]], prealloc_entries: int = DEFAUL
     return ReplayOutcome(list(res[:n]), list(ev[:n_ev]), summ)
 
 
-class TeamRuntime:
-    """omplab::TeamRuntime with the device runtime behind it.
+class SharedArgsAllocator:
+    """DeviceRuntime.h:46-52: hooks for shared-args lists past the window.
 
-    ``prealloc_base`` is reported as the args address of regions that fit the
-    shared-memory window (the reference's PreallocBase); regions that spill
-    report a distinct non-zero address per live block.
+    ``allocate(nbytes)`` returns a non-zero block address, or 0 when the heap
+    is exhausted; ``release(addr)`` gets back exactly such an address.  The
+    runtime only stages and compares list addresses, so any distinct
+    non-zero integers will do (as in the reference's RecordingHeap)."""
+
+    def allocate(self, nbytes: int) -> int:  # pragma: no cover - interface
+        raise NotImplementedError
+
+    def release(self, addr: int) -> None:  # pragma: no cover - interface
+        raise NotImplementedError
+
+
+class RecordingHeap(SharedArgsAllocator):
+    """The reference's test heap (RuntimeTests.cpp:19-42): distinct
+    addresses, live blocks by address, allocation / free counts."""
+
+    def __init__(self, fail_all: bool = False, first: int = 0x1000):
+        self.fail_all = fail_all
+        self.next = first
+        self.live_bytes = {}
+        self.allocs = 0
+        self.frees = 0
+
+    def allocate(self, nbytes: int) -> int:
+        if self.fail_all:
+            return 0
+        addr = self.next
+        self.next += nbytes + 64
+        self.live_bytes[addr] = nbytes
+        self.allocs += 1
+        return addr
+
+    def release(self, addr: int) -> None:
+        if addr not in self.live_bytes:
+            raise AssertionError(f"release of an address that is not live: {addr:#x}")
+        del self.live_bytes[addr]
+        self.frees += 1
+
+
+class TeamRuntime:
+    """omplab::TeamRuntime(RuntimeConfig, PreallocBase, SharedArgsAllocator&)
+    over one GPU-resident team handle (``ompds_team_*``).
+
+    Every call runs the team's __device__ protocol function once (O(1) per
+    call, no history replay).  ``heap`` is called where the reference calls
+    it (DeviceRuntime.cpp:61-74, 108-121); by default a :class:`RecordingHeap`.
+    Methods return what the reference's out-parameters carry: e.g.
+    ``prepareParallel`` -> (RtResult, ArgsAddr).
     """
 
-    def __init__(self, config: Optional[RuntimeConfig] = None, prealloc_base: int = 0x2000):
+    def __init__(self, config: Optional[RuntimeConfig] = None, prealloc_base: int = 0x2000,
+                 heap: Optional[SharedArgsAllocator] = None):
         self.config = config or RuntimeConfig()
         self.prealloc_base = prealloc_base
-        self._calls: List[Tuple[int, int, int]] = []
+        self.heap = heap if heap is not None else RecordingHeap()
         self._fn_names: List[str] = []
-        self._last: Optional[ReplayOutcome] = None
+        self._fn_ids = {}
+        self._events: List[RuntimeEvent] = []
+        self._summary = L.RtSummary()
+        heap_ref = self.heap
+        # keep the ctypes trampolines alive as long as the handle
+        self._alloc = L.AllocFn(lambda nbytes, _u: int(heap_ref.allocate(int(nbytes))))
+        self._release = L.ReleaseFn(lambda addr, _u: heap_ref.release(int(addr)))
+        cfg = L.RuntimeConfig(self.config.prealloc_entries,
+                              1 if self.config.fail_dynamic_alloc else 0)
+        h = C.c_void_p()
+        L.check(L.lib().ompds_team_create(C.byref(cfg), prealloc_base, self._alloc,
+                                          self._release, None, C.byref(h)), "ompds_team_create")
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and L._lib is not None:
+            L._lib.ompds_team_destroy(h)
+            self._h = None
 
     # -- internals ---------------------------------------------------------
-    def _run(self, op: int, role: int, arg: int) -> Tuple[RtResult, L.RtResult]:
-        self._calls.append((op, role, int(arg)))
-        out = replay(self._calls, self.config.prealloc_entries, self.config.fail_dynamic_alloc)
-        self._last = out
-        r = out.results[-1]
-        if r.status != 0:
-            self._calls.pop()  # a trap leaves the state untouched
-            return RtResult(False, trap_reason(r.status), r.status), r
-        return RtResult(), r
+    def _done(self, status: int) -> RtResult:
+        if status >= L.ERR_CUDA:
+            L.check(status, "ompds_team")
+        if status != 0:
+            return RtResult(False, trap_reason(status), status)
+        lib = L.lib()
+        lib.ompds_team_summary(self._h, C.byref(self._summary))
+        buf = (L.Event * 8)()
+        total = C.c_int32()
+        while True:
+            first = len(self._events)
+            st = lib.ompds_team_events(self._h, first, buf, 8, C.byref(total))
+            for e in buf[:max(0, min(8, total.value - first))]:
+                fn = self._fn_names[e.fn] if 0 <= e.fn < len(self._fn_names) else ""
+                self._events.append(RuntimeEvent(L.EVENT_KIND_NAMES[e.kind], fn, e.nargs,
+                                                 e.bytes))
+            if st != L.ERR_CAPACITY:
+                break
+        return RtResult()
 
-    def _addr(self, kind: int) -> int:
-        if kind == L.ADDR_PREALLOC:
-            return self.prealloc_base
-        if kind == L.ADDR_DYNAMIC:
-            return 0x4000_0000 + 0x100 * len(self._fn_names)
-        return 0
+    def _intern(self, fn: str) -> int:
+        if fn not in self._fn_ids:
+            self._fn_ids[fn] = len(self._fn_names)
+            self._fn_names.append(fn)
+        return self._fn_ids[fn]
 
     # -- the reference API -------------------------------------------------
     def kernelInit(self, role: int, worker_count: int) -> RtResult:
-        return self._run(L.OP_KERNEL_INIT, role, worker_count)[0]
+        return self._done(L.lib().ompds_team_kernel_init(self._h, role, worker_count))
 
     def prepareParallel(self, role: int, fn: str, nargs: int) -> Tuple[RtResult, int]:
         """Returns (RtResult, ArgsAddr)."""
-        res, raw = self._run(L.OP_PREPARE_PARALLEL, role, nargs)
-        if not res.ok:
-            return res, 0
-        self._fn_names.append(fn)
-        return res, self._addr(raw.addr_kind)
+        addr = C.c_uint64()
+        res = self._done(L.lib().ompds_team_prepare_parallel(self._h, role, self._intern(fn),
+                                                             nargs, C.byref(addr)))
+        return res, (addr.value if res.ok else 0)
 
     def kernelParallel(self, role: int) -> Tuple[RtResult, str, int, bool]:
         """Returns (RtResult, WfName, ArgsAddr, Participate)."""
-        res, raw = self._run(L.OP_KERNEL_PARALLEL, role, 0)
+        fn, part, addr = C.c_int32(-1), C.c_int32(0), C.c_uint64()
+        res = self._done(L.lib().ompds_team_kernel_parallel(self._h, role, C.byref(fn),
+                                                            C.byref(addr), C.byref(part)))
         if not res.ok:
             return res, "", 0, False
-        wf = self._fn_names[raw.wf] if raw.wf >= 0 else ""
-        return res, wf, self._addr(raw.addr_kind), bool(raw.participate)
+        wf = self._fn_names[fn.value] if fn.value >= 0 else ""
+        return res, wf, addr.value, bool(part.value)
 
     def endParallel(self, role: int) -> RtResult:
-        return self._run(L.OP_END_PARALLEL, role, 0)[0]
+        return self._done(L.lib().ompds_team_end_parallel(self._h, role))
 
     def kernelDeinit(self, role: int) -> RtResult:
-        return self._run(L.OP_KERNEL_DEINIT, role, 0)[0]
+        return self._done(L.lib().ompds_team_kernel_deinit(self._h, role))
 
     # -- accessors (DeviceRuntime.h:97-102) --------------------------------
-    def _summary(self) -> L.RtSummary:
-        if self._last is None or (self._last.results and self._last.results[-1].status):
-            self._last = replay(self._calls, self.config.prealloc_entries,
-                                self.config.fail_dynamic_alloc)
-        return self._last.summary
-
     def workerCount(self) -> int:
-        return self._summary().workers
+        return self._summary.workers
 
     def dynamicAllocs(self) -> int:
-        return self._summary().dynamic_allocs
+        return self._summary.dynamic_allocs
 
     def dynamicFrees(self) -> int:
-        return self._summary().dynamic_frees
+        return self._summary.dynamic_frees
 
     def leakedBlocks(self) -> int:
-        return self._summary().leaked_blocks
+        return self._summary.leaked_blocks
 
     def terminated(self) -> bool:
-        return bool(self._summary().terminated)
+        return bool(self._summary.terminated)
 
     def events(self) -> List[RuntimeEvent]:
-        self._summary()
-        out = []
-        for e in self._last.events:
-            kind = L.EVENT_KIND_NAMES[e.kind]
-            fn = self._fn_names[e.fn] if e.fn >= 0 and e.fn < len(self._fn_names) else ""
-            out.append(RuntimeEvent(kind, fn, e.nargs, e.bytes))
-        return out
+        return list(self._events)

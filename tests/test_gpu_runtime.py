@@ -46,8 +46,8 @@ def test_device_runtime_matches_oracle_on_long_fuzz():
 
 # proj/tests/RuntimeTests.cpp, through the TeamRuntime mirror -------------------
 
-def live(workers=8, cfg=None):
-    rt = R.TeamRuntime(cfg or R.RuntimeConfig(), prealloc_base=0x2000)
+def live(workers=8, cfg=None, heap=None):
+    rt = R.TeamRuntime(cfg or R.RuntimeConfig(), prealloc_base=0x2000, heap=heap)
     assert rt.kernelInit(R.MASTER, workers).ok
     return rt
 
@@ -127,3 +127,60 @@ def test_byte_law_for_every_count():
         dyn = rt.events()[-1].bytes
         assert dyn == R.dynamic_args_bytes(n)
         assert (addr == 0x2000) == (n <= 20)
+
+
+def test_allocator_sees_exactly_the_reference_calls():
+    """The injected SharedArgsAllocator (RuntimeTests.cpp:19-42's
+    RecordingHeap): allocate(8*nargs) once per spilled region, the list
+    address returned is the allocator's block, release(that address) at the
+    last retirement -- with 3 workers, only the third retire frees."""
+    heap = R.RecordingHeap()
+    rt = live(workers=3, heap=heap)
+    res, addr = rt.prepareParallel(R.MASTER, "wf", 40)
+    assert res.ok and heap.live_bytes == {addr: 320} and heap.allocs == 1
+    for _ in range(3):
+        res, wf, a, part = rt.kernelParallel(R.WORKER)
+        assert res.ok and wf == "wf" and a == addr and part
+    for k in range(3):
+        assert rt.endParallel(R.WORKER).ok
+        assert (addr in heap.live_bytes) == (k < 2)
+    assert heap.frees == 1 and rt.leakedBlocks() == 0
+    # FailDynamicAlloc never reaches the heap; an exhausted heap traps and
+    # leaves the team Idle
+    h2 = R.RecordingHeap()
+    rt2 = live(cfg=R.RuntimeConfig(fail_dynamic_alloc=True), heap=h2)
+    res, _ = rt2.prepareParallel(R.MASTER, "wf", 21)
+    assert res.trap_reason == "shared-args-alloc-failed" and h2.allocs == 0
+    h3 = R.RecordingHeap(fail_all=True)
+    rt3 = live(heap=h3)
+    res, _ = rt3.prepareParallel(R.MASTER, "wf", 21)
+    assert res.trap_reason == "shared-args-alloc-failed"
+    h3.fail_all = False
+    res, addr = rt3.prepareParallel(R.MASTER, "wf", 21)
+    assert res.ok and h3.live_bytes == {addr: 168}
+
+
+def test_handle_calls_are_constant_time():
+    """No history replay: the 1000th region costs what the 10th does."""
+    import time
+    rt = live(workers=1)
+
+    def region():
+        assert rt.prepareParallel(R.MASTER, "wf", 2)[0].ok
+        assert rt.kernelParallel(R.WORKER)[0].ok
+        assert rt.endParallel(R.WORKER).ok
+
+    for _ in range(10):
+        region()
+    t0 = time.perf_counter()
+    for _ in range(50):
+        region()
+    early = time.perf_counter() - t0
+    for _ in range(900):
+        region()
+    t0 = time.perf_counter()
+    for _ in range(50):
+        region()
+    late = time.perf_counter() - t0
+    assert late < 3 * early, (early, late)
+    assert len(rt.events()) == 1 + 3 * 1010
