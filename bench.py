@@ -581,10 +581,14 @@ def regions_section(RG, torch, dist, dev, stream, sms, rank, world):
     ov["config1_protocol_ns_per_region"] = round(ns_per_region - ov["handoff_ns"], 1)
     # config 3: each worker warp pushes and pops 2 frames per nested region
     ov["config3_push_pop_ns_per_region"] = round(2 * ov["push_pop_pair_slot_ns"], 2)
-    ov["how"] = ("one 2-warp CTA, clock64 and %globaltimer over 8192 iterations each; "
-                 "push_pop_pair_* = (push + store/load in a 40 B/lane frame + pop) - "
-                 "(the same store/load at a fixed smem address); handoff = release + "
-                 "join named barriers between the master and one worker warp")
+    ov["config3_bookkeeping_ns_per_region"] = round(2 * ov["push_pop_pair_bookkeeping_ns"], 2)
+    ov["how"] = ("one warp per mode, clock64 and %globaltimer over 8192 iterations; iteration i "
+                 "pushes 1-2 frames of 40 B x 32 lanes (depth from a hash of i: frame size, "
+                 "lanes, depths and slot capacity are kernel arguments), stores and loads one "
+                 "word per lane in each, pops them; push_pop_pair_slot/chain = (that loop - the "
+                 "same accesses at fixed addresses) per pair; bookkeeping = the push/pop "
+                 "dependent chain with no frame access; handoff = release + join named "
+                 "barriers between the master and one worker warp")
     return {"ns_per_region": round(ns_per_region, 1),
             "ns_per_region_int_analog": round(ns_int, 1),
             "regions_per_s": round(1e9 / ns_per_region, 1),

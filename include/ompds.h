@@ -499,30 +499,41 @@ int32_t ompds_checksum(int32_t elem, const void *data, int64_t n,
 
 /* Cost of the runtime's building blocks on one SM (north_star: "push/pop +
  * handoff overhead"), measured by one 2-warp CTA with clock64 and
- * %globaltimer over `iterations` iterations each:
- *   smem_access    a store + load at a fixed shared address (the baseline);
- *   push_pop_slot  data-sharing stack push of a 40-byte-per-lane frame (the
- *                  config-3 level-1 frame), the same store + load in it, pop
- *                  -- frame in the warp's shared-memory slot;
- *   push_pop_chain the same with the frame on the global overflow chain;
- *   handoff        master warp <-> worker warp: the release and the join
- *                  barrier of one region with nothing staged (named barrier
- *                  1, non-aligned, as the team kernels use).
- * Push/pop overhead per pair = push_pop_* - smem_access. */
+ * %globaltimer.  Inputs (0 = default): iterations; frame_bytes per lane
+ * (4..256, multiple of 4; 40 = config 3's level-1 frame); lanes (1..32);
+ * max_depth (1..4, default 2 = config 3's two frames per worker warp);
+ * seed.  Iteration i pushes d_i in [1, max_depth] frames (a hash of i and
+ * seed: a run-time depth pattern), stores and loads one word per lane in
+ * each and pops them.  Outputs, in cycles per iteration:
+ *   smem_baseline / slot        the same accesses at fixed shared addresses /
+ *                               through push+pop with frames in the smem slot;
+ *   global_baseline / chain     fixed global addresses / push+pop with every
+ *                               frame on the global overflow chain;
+ *   bookkeeping(_baseline)      push+pop with no frame access (the
+ *                               bookkeeping's dependent chain) / without;
+ *   handoff                     release + join named barriers, master warp <->
+ *                               one worker warp, nothing staged.
+ * Cost per push+pop pair = (mode - its baseline) / (pairs / iterations). */
 typedef struct ompds_overhead_probe {
-  int32_t iterations;
+  int32_t iterations;  /* in: [1, 1<<20]                          */
+  int32_t frame_bytes; /* in                                       */
+  int32_t lanes;       /* in                                       */
+  int32_t max_depth;   /* in                                       */
+  uint32_t seed;       /* in                                       */
   int32_t reserved0;
-  double sm_clock_mhz; /* clock64 cycles per %globaltimer microsecond */
-  double smem_access_cycles;
-  double push_pop_slot_cycles;
-  double push_pop_chain_cycles;
+  double sm_clock_mhz; /* out: clock64 cycles per %globaltimer us  */
+  double pairs;        /* out: push/pop pairs executed per mode    */
+  double smem_baseline_cycles;
+  double slot_cycles;
+  double global_baseline_cycles;
+  double chain_cycles;
+  double bookkeeping_cycles;
+  double bookkeeping_baseline_cycles;
   double handoff_cycles;
-} ompds_overhead_probe; /* 48 bytes */
+} ompds_overhead_probe; /* 96 bytes */
 
-/* Runs the probe on the current device and `stream`; synchronises and
- * writes `*out` (host memory).  iterations in [1, 1<<20]. */
-int32_t ompds_probe_overheads(int32_t iterations, ompds_overhead_probe *out,
-                              void *stream);
+/* Runs the probe on the current device and `stream`; synchronises. */
+int32_t ompds_probe_overheads(ompds_overhead_probe *io, void *stream);
 
 /* Dynamic smem bytes per CTA the launchers request for a team region with
  * depot `total_shared` (== ompds_shared_footprint for the reference layout). */

@@ -102,9 +102,12 @@ class Launch(C.Structure):
 
 
 class OverheadProbe(C.Structure):
-    _fields_ = [("iterations", C.c_int32), ("reserved0", C.c_int32),
-                ("sm_clock_mhz", C.c_double), ("smem_access_cycles", C.c_double),
-                ("push_pop_slot_cycles", C.c_double), ("push_pop_chain_cycles", C.c_double),
+    _fields_ = [("iterations", C.c_int32), ("frame_bytes", C.c_int32), ("lanes", C.c_int32),
+                ("max_depth", C.c_int32), ("seed", C.c_uint32), ("reserved0", C.c_int32),
+                ("sm_clock_mhz", C.c_double), ("pairs", C.c_double),
+                ("smem_baseline_cycles", C.c_double), ("slot_cycles", C.c_double),
+                ("global_baseline_cycles", C.c_double), ("chain_cycles", C.c_double),
+                ("bookkeeping_cycles", C.c_double), ("bookkeeping_baseline_cycles", C.c_double),
                 ("handoff_cycles", C.c_double)]
 
 
@@ -191,7 +194,7 @@ _SIGS = {
                                            _P, _P]),
     "ompds_fill_uniform": (C.c_int32, [C.c_int32, _P, C.c_int64, C.c_uint64, C.c_int64, _P]),
     "ompds_checksum": (C.c_int32, [C.c_int32, _P, C.c_int64, _P, _P]),
-    "ompds_probe_overheads": (C.c_int32, [C.c_int32, C.POINTER(OverheadProbe), _P]),
+    "ompds_probe_overheads": (C.c_int32, [C.POINTER(OverheadProbe), _P]),
     "ompds_team_smem_bytes": (C.c_int64, [C.c_int64, C.c_int32]),
 }
 

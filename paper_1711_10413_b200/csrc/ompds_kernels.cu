@@ -775,83 +775,6 @@ __global__ void fill_i32_kernel(int32_t *out, int64_t n, uint64_t seed,
   }
 }
 
-// ompds_probe_overheads: warp 0 times the data-sharing stack against a fixed
-// shared address; then warp 0 (worker) and warp 1 (master) time the bare
-// two-barrier region handoff.  Each phase records clock64 and %globaltimer.
-constexpr int kProbeFrame = 40; // bytes per lane: config 3's level-1 frame
-constexpr int kProbeSlot = 4096;
-
-template <int mode>
-__device__ __forceinline__ int32_t probe_stack(unsigned char *slot, unsigned char *chain,
-                                               int64_t chain_bytes, int32_t iters,
-                                               long long *cyc, long long *ns) {
-  const uint32_t lane = lane_id();
-  DsStack ds;
-  // mode 0: no push/pop; 1: frames in the slot; 2: frames on the chain
-  ds.init(slot, mode == 2 ? 0 : kProbeSlot, chain, chain_bytes);
-  int32_t acc = 0;
-  __syncwarp();
-  const long long t0 = clock64();
-  const int64_t g0 = globaltimer_ns();
-  for (int32_t i = 0; i < iters; ++i) {
-    unsigned char *base = slot;
-    Frame f{};
-    if constexpr (mode != 0) {
-      f = ds.push(kProbeFrame, kWarp);
-      base = f.base;
-    }
-    volatile int32_t *e = reinterpret_cast<volatile int32_t *>(base + lane * kProbeFrame);
-    *e = i + acc;
-    acc += *e;
-    if constexpr (mode != 0)
-      acc += ds.pop(f);
-  }
-  __syncwarp();
-  *cyc = clock64() - t0;
-  *ns = globaltimer_ns() - g0;
-  return acc;
-}
-
-__global__ void __launch_bounds__(64)
-overhead_probe_kernel(int32_t iters, unsigned char *chain, int64_t chain_bytes,
-                      long long *out) {
-  __shared__ __align__(16) unsigned char slot[kProbeSlot];
-  const uint32_t warp = threadIdx.x / 32;
-  long long c[4] = {}, t[4] = {};
-  int32_t acc = 0;
-  if (warp == 0) {
-    // untimed pass: the chain's first touch (TLB, L2) is not a push/pop cost
-    acc += probe_stack<2>(slot, chain, chain_bytes, iters < 512 ? iters : 512, &c[2], &t[2]);
-    acc += probe_stack<0>(slot, chain, chain_bytes, iters, &c[0], &t[0]);
-    acc += probe_stack<1>(slot, chain, chain_bytes, iters, &c[1], &t[1]);
-    acc += probe_stack<2>(slot, chain, chain_bytes, iters, &c[2], &t[2]);
-  }
-  __syncthreads();
-  // region handoff without the runtime: release + join per iteration.  A
-  // BAR.SYNC.DEFER_BLOCKING lets the next clock read issue before the
-  // barrier resolves, so a few untimed handoffs first bring both warps into
-  // step, and warp 0 (the last to reach __syncthreads) reports.
-  for (int i = 0; i < 16; ++i) {
-    bar_sync(kBarHandoff, 64);
-    bar_sync(kBarHandoff, 64);
-  }
-  const long long h0 = clock64();
-  const int64_t hg0 = globaltimer_ns();
-  for (int32_t i = 0; i < iters; ++i) {
-    bar_sync(kBarHandoff, 64);
-    bar_sync(kBarHandoff, 64);
-  }
-  c[3] = clock64() - h0;
-  t[3] = globaltimer_ns() - hg0;
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < 4; ++k) {
-      out[2 * k] = c[k];
-      out[2 * k + 1] = t[k];
-    }
-    out[8] = acc;
-  }
-}
-
 template <class T>
 __global__ void checksum_kernel(const T *data, int64_t n,
                                 unsigned long long *out) {
@@ -1361,40 +1284,6 @@ int32_t ompds_fill_uniform(int32_t elem, void *out, int64_t n, uint64_t seed,
     fill_i32_kernel<<<blocks, 256, 0, st>>>(static_cast<int32_t *>(out), n,
                                             seed, first);
   OMPDS_CUDA(cudaGetLastError());
-  return OMPDS_OK;
-}
-
-int32_t ompds_probe_overheads(int32_t iterations, ompds_overhead_probe *out,
-                              void *stream) {
-  if (!out || iterations < 1 || iterations > (1 << 20))
-    return OMPDS_ERR_INVALID;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int64_t chain_bytes = 1 << 16;
-  unsigned char *chain = nullptr;
-  long long *dev = nullptr;
-  long long h[9] = {};
-  OMPDS_CUDA(cudaMalloc(&chain, chain_bytes + sizeof h));
-  dev = reinterpret_cast<long long *>(chain + chain_bytes);
-  overhead_probe_kernel<<<1, 64, 0, st>>>(iterations, chain, chain_bytes, dev);
-  cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(h, dev, sizeof h, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess)
-    e = cudaStreamSynchronize(st);
-  cudaFree(chain);
-  OMPDS_CUDA(e);
-  long long cyc = 0, ns = 0;
-  for (int k = 0; k < 4; ++k) {
-    cyc += h[2 * k];
-    ns += h[2 * k + 1];
-  }
-  out->iterations = iterations;
-  out->reserved0 = 0;
-  out->sm_clock_mhz = ns > 0 ? 1e3 * double(cyc) / double(ns) : 0.0;
-  out->smem_access_cycles = double(h[0]) / iterations;
-  out->push_pop_slot_cycles = double(h[2]) / iterations;
-  out->push_pop_chain_cycles = double(h[4]) / iterations;
-  out->handoff_cycles = double(h[6]) / iterations;
   return OMPDS_OK;
 }
 

@@ -270,25 +270,44 @@ def fill_uniform(t: torch.Tensor, seed: int, first: int = 0,
                                        seed, first, C.c_void_p(s)), "ompds_fill_uniform")
 
 
-def probe_overheads(iterations: int = 8192,
+def probe_overheads(iterations: int = 8192, frame_bytes: int = 40, max_depth: int = 2,
+                    lanes: int = 32, seed: int = 0x5eed01ab,
                     stream: Optional[torch.cuda.Stream] = None) -> dict:
     """The runtime's building blocks on one SM (ompds_probe_overheads):
-    cycles and ns per data-sharing stack push + pop pair (frame in the smem
-    slot / on the global chain, net of the store + load done in the frame)
-    and per bare region handoff (release + join barriers)."""
-    p = L.OverheadProbe()
+    cycles and ns per data-sharing stack push + pop pair -- frames in the
+    smem slot / on the global chain, net of the same store + load at fixed
+    addresses, and the bookkeeping's own dependent chain -- and per bare
+    region handoff (release + join barriers).  Depths vary per iteration
+    (1..max_depth from a hash of the iteration and `seed`)."""
+    p = L.OverheadProbe(iterations, frame_bytes, lanes, max_depth, seed & 0xFFFFFFFF, 0)
     s = (stream or torch.cuda.current_stream()).cuda_stream
-    L.check(L.lib().ompds_probe_overheads(iterations, C.byref(p), C.c_void_p(s)),
-            "ompds_probe_overheads")
+    L.check(L.lib().ompds_probe_overheads(C.byref(p), C.c_void_p(s)), "ompds_probe_overheads")
     ns = 1e3 / p.sm_clock_mhz if p.sm_clock_mhz > 0 else float("nan")
-    slot = p.push_pop_slot_cycles - p.smem_access_cycles
-    chain = p.push_pop_chain_cycles - p.smem_access_cycles
-    return {"iterations": p.iterations, "sm_clock_mhz": round(p.sm_clock_mhz, 1),
-            "smem_store_load_cycles": round(p.smem_access_cycles, 2),
+    per_it = p.pairs / p.iterations  # pairs per iteration
+
+    def pair(mode, base):
+        return (mode - base) / per_it
+    slot = pair(p.slot_cycles, p.smem_baseline_cycles)
+    chain = pair(p.chain_cycles, p.global_baseline_cycles)
+    book = pair(p.bookkeeping_cycles, p.bookkeeping_baseline_cycles)
+    # what a frame on the chain costs against one in the slot, per pair (the
+    # placement decision), including its store + load
+    placement = pair(p.chain_cycles, p.slot_cycles)
+    return {"iterations": p.iterations, "frame_bytes_per_lane": p.frame_bytes,
+            "lanes": p.lanes, "max_depth": p.max_depth, "pairs_per_iteration": round(per_it, 4),
+            "sm_clock_mhz": round(p.sm_clock_mhz, 1),
+            "cycles_per_iteration": {
+                "smem_baseline": round(p.smem_baseline_cycles, 2), "slot": round(p.slot_cycles, 2),
+                "global_baseline": round(p.global_baseline_cycles, 2),
+                "chain": round(p.chain_cycles, 2), "bookkeeping": round(p.bookkeeping_cycles, 2),
+                "bookkeeping_baseline": round(p.bookkeeping_baseline_cycles, 2)},
             "push_pop_pair_slot_cycles": round(slot, 2),
             "push_pop_pair_slot_ns": round(slot * ns, 2),
             "push_pop_pair_chain_cycles": round(chain, 2),
             "push_pop_pair_chain_ns": round(chain * ns, 2),
+            "push_pop_pair_bookkeeping_cycles": round(book, 2),
+            "push_pop_pair_bookkeeping_ns": round(book * ns, 2),
+            "chain_vs_slot_per_pair_cycles": round(placement, 2),
             "handoff_cycles": round(p.handoff_cycles, 2),
             "handoff_ns": round(p.handoff_cycles * ns, 2)}
 

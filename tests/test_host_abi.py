@@ -44,7 +44,7 @@ def test_struct_sizes_match_the_c_abi():
     assert C.sizeof(P.DepotLayout) == 32
     assert C.sizeof(P.Launch) == 56
     assert C.sizeof(P.TeamStats) == 56
-    assert C.sizeof(P.OverheadProbe) == 48
+    assert C.sizeof(P.OverheadProbe) == 96
 
 
 def test_trap_strings_are_the_reference_strings():
@@ -227,12 +227,36 @@ def test_team_range_outside_the_grid_is_rejected(first, teams, total):
 
 def test_overhead_probe_validates_before_touching_a_gpu():
     import ctypes as C
-    p = P.OverheadProbe()
-    assert P.lib().ompds_probe_overheads(0, C.byref(p), None) == P.ERR_INVALID
-    assert P.lib().ompds_probe_overheads((1 << 20) + 1, C.byref(p), None) == P.ERR_INVALID
-    assert P.lib().ompds_probe_overheads(16, None, None) == P.ERR_INVALID
-    if P.lib().ompds_device_count() == 0:
-        assert P.lib().ompds_probe_overheads(16, C.byref(p), None) == P.ERR_CUDA
+    L = P.lib()
+    for bad in (dict(iterations=0), dict(iterations=(1 << 20) + 1),
+                dict(iterations=16, frame_bytes=6), dict(iterations=16, frame_bytes=512),
+                dict(iterations=16, max_depth=5), dict(iterations=16, lanes=33)):
+        p = P.OverheadProbe(**bad)
+        assert L.ompds_probe_overheads(C.byref(p), None) == P.ERR_INVALID, bad
+    assert L.ompds_probe_overheads(None, None) == P.ERR_INVALID
+    if L.ompds_device_count() == 0:
+        p = P.OverheadProbe(iterations=16)
+        assert L.ompds_probe_overheads(C.byref(p), None) == P.ERR_CUDA
+
+
+def test_team_handle_validates_and_needs_a_gpu():
+    """ompds_team_create: invalid configurations are refused on the host;
+    without a GPU there is no handle (no host fallback)."""
+    import ctypes as C
+    L = P.lib()
+    h = C.c_void_p()
+    cfg = P.RuntimeConfig(-1, 0)
+    assert L.ompds_team_create(C.byref(cfg), 0x2000, P.AllocFn(), P.ReleaseFn(), None,
+                               C.byref(h)) == P.ERR_INVALID
+    cfg = P.RuntimeConfig(20, 0)
+    alloc = P.AllocFn(lambda n, u: 0x1000)
+    assert L.ompds_team_create(C.byref(cfg), 0x2000, alloc, P.ReleaseFn(), None,
+                               C.byref(h)) == P.ERR_INVALID  # one callback without the other
+    assert L.ompds_team_kernel_init(None, 0, 8) == P.ERR_INVALID
+    if L.ompds_device_count() == 0:
+        assert L.ompds_team_create(C.byref(cfg), 0x2000, P.AllocFn(), P.ReleaseFn(), None,
+                                   C.byref(h)) == P.ERR_CUDA
+        assert not h.value
 
 
 def test_element_misaligned_pointers_are_rejected_before_a_gpu():
