@@ -502,7 +502,8 @@ int32_t ompds_checksum(int32_t elem, const void *data, int64_t n,
  * %globaltimer.  Inputs (0 = default): iterations; frame_bytes per lane
  * (4..256, multiple of 4; 40 = config 3's level-1 frame); lanes (1..32);
  * max_depth (1..4, default 2 = config 3's two frames per worker warp);
- * seed.  Iteration i pushes d_i in [1, max_depth] frames (a hash of i and
+ * seed; frame_bytes * lanes * max_depth <= 8192, the probe's smem slot).
+ * Iteration i pushes d_i in [1, max_depth] frames (a hash of i and
  * seed: a run-time depth pattern), stores and loads one word per lane in
  * each and pops them.  Outputs, in cycles per iteration:
  *   smem_baseline / slot        the same accesses at fixed shared addresses /

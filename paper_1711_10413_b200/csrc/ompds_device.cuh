@@ -711,6 +711,18 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
   // no __syncwarp: the join barrier that follows orders the leader's
   // shared-memory updates for every participant
 }
+// end_parallel_warp for a region whose list is the window and whose team
+// keeps no event log (the lean instantiation: the launcher guarantees both).
+__device__ __forceinline__ void end_parallel_window(const TeamCtx &t, uint32_t plan) {
+  const bool leader = plan & 1u;
+  const uint32_t n = plan >> 8;
+  if (plan & 2u) {
+    __syncwarp(); // every lane's fetch reads before the leader's reset
+    retire_window_if(t, leader);
+  } else {
+    red_add_if(t.rt_s + Rt::kActive, (n << 16) - n, leader);
+  }
+}
 // Master warp, after the join barrier of a region it staged with the window
 // list and no event log, when the workers retired with fire-and-forget
 // atomics (several worker warps): the region was staged successfully, so
@@ -848,56 +860,52 @@ struct DsStack {
     high_water = 0;
   }
 
-  // __kmpc_data_sharing_push_stack(bytes_per_lane * lanes)
-  __device__ __forceinline__ Frame push(int64_t bytes_per_lane, int lanes) {
-    Frame f;
+  // Frame bytes (rounded to 8), or 0xffffffff when the frame cannot fit
+  // anywhere (over 2 GB, or negative).  Frame sizes are loop-invariant in
+  // region code, so this is hoisted out of region loops.
+  __device__ __forceinline__ static uint32_t frame_need(int64_t bytes_per_lane, int lanes) {
     const int64_t want = bytes_per_lane * lanes;
-    // frames over 2 GB cannot fit anywhere: overflow
-    const uint32_t need = want < 0 || want > 0x7ffffff0
-                              ? 0xffffffffu
-                              : (static_cast<uint32_t>(want) + 7u) & ~7u;
-    f.status = OMPDS_OK;
-    if (ovf_top == 0 && need <= slot_cap - top) {
-      f.base = slot + top;
-      f.offset = static_cast<int32_t>(top);
-      f.in_smem = 1;
-      top += need;
-    } else if (ovf != nullptr && need <= ovf_cap - ovf_top) {
-      f.base = ovf + ovf_top;
-      f.offset = static_cast<int32_t>(ovf_top);
-      f.in_smem = 0;
-      ovf_top += need;
-    } else {
-      f.base = nullptr;
-      f.offset = -1;
-      f.in_smem = 0;
-      f.status = OMPDS_TRAP_STACK_OVERFLOW;
-      return f;
-    }
-    ++depth;
-    if (depth > max_depth)
-      max_depth = depth;
-    if (top + ovf_top > high_water)
-      high_water = top + ovf_top;
+    return want < 0 || want > 0x7ffffff0 ? 0xffffffffu
+                                         : (static_cast<uint32_t>(want) + 7u) & ~7u;
+  }
+
+  // __kmpc_data_sharing_push_stack(bytes_per_lane * lanes).  Branch-free:
+  // the placement decision (slot while the chain is empty and the frame
+  // fits, else the chain) and the bookkeeping are selects on 32-bit
+  // registers, so the dependent chain from one push to the next is a few
+  // integer instructions (profiles/: ompds_probe_overheads, bookkeeping mode).
+  __device__ __forceinline__ Frame push(int64_t bytes_per_lane, int lanes) {
+    return push_bytes(frame_need(bytes_per_lane, lanes));
+  }
+  __device__ __forceinline__ Frame push_bytes(uint32_t need) {
+    const bool in_slot = (ovf_top == 0u) & (need <= slot_cap - top);
+    const bool in_ovf = !in_slot & (ovf != nullptr) & (need <= ovf_cap - ovf_top);
+    const bool ok = in_slot | in_ovf;
+    const uint32_t off = in_slot ? top : ovf_top;
+    Frame f;
+    f.base = ok ? (in_slot ? slot : ovf) + off : nullptr;
+    f.offset = ok ? static_cast<int32_t>(off) : -1;
+    f.in_smem = in_slot;
+    f.status = ok ? OMPDS_OK : OMPDS_TRAP_STACK_OVERFLOW;
+    top += in_slot ? need : 0u;
+    ovf_top += in_ovf ? need : 0u;
+    depth += ok;
+    max_depth = max(max_depth, depth);
+    high_water = max(high_water, top + ovf_top);
     return f;
   }
 
-  // __kmpc_data_sharing_pop_stack(frame)
+  // __kmpc_data_sharing_pop_stack(frame): strict LIFO -- the frame must be
+  // the top of its segment (and a slot frame can only be popped once the
+  // chain is empty).  Branch-free like push.
   __device__ __forceinline__ int32_t pop(const Frame &f) {
-    if (depth <= 0 || f.offset < 0)
-      return OMPDS_TRAP_STACK_UNDERFLOW;
     const uint32_t off = static_cast<uint32_t>(f.offset);
-    if (f.in_smem) {
-      if (ovf_top != 0 || off > top)
-        return OMPDS_TRAP_STACK_UNDERFLOW;
-      top = off;
-    } else {
-      if (off > ovf_top)
-        return OMPDS_TRAP_STACK_UNDERFLOW;
-      ovf_top = off;
-    }
-    --depth;
-    return OMPDS_OK;
+    const bool bad = (depth <= 0) | (f.offset < 0) |
+                     (f.in_smem ? (ovf_top != 0u) | (off > top) : off > ovf_top);
+    top = !bad && f.in_smem ? off : top;
+    ovf_top = !bad && !f.in_smem ? off : ovf_top;
+    depth -= !bad;
+    return bad ? OMPDS_TRAP_STACK_UNDERFLOW : OMPDS_OK;
   }
 };
 

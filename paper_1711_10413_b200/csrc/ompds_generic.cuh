@@ -138,6 +138,9 @@ struct Master {
   TeamCtx t;
   const TeamParams *p;
   bool leader;
+  bool lean;           // the launch's lean instantiation (a compile-time constant
+                       // after inlining): no event log, every list fits the
+                       // window -- the general prepare path is compiled out
   bool join_completes; // completes_at_join(): several worker warps, no event log
   int32_t fast_nargs;  // the fast prepare applies to nargs <= this: the
                        // window size without an event log, -1 with one
@@ -243,7 +246,23 @@ struct Master {
       regions += 1;
       return OMPDS_OK;
     }
+    if (lean)
+      return parallel_refused(prepare_check(st.phase, st.active, nargs));
     return parallel_general(fn, nargs, addr_of);
+  }
+
+  // Lean instantiation, a prepare the fast path does not cover: only a
+  // protocol violation gets here (the launcher chose lean because no region
+  // needs more than the window and nothing is logged).  The trap is recorded
+  // and the handoff still runs, so the workers see an unstaged region.
+  __device__ __noinline__ int32_t parallel_refused(int32_t s) {
+    if (s == OMPDS_OK)
+      s = OMPDS_ERR_INVALID;
+    sync_status(s);
+    bar_sync(kBarHandoff, team_threads); // release the workers
+    bar_sync(kBarHandoff, team_threads); // join
+    barriers += 2;
+    return trap;
   }
 
   template <class AddrOf>
@@ -373,7 +392,12 @@ struct Worker {
   }
 };
 
-template <class Prog>
+// kLean: the instantiation for launches with no event log, no allocation
+// hook and no list past the window (decided on the host per launch): the
+// general fetch / prepare / retire paths and the event-log bookkeeping are
+// compiled out, which shortens the region's dependent chain and frees
+// registers (more teams per SM).  Results and statistics are identical.
+template <class Prog, bool kLean>
 __global__ void OMPDS_GENERIC_LB
     generic_mode_kernel(const __grid_constant__ TeamParams p,
                         const __grid_constant__ typename Prog::Args a) {
@@ -383,11 +407,11 @@ __global__ void OMPDS_GENERIC_LB
   const int worker_warps = static_cast<int>(team_threads >> 5) - 1;
 
   TeamCtx t = make_team(
-      smem, p.depot_cap, p.prealloc, p.fail_dyn,
+      smem, p.depot_cap, p.prealloc, kLean ? 0 : p.fail_dyn,
       p.slabs ? p.slabs + size_t(blockIdx.x) * p.slab_bytes : nullptr,
       p.slab_bytes,
-      p.events ? p.events + size_t(blockIdx.x) * p.max_events : nullptr,
-      p.max_events, p.list_malloc);
+      !kLean && p.events ? p.events + size_t(blockIdx.x) * p.max_events : nullptr,
+      kLean ? 0 : p.max_events, kLean ? 0 : p.list_malloc);
   // Prologue: zero the team region (Simulator.cpp:286), runtime span last.
   const int64_t region = team_region_bytes(p.depot_cap, p.prealloc);
   for (int64_t i = threadIdx.x; i < region; i += team_threads)
@@ -427,6 +451,13 @@ __global__ void OMPDS_GENERIC_LB
       if (__builtin_expect(fetch_is_fast(st, wm), 1)) {
         fetch_account_fast(t, st, wm); // a staged region, no event log
         f = fetch_from(st);
+      } else if constexpr (kLean) {
+        if (st.phase == kTerminated)
+          break; // termination sentinel (wf == null)
+        if (w.mine) // the master's prepare trapped: nothing is staged
+          t.trap(OMPDS_TRAP_PARALLEL_NOT_STAGED);
+        bar_sync(kBarHandoff, team_threads);
+        continue;
       } else {
         f = fetch_general(t, st, wm, w.mine);
         if (f.fn < 0) {
@@ -445,7 +476,10 @@ __global__ void OMPDS_GENERIC_LB
       OMPDS_TL(rr, 7);
       Prog::region(f.fn, sv, w, a);
       OMPDS_TL(rr, 8);
-      end_parallel_warp(t, plan);
+      if constexpr (kLean)
+        end_parallel_window(t, plan); // every list is the window, no log
+      else
+        end_parallel_warp(t, plan);
       OMPDS_TL(rr, 9);
       bar_sync(kBarHandoff, team_threads); // barrier.parallel (join)
       OMPDS_TL(rr, 10);
@@ -455,6 +489,7 @@ __global__ void OMPDS_GENERIC_LB
     m.t = t;
     m.p = &p;
     m.leader = lane_id() == 0;
+    m.lean = kLean;
     m.join_completes = completes_at_join(t, p.workers);
     m.fast_nargs = t.events == nullptr ? t.prealloc : -1;
     m.team_threads = team_threads;
@@ -579,11 +614,15 @@ inline int32_t validate_launch(const ompds_launch *l) {
 
 inline constexpr uint32_t kSlabBytes = 8192; // per team: args lists + depot overflow
 
+// `n_caps`: the largest nargs any region of the program stages (the fixed
+// configs' capture counts); `allow_lean = false` for programs whose regions
+// are only known at run time (ProgramProg).
 template <class Prog>
 int32_t launch_generic(const ompds_launch *l, const FixedLayout &lay,
                        int32_t n_caps, const typename Prog::Args &args,
                        ompds_team_stats *stats, ompds_event *events,
-                       int64_t warp_slot_bytes = 0, int64_t warp_ovf_bytes = 0) {
+                       int64_t warp_slot_bytes = 0, int64_t warp_ovf_bytes = 0,
+                       bool allow_lean = true) {
   int32_t s = validate_launch(l);
   if (s)
     return s;
@@ -624,7 +663,10 @@ int32_t launch_generic(const ompds_launch *l, const FixedLayout &lay,
     smem = static_cast<size_t>(round_up(int64_t(smem), 16) + worker_warps * p.warp_slot_bytes);
   if (smem > 227 * 1024)
     return OMPDS_ERR_INVALID;
-  auto kern = generic_mode_kernel<Prog>;
+  // the lean instantiation whenever nothing needs the general paths
+  const bool lean = allow_lean && !l->log_events && !l->fail_dynamic_alloc &&
+                    l->list_allocator == OMPDS_LIST_SLAB && n_caps <= l->prealloc_entries;
+  auto kern = lean ? generic_mode_kernel<Prog, true> : generic_mode_kernel<Prog, false>;
   if (smem > 48 * 1024)
     OMPDS_CUDA(cudaFuncSetAttribute(kern,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -436,49 +436,67 @@ template <class T> struct NestedProg {
         *reinterpret_cast<int32_t *>(m.cap(0)) += 1;
     }
   }
-  __device__ static void region(int32_t, const SharedVars &sv, Worker &w,
-                                const Args &a) {
-    const int32_t *cp = static_cast<const int32_t *>(sv.get(0));
-    const T *sp = static_cast<const T *>(sv.get(1));
-    const uint32_t lane = lane_id();
-    // L1: its captured locals live in this warp's stack frame.
-    Frame f1 = w.ds.push(a.l1_bytes, kWarp);
-    Frame f2{};
-    int32_t s1 = OMPDS_OK, s2 = OMPDS_OK;
-    if (f1.status != OMPDS_OK)
-      goto done; // overflow chain exhausted: recorded, region skipped
-    {
-    unsigned char *my1 = f1.base + int64_t(lane) * a.l1_bytes;
+  // L2 (serialized nested region) on its frame `my2` (this lane's f): reads
+  // and writes L1's frame through e / v -- shared, not copied.
+  __device__ static __forceinline__ void level2(unsigned char *my2, int32_t *e, T *v,
+                                                int32_t c, T *dst, bool mine, const Args &a) {
+    T *f = reinterpret_cast<T *>(my2 + a.f_off);
+    *f = T(*e) + v[3];
+    // L3 (serialized nested region)
+    if (mine)
+      *dst = *dst + (*f + T(c));
+    *f = *f * T(2);
+    v[0] = *f;
+    *e = *e + 1;
+  }
+  // L1 on its frame `my1` (this lane's e, v[4]); pushes and pops L2's frame.
+  __device__ static __forceinline__ void level1(unsigned char *my1, Worker &w, int32_t c,
+                                                const T *sp, T *dst, Frame &f2, int32_t &s2,
+                                                const Args &a) {
     int32_t *e = reinterpret_cast<int32_t *>(my1 + a.e_off);
     T *v = reinterpret_cast<T *>(my1 + a.v_off);
-    *e = w.wid + *cp;
+    *e = w.wid + c;
     const T sw = sp[w.wid % 8];
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       v[j] = sw * T(j + 1);
     // L2 (serialized nested region): globalizes f.
     f2 = w.ds.push(a.l2_bytes, kWarp);
-    if (f2.status != OMPDS_OK) {
-      s1 = w.ds.pop(f1);
-      goto done;
-    }
-    {
-    T *f = reinterpret_cast<T *>(f2.base + int64_t(lane) * a.l2_bytes + a.f_off);
-    *f = T(*e) + v[3];
-    // L3 (serialized nested region)
-    T *dst = a.a + size_t(w.team) * w.workers + w.wid;
-    if (w.mine)
-      *dst = *dst + (*f + T(*cp));
-    *f = *f * T(2);
-    v[0] = *f;
-    *e = *e + 1;
+    if (f2.status != OMPDS_OK)
+      return;
+    const uint32_t lane = lane_id();
+    // Frame accesses are issued in the frame's own address space: the slot
+    // pointer derives from the CTA's shared memory (LDS/STS), the chain from
+    // the workspace (LDG/STG) -- two inlined copies of the body, not generic
+    // loads and stores.
+    if (f2.in_smem)
+      level2(w.ds.slot + f2.offset + int64_t(lane) * a.l2_bytes, e, v, c, dst, w.mine, a);
+    else
+      level2(w.ds.ovf + f2.offset + int64_t(lane) * a.l2_bytes, e, v, c, dst, w.mine, a);
     s2 = w.ds.pop(f2);
     if (w.mine)
       *dst = *dst + (v[0] + T(*e));
-    s1 = w.ds.pop(f1);
+  }
+  __device__ static void region(int32_t, const SharedVars &sv, Worker &w,
+                                const Args &a) {
+    const int32_t *cp = static_cast<const int32_t *>(sv.get(0));
+    const T *sp = static_cast<const T *>(sv.get(1));
+    const uint32_t lane = lane_id();
+    // c is shared with the master, which is parked at the join while the
+    // region runs: one load serves the whole region.
+    const int32_t c = *cp;
+    T *dst = a.a + size_t(w.team) * w.workers + w.wid;
+    // L1: its captured locals live in this warp's stack frame.
+    Frame f1 = w.ds.push(a.l1_bytes, kWarp);
+    Frame f2{};
+    int32_t s1 = OMPDS_OK, s2 = OMPDS_OK;
+    if (f1.status == OMPDS_OK) {
+      if (f1.in_smem)
+        level1(w.ds.slot + f1.offset + int64_t(lane) * a.l1_bytes, w, c, sp, dst, f2, s2, a);
+      else
+        level1(w.ds.ovf + f1.offset + int64_t(lane) * a.l1_bytes, w, c, sp, dst, f2, s2, a);
+      s1 = w.ds.pop(f1); // also after a failed L2 push: L1's frame is popped
     }
-    }
-  done:
     __syncwarp();
     // the warp's stack statistics: after its last region, or at a failure
     const int32_t st_any = f1.status | f2.status | s1 | s2;
@@ -1212,7 +1230,8 @@ int32_t ompds_run_program(const ompds_launch *launch, const ompds_program *pr,
   // `host` (pageable) before cudaMemcpyAsync returned, and the next launch's
   // copy into the same workspace buffer is ordered behind this kernel by the
   // stream (ensure_buffer synchronizes the stream before it ever frees it).
-  return launch_generic<ProgramProg>(launch, lay, 0, a, stats, events);
+  return launch_generic<ProgramProg>(launch, lay, 0, a, stats, events, 0, 0,
+                                     /*allow_lean=*/false);
 }
 
 int32_t ompds_run_stream_host(const ompds_launch *launch, int32_t elem,

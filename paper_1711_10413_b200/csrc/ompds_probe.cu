@@ -108,10 +108,9 @@ __device__ __forceinline__ int32_t probe_loop(const ProbeArgs a, unsigned char *
           acc += f[k].offset ^ in_smem;
         else if constexpr (kMode == 5)
           acc += static_cast<int32_t>(k * stride) ^ in_smem;
-        else if (in_smem)
-          acc += touch_shared(base + lane * fb, a.zero, i + acc);
-        else
-          acc += touch_global(base + lane * fb, a.zero, i + acc);
+        else if (lane < static_cast<uint32_t>(a.lanes)) // the frame's lanes only
+          acc += in_smem ? touch_shared(base + lane * fb, a.zero, i + acc)
+                         : touch_global(base + lane * fb, a.zero, i + acc);
       }
     }
 #pragma unroll
@@ -187,10 +186,10 @@ extern "C" int32_t ompds_probe_overheads(ompds_overhead_probe *io, void *stream)
       r.lanes > kWarp)
     return OMPDS_ERR_INVALID;
   const int64_t frame = round_up(int64_t(r.frame_bytes) * r.lanes, 8);
-  if (frame * kProbeMaxDepth > kProbeSlot)
+  if (frame * r.max_depth > kProbeSlot) // the deepest iteration fits the slot
     return OMPDS_ERR_INVALID;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int64_t chain_bytes = frame * kProbeMaxDepth;
+  const int64_t chain_bytes = frame * r.max_depth;
   unsigned char *chain = nullptr;
   long long h[27] = {};
   OMPDS_CUDA(cudaMalloc(&chain, round_up(chain_bytes, 256) + sizeof h));
