@@ -423,7 +423,7 @@ def main():
                                                           rank, world)
     configs = other_configs(RG, dev, stream, sms) if rank == 0 and not args.only_stream \
         else {}
-    regs = ptxas_regs("StreamProgIdE") or 64
+    regs = ptxas_regs("StreamProgIdEELb1E") or 64
     thr = ((workers + 31) // 32) * 32 + 32
     occ = OCC.occupancy_for("b200", smem_bytes, regs, thr)
 
@@ -544,7 +544,7 @@ def regions_section(RG, torch, dist, dev, stream, sms, rank, world):
     # launches teams [r*T, (r+1)*T) of the N*T grid (first_team/total_teams),
     # the whole-job rate is N*T*R2 over the slowest rank's time.
     from paper_1711_10413_b200 import occupancy as OCC
-    per_sm1 = OCC.occupancy_for("b200", 265, ptxas_regs("RegionsProgIdE") or 52, 64).actual
+    per_sm1 = OCC.occupancy_for("b200", 265, ptxas_regs("RegionsProgIdEELb1E") or 52, 64).actual
     R2, teams2 = 2000, sms * per_sm1
     a2 = torch.zeros(world * teams2 * 32, dtype=torch.float64, device=dev)
     rng = dict(first_team=rank * teams2, total_teams=world * teams2)
@@ -595,7 +595,7 @@ def regions_section(RG, torch, dist, dev, stream, sms, rank, world):
             "sm_clock_mhz_around": [clk_before, clk_after],
             "smem_bytes_per_cta": smem1,
             "teams_per_sm": per_sm1,
-            "regs_per_thread": ptxas_regs("RegionsProgIdE"),
+            "regs_per_thread": ptxas_regs("RegionsProgIdEELb1E"),
             "workload": "config 1: 1 team x 32 workers, 4 shared scalars (2 int, 2 double), "
                         f"{R} regions in a sequential loop",
             "aggregate_regions_per_s": round(agg_regions_per_s, 0),
@@ -690,7 +690,7 @@ def other_configs(RG, dev, stream, sms):
                   f"CUDA events; ms_queued: {K} x [L2 evict; region] minus {K} x [L2 evict], "
                   "queued back to back (ncu's kernel duration: 42.6-43.2 us)",
         "smem_bytes_per_cta": st.smem_bytes, "depot_in_smem": st.depot_in_smem,
-        "regs_per_thread": ptxas_regs("SharedArrayProgIdE"),
+        "regs_per_thread": ptxas_regs("SharedArrayProgIdEELb1E"),
         "staging": "cp.async.bulk (TMA) of d[256] into the depot slot",
         "roofline_frac": None,
         "l2": "evicted before every launch by reading a 256 MB buffer"}
@@ -714,7 +714,7 @@ def other_configs(RG, dev, stream, sms):
                     "frames_in_smem": stacks[0][0].frame_in_smem,
                     "warp_slot_bytes": slot,
                     "smem_bytes_per_cta": o3.team_stats()[0].smem_bytes,
-                    "regs_per_thread": ptxas_regs("NestedProgIdE")}
+                    "regs_per_thread": ptxas_regs("NestedProgIdEELb1E")}
     return out
 
 

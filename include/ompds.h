@@ -274,6 +274,57 @@ int32_t ompds_layout_build(const ompds_frame_var *vars, int32_t n_vars,
                            ompds_depot_slot *slots, int32_t max_slots,
                            int32_t *owners, int32_t max_owners);
 
+/* ------------------------------------------------------------------------ */
+/* Manifest JSON: the descriptor export of the reference compiler           */
+/* (Compiler.cpp:112-155 manifestJson: nlohmann dump(2) + "\n").           */
+/* ------------------------------------------------------------------------ */
+typedef struct ompds_manifest {
+  const char *kernel;               /* kernel function name ("" when none)  */
+  int32_t teams;                    /* LaunchDefaults (IR.h:260-266)        */
+  int32_t workers;
+  int32_t prealloc_entries;
+  int32_t has_layout;               /* 0: no kernel layout (empty depot)    */
+  const ompds_depot_layout *layout; /* the kernel frame group's layout      */
+  const ompds_depot_slot *slots;    /* the slots array of ompds_layout_build */
+  const int32_t *owners;            /* its owners array (var indices)       */
+  const char *const *var_names;     /* name of every var index              */
+} ompds_manifest;
+
+/* Writes the manifest text, byte-identical to the reference's, and a NUL.
+ * *len = text length without the NUL; OMPDS_ERR_CAPACITY (with *len set)
+ * when cap <= *len. */
+int32_t ompds_manifest_write(const ompds_manifest *m, char *out, int64_t cap, int64_t *len);
+
+typedef struct ompds_manifest_info {
+  int64_t kernel;           /* offset of the kernel name in `names`         */
+  int32_t teams;
+  int32_t workers;
+  int64_t total_local;
+  int64_t total_shared;
+  int32_t mirrored;
+  int32_t prealloc_entries;
+  int64_t stack_bytes;
+  int64_t prealloc_bytes;
+  int64_t runtime_bytes;
+  int64_t shared_footprint;
+  int32_t n_slots;
+  int32_t n_owners;
+} ompds_manifest_info;
+
+/* Parses manifest JSON (any whitespace / key order).  Slots go to `slots`
+ * (owner_begin / n_owners index `owner_names`, whose entries are offsets of
+ * NUL-terminated names in `names`).  OMPDS_ERR_INVALID for malformed JSON,
+ * a missing or mistyped field, or a manifest that breaks the reference's
+ * laws: offsets are the prefix sums of the sizes, total_local = total_shared
+ * = stack_bytes = the sum of the sizes, prealloc_bytes = 8 x
+ * prealloc_entries, runtime_bytes = 49, shared_footprint = total_shared +
+ * prealloc_bytes + runtime_bytes.  OMPDS_ERR_CAPACITY when an output array
+ * is too small (info still filled). */
+int32_t ompds_manifest_parse(const char *text, int64_t len, ompds_manifest_info *info,
+                             ompds_depot_slot *slots, int32_t max_slots,
+                             int64_t *owner_names, int32_t max_owners, char *names,
+                             int64_t names_cap);
+
 /* Per-team shared footprint: depot + prealloc window + runtime span
  * (Simulator.cpp:281-284, Occupancy.h:49-51). */
 int64_t ompds_shared_footprint(int64_t total_shared, int32_t prealloc_entries);

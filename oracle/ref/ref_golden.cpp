@@ -245,6 +245,8 @@ static json programJson(const std::string &Src, const std::string &Stem,
   J["layouts"] = layoutsJson(C.Machine);
   J["frame_vars"] = frameVarsJson(C.PostCodegen);
   J["manifest"] = json::parse(manifestJson(C.Machine, DefaultPreallocEntries));
+  // the exact text (dump(2) + "\n") the reference writes, for byte-level parity
+  J["manifest_text"] = manifestJson(C.Machine, DefaultPreallocEntries);
   {
     auto Det = detectSharedVariables(C.PostCodegen);
     json D = json::object();

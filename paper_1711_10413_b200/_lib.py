@@ -101,6 +101,22 @@ class Launch(C.Structure):
                 ("total_teams", C.c_int32), ("reserved0", C.c_int32)]
 
 
+class Manifest(C.Structure):
+    _fields_ = [("kernel", C.c_char_p), ("teams", C.c_int32), ("workers", C.c_int32),
+                ("prealloc_entries", C.c_int32), ("has_layout", C.c_int32),
+                ("layout", C.POINTER(DepotLayout)), ("slots", C.POINTER(DepotSlot)),
+                ("owners", C.POINTER(C.c_int32)), ("var_names", C.POINTER(C.c_char_p))]
+
+
+class ManifestInfo(C.Structure):
+    _fields_ = [("kernel", C.c_int64), ("teams", C.c_int32), ("workers", C.c_int32),
+                ("total_local", C.c_int64), ("total_shared", C.c_int64),
+                ("mirrored", C.c_int32), ("prealloc_entries", C.c_int32),
+                ("stack_bytes", C.c_int64), ("prealloc_bytes", C.c_int64),
+                ("runtime_bytes", C.c_int64), ("shared_footprint", C.c_int64),
+                ("n_slots", C.c_int32), ("n_owners", C.c_int32)]
+
+
 class OverheadProbe(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("frame_bytes", C.c_int32), ("lanes", C.c_int32),
                 ("max_depth", C.c_int32), ("seed", C.c_uint32), ("reserved0", C.c_int32),
@@ -176,6 +192,12 @@ _SIGS = {
                                         C.POINTER(DepotLayout), C.POINTER(DepotSlot), C.c_int32,
                                         C.POINTER(C.c_int32), C.c_int32]),
     "ompds_shared_footprint": (C.c_int64, [C.c_int64, C.c_int32]),
+    "ompds_manifest_write": (C.c_int32, [C.POINTER(Manifest), C.c_char_p, C.c_int64,
+                                          C.POINTER(C.c_int64)]),
+    "ompds_manifest_parse": (C.c_int32, [C.c_char_p, C.c_int64, C.POINTER(ManifestInfo),
+                                          C.POINTER(DepotSlot), C.c_int32,
+                                          C.POINTER(C.c_int64), C.c_int32, C.c_char_p,
+                                          C.c_int64]),
     "ompds_gpu_spec_get": (C.c_int32, [C.c_char_p, C.POINTER(GpuSpec)]),
     "ompds_occupancy_for": (C.c_int32, [C.POINTER(GpuSpec), C.c_int64, C.c_int32, C.c_int32,
                                          C.POINTER(Occupancy)]),

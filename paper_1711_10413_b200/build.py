@@ -17,7 +17,8 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_build")
 LIB = os.path.join(OUT_DIR, "libompds_b200.so")
 SOURCES = [os.path.join(CSRC, "ompds_kernels.cu"), os.path.join(CSRC, "ompds_team.cu"),
-           os.path.join(CSRC, "ompds_probe.cu"), os.path.join(CSRC, "ompds_host.cpp")]
+           os.path.join(CSRC, "ompds_probe.cu"), os.path.join(CSRC, "ompds_host.cpp"),
+           os.path.join(CSRC, "ompds_manifest.cpp")]
 HEADERS = [os.path.join(CSRC, "ompds_device.cuh"), os.path.join(CSRC, "ompds_generic.cuh"),
            os.path.join(os.path.dirname(HERE), "include", "ompds.h")]
 

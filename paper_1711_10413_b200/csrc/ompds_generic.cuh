@@ -255,7 +255,9 @@ struct Master {
   // protocol violation gets here (the launcher chose lean because no region
   // needs more than the window and nothing is logged).  The trap is recorded
   // and the handoff still runs, so the workers see an unstaged region.
-  __device__ __noinline__ int32_t parallel_refused(int32_t s) {
+  // (Inlined: a call would take the Master's address and move the whole
+  // object to local memory for every region.)
+  __device__ __forceinline__ int32_t parallel_refused(int32_t s) {
     if (s == OMPDS_OK)
       s = OMPDS_ERR_INVALID;
     sync_status(s);

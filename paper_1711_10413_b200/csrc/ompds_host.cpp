@@ -47,29 +47,6 @@ struct Slot {
   std::vector<int32_t> owners; // var indices; empty = dropped by repacking
 };
 
-// Coloring liveness of one slot, in doubled coordinates (see ompds.h).
-struct Live {
-  int64_t first = -1, last = -1;
-  bool pinned = false;
-  bool empty() const { return first < 0; }
-  bool disjoint(const Live &o) const {
-    if (empty() || o.empty())
-      return true;
-    return last < o.first || o.last < first;
-  }
-  void merge(const Live &o) {
-    if (o.empty())
-      return;
-    if (empty()) {
-      first = o.first;
-      last = o.last;
-      return;
-    }
-    first = std::min(first, o.first);
-    last = std::max(last, o.last);
-  }
-};
-
 struct Group {
   std::vector<Slot> slots;
   std::vector<int32_t> slot_var; // slot -> defining var
@@ -85,59 +62,72 @@ void lowerShared(Group &g, const ompds_frame_var *vars) {
         s.shared = true;
 }
 
-// color-stack (LoweringPasses.cpp:458-538), per member function.
+// color-stack (LoweringPasses.cpp:458-538), per member function, restated
+// as first-fit interval packing.  Each candidate slot (local, unpinned, with
+// a live interval) is visited in slot order and joins the earliest packing
+// group -- led by an earlier candidate -- whose hull (the span from the
+// first to the last use of everything packed into it so far) it does not
+// touch; otherwise it starts a group of its own.  Packing a slot into a
+// group keeps the larger size and alignment and widens the group's hull.
+// This is the reference's leader-by-leader scan seen from the other side:
+// when slot b is visited, every earlier leader's hull holds exactly the
+// slots before b that the reference would have merged into it by then, and
+// b lands in the first leader that the reference's scan would give it to.
+// Slots with no use are left alone (repacking drops the empty ones).
 void colorStack(Group &g, const ompds_frame_var *vars) {
-  // Member functions present in this group, in first-appearance order.
-  std::vector<int32_t> funcs;
+  struct Span {
+    int64_t lo, hi; // doubled positions, inclusive
+  };
+  struct Packing {
+    int32_t leader; // slot receiving the packed owners
+    Span hull;
+  };
+  std::vector<int32_t> funcs; // member functions, first-appearance order
   for (int32_t v : g.slot_var)
     if (std::find(funcs.begin(), funcs.end(), vars[v].func) == funcs.end())
       funcs.push_back(vars[v].func);
-  for (int32_t f : funcs) {
-    std::vector<int32_t> ids; // slots whose frame index lives in f
-    for (size_t s = 0; s < g.slot_var.size(); ++s)
-      if (vars[g.slot_var[s]].func == f)
-        ids.push_back(static_cast<int32_t>(s));
-    if (ids.size() < 2)
-      continue; // SlotOfValue.size() < 2
-    std::vector<Live> live(g.slots.size());
-    for (int32_t s : ids) {
-      const ompds_frame_var &v = vars[g.slot_var[s]];
-      Live &l = live[s];
-      if (v.flags & OMPDS_VAR_ESCAPES) {
-        // The only direct use left is the cast right after the alloca.
-        if (v.def_pos >= 0)
-          l.first = l.last = 2 * int64_t(v.def_pos) + 1;
-      } else if (v.live_first >= 0) {
-        l.first = 2 * int64_t(v.live_first);
-        l.last = 2 * int64_t(v.live_last);
-        l.pinned = (v.flags & OMPDS_VAR_PINNED) != 0;
-      } else {
-        l.pinned = (v.flags & OMPDS_VAR_PINNED) != 0;
-      }
-    }
-    auto mergeable = [&](int32_t s) {
-      return !g.slots[s].shared && !live[s].pinned && !g.slots[s].owners.empty();
-    };
-    for (size_t a = 0; a < ids.size(); ++a) {
-      const int32_t sa = ids[a];
-      if (!mergeable(sa))
+  for (int32_t fn : funcs) {
+    int32_t in_func = 0;
+    for (int32_t v : g.slot_var)
+      in_func += vars[v].func == fn;
+    if (in_func < 2)
+      continue; // a single frame index: nothing to color (SlotOfValue.size() < 2)
+    std::vector<Packing> packs;
+    for (size_t si = 0; si < g.slot_var.size(); ++si) {
+      const ompds_frame_var &v = vars[g.slot_var[si]];
+      Slot &slot = g.slots[si];
+      if (v.func != fn || slot.shared)
         continue;
-      for (size_t b = a + 1; b < ids.size(); ++b) {
-        const int32_t sb = ids[b];
-        if (g.slots[sb].owners.empty() || !mergeable(sb))
-          continue;
-        if (live[sb].empty() || live[sa].empty())
-          continue; // dead slots are dropped by repacking, not merged
-        if (!live[sa].disjoint(live[sb]))
-          continue;
-        Slot &dst = g.slots[sa];
-        Slot &src = g.slots[sb];
-        dst.size = std::max(dst.size, src.size);
-        dst.align = std::max(dst.align, src.align);
-        dst.owners.insert(dst.owners.end(), src.owners.begin(), src.owners.end());
-        src.owners.clear();
-        live[sa].merge(live[sb]);
+      // the span of the frame value's uses; an escaping alloca's only direct
+      // use is the address-space cast right after it (doubled 2*def+1)
+      Span use{-1, -1};
+      bool pinned = false;
+      if (v.flags & OMPDS_VAR_ESCAPES) {
+        if (v.def_pos >= 0)
+          use = {2 * int64_t(v.def_pos) + 1, 2 * int64_t(v.def_pos) + 1};
+      } else {
+        pinned = (v.flags & OMPDS_VAR_PINNED) != 0;
+        if (v.live_first >= 0)
+          use = {2 * int64_t(v.live_first), 2 * int64_t(v.live_last)};
       }
+      if (pinned || use.lo < 0)
+        continue; // never packed, never a leader
+      Packing *home = nullptr;
+      for (Packing &pk : packs)
+        if (use.hi < pk.hull.lo || pk.hull.hi < use.lo) {
+          home = &pk;
+          break;
+        }
+      if (!home) {
+        packs.push_back({static_cast<int32_t>(si), use});
+        continue;
+      }
+      Slot &lead = g.slots[static_cast<size_t>(home->leader)];
+      lead.size = std::max(lead.size, slot.size);
+      lead.align = std::max(lead.align, slot.align);
+      lead.owners.insert(lead.owners.end(), slot.owners.begin(), slot.owners.end());
+      slot.owners.clear();
+      home->hull = {std::min(home->hull.lo, use.lo), std::max(home->hull.hi, use.hi)};
     }
   }
 }

@@ -168,6 +168,84 @@ def parse_frame_blocks(text: str):
     return out
 
 
+@dataclass
+class Manifest:  # Compiler.cpp:112-155
+    kernel: str
+    teams: int
+    workers: int
+    depot: DepotLayout
+    prealloc_entries: int
+    prealloc_bytes: int
+    runtime_bytes: int
+    shared_footprint: int
+    stack_bytes: int
+
+
+def manifest_text(vars_: Sequence[FrameVar], n_groups: int, kernel: str, teams: int,
+                  workers: int, pipeline: str = "default",
+                  prealloc_entries: int = L.DEFAULT_PREALLOC_ENTRIES,
+                  kernel_group: int = 0) -> str:
+    """The reference compiler's manifest JSON (``manifestJson``, byte for
+    byte) for the kernel frame group of ``vars_``, via the C ABI's frame
+    pipeline and ``ompds_manifest_write``."""
+    lib = L.lib()
+    n = len(vars_)
+    arr = (L.FrameVar * max(n, 1))()
+    for i, v in enumerate(vars_):
+        flags = (L.VAR_ESCAPES if v.escapes else 0) | (L.VAR_PINNED if v.pinned else 0)
+        arr[i] = L.FrameVar(v.group, v.func, flags, v.def_pos, v.bytes, v.first, v.last)
+    lays = (L.DepotLayout * max(n_groups, 1))()
+    slots = (L.DepotSlot * max(n, 1))()
+    owners = (C.c_int32 * max(n, 1))()
+    L.check(lib.ompds_layout_build(arr, n, n_groups, PIPELINES[pipeline], lays, slots, max(n, 1),
+                                   owners, max(n, 1)), "ompds_layout_build")
+    names = (C.c_char_p * max(n, 1))(*[v.name.encode() for v in vars_])
+    has = 0 <= kernel_group < n_groups
+    m = L.Manifest(kernel.encode(), teams, workers, prealloc_entries, 1 if has else 0,
+                   C.pointer(lays[kernel_group]) if has else None, slots, owners, names)
+    size = C.c_int64()
+    buf = C.create_string_buffer(4096)
+    rc = lib.ompds_manifest_write(C.byref(m), buf, len(buf), C.byref(size))
+    if rc == L.ERR_CAPACITY:
+        buf = C.create_string_buffer(size.value + 1)
+        rc = lib.ompds_manifest_write(C.byref(m), buf, len(buf), C.byref(size))
+    L.check(rc, "ompds_manifest_write")
+    return buf.raw[:size.value].decode()
+
+
+def parse_manifest(text: str) -> Manifest:
+    """Reads manifest JSON back (``ompds_manifest_parse``: any key order and
+    whitespace; the reference's size laws are checked)."""
+    lib = L.lib()
+    raw = text.encode()
+    info = L.ManifestInfo()
+    cap_s, cap_o, cap_n = 64, 256, 1 << 14
+    for _ in range(2):
+        slots = (L.DepotSlot * cap_s)()
+        onames = (C.c_int64 * cap_o)()
+        names = C.create_string_buffer(cap_n)
+        rc = lib.ompds_manifest_parse(raw, len(raw), C.byref(info), slots, cap_s, onames, cap_o,
+                                      names, cap_n)
+        if rc != L.ERR_CAPACITY:
+            break
+        cap_s, cap_o, cap_n = max(info.n_slots, 1), max(info.n_owners, 1), len(raw) + 1
+    L.check(rc, "ompds_manifest_parse")
+
+    def name_at(off):
+        end = names.raw.index(b"\0", off)
+        return names.raw[off:end].decode()
+    ss = []
+    for k in range(info.n_slots):
+        s = slots[k]
+        ss.append(DepotSlot(s.offset, s.size, s.align, bool(s.shared),
+                            [name_at(onames[j]) for j in range(s.owner_begin,
+                                                               s.owner_begin + s.n_owners)]))
+    depot = DepotLayout(ss, info.total_local, info.total_shared, bool(info.mirrored))
+    return Manifest(name_at(info.kernel), info.teams, info.workers, depot, info.prealloc_entries,
+                    info.prealloc_bytes, info.runtime_bytes, info.shared_footprint,
+                    info.stack_bytes)
+
+
 def manifest_depot(lay: DepotLayout, prealloc_entries: int = L.DEFAULT_PREALLOC_ENTRIES) -> dict:
     """The depot part of the reference manifest (Compiler.cpp:112-155)."""
     return {
