@@ -400,6 +400,13 @@ typedef struct ompds_launch {
                                sharded across GPUs by range             */
   int32_t total_teams;
   int32_t reserved0;        /* must be 0                                  */
+  int32_t *barrier_arrivals; /* optional (NULL = off), device, teams x (W+32):
+                               for every thread of the reference's team
+                               (workers 0..W-1, the master W, the reserved
+                               warp's idle lanes W+1..W+31) the hardware
+                               barrier arrivals of the lane that plays it
+                               (SimStats::BarrierEntries, Simulator.h:42-55;
+                               see DESIGN.md for the idle lanes)          */
 } ompds_launch;
 
 #define OMPDS_LIST_SLAB 0

@@ -131,6 +131,8 @@ static json simJson(const Module &M, const SimOptions &O, bool WithEvents) {
                      ? 0
                      : R.Stats.BarrierEntries[T][0]);
   J["worker0_barrier_entries"] = Wb;
+  // SimStats::BarrierEntries[team][launched tid], every thread of every team
+  J["barrier_entries"] = R.Stats.BarrierEntries;
   J["dynamic_alloc_bytes"] = R.Stats.DynamicAllocBytes;
   J["dynamic_allocs"] = R.Stats.DynamicAllocs;
   J["dynamic_frees"] = R.Stats.DynamicFrees;

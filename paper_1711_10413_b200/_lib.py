@@ -98,7 +98,8 @@ class Launch(C.Structure):
                 ("fail_dynamic_alloc", C.c_int32), ("depot_capacity", C.c_int64),
                 ("log_events", C.c_int32), ("max_events", C.c_int32), ("stream", C.c_void_p),
                 ("list_allocator", C.c_int32), ("first_team", C.c_int32),
-                ("total_teams", C.c_int32), ("reserved0", C.c_int32)]
+                ("total_teams", C.c_int32), ("reserved0", C.c_int32),
+                ("barrier_arrivals", C.c_void_p)]
 
 
 class Manifest(C.Structure):

@@ -93,6 +93,7 @@ struct TeamParams {
   int32_t list_malloc;           // OMPDS_LIST_MALLOC
   int32_t first_team;            // omp_get_team_num() of CTA 0
   int32_t total_teams;           // omp_get_num_teams()
+  int32_t *bar_arrivals;         // teams x (W+32) per-thread barrier arrivals, or null
 };
 
 // Depot accessors for the master's sequential code (see Master::with_depot).
@@ -146,7 +147,7 @@ struct Master {
                        // window size without an event log, -1 with one
   uint32_t team_threads;
   int32_t trap = 0;
-  int32_t barriers = 0;
+  int32_t barriers = 0;  // protocol barriers of the master (2 per region)
   int32_t regions = 0;
   DsStack ds;
   Frame depot;
@@ -344,6 +345,14 @@ struct Master {
     if (leader)
       s = kernel_deinit(t, kMaster);
     sync_status(s);
+    // SimStats::BarrierEntries for the reserved warp: the master (logical tid
+    // W, lane 0) and the idle lanes (W+1.., lanes 1..31) each made this
+    // lane's handoff arrivals -- the protocol's `barriers` plus the
+    // termination release -- and no other barrier (they never reach a
+    // region's `omp barrier`, id 2).
+    if (p->bar_arrivals)
+      p->bar_arrivals[size_t(blockIdx.x) * (p->workers + kWarp) + p->workers + lane_id()] =
+          barriers + 1;
     if (leader && p->stats) {
       ompds_team_stats st{};
       st.trap = trap ? trap : t.at<int32_t>(Rt::kTrap);
@@ -389,8 +398,11 @@ struct Worker {
   // `#pragma omp barrier` inside the region: every worker of the team (the
   // master warp is parked at the join and does not take part); all lanes of
   // every worker warp must arrive, padding lanes included.
+  int32_t *arrivals;        // this lane's barrier arrival counter (or null)
   __device__ __forceinline__ void barrier() const {
     bar_sync(kBarRegion, worker_threads);
+    if (arrivals)
+      ++*arrivals;
   }
 };
 
@@ -445,8 +457,14 @@ __global__ void OMPDS_GENERIC_LB
                    : nullptr;
     w.ds.init(slot, p.warp_slot_bytes, ovf, p.warp_ovf ? p.warp_ovf_bytes : 0);
     const WarpMask wm = WarpMask::of(t, w.mine); // loop-invariant participation
+    // barrier arrivals of this lane (SimStats::BarrierEntries), counted only
+    // by the general instantiation when the launch asks for them
+    int32_t arrivals = 0;
+    const bool count = !kLean && p.bar_arrivals != nullptr;
+    w.arrivals = count ? &arrivals : nullptr;
     for (int32_t rr = 0;; ++rr) {
       bar_sync(kBarHandoff, team_threads); // await.work
+      arrivals += count;
       OMPDS_TL(rr, 5);
       const StagedState st = load_staged_state(t, wm.win_off);
       Fetch f;
@@ -466,6 +484,7 @@ __global__ void OMPDS_GENERIC_LB
           if (f.status == OMPDS_OK)
             break; // termination sentinel (wf == null)
           bar_sync(kBarHandoff, team_threads); // trapped fetch: skip the region
+          arrivals += count;
           continue;
         }
       }
@@ -484,8 +503,11 @@ __global__ void OMPDS_GENERIC_LB
         end_parallel_warp(t, plan);
       OMPDS_TL(rr, 9);
       bar_sync(kBarHandoff, team_threads); // barrier.parallel (join)
+      arrivals += count;
       OMPDS_TL(rr, 10);
     }
+    if (count && w.mine) // worker threads of the reference's team (tid < W)
+      p.bar_arrivals[size_t(blockIdx.x) * (p.workers + kWarp) + w.wid] = arrivals;
   } else {
     Master m;
     m.t = t;
@@ -639,6 +661,7 @@ int32_t launch_generic(const ompds_launch *l, const FixedLayout &lay,
   p.events = l->log_events ? events : nullptr;
   p.list_malloc = l->list_allocator == OMPDS_LIST_MALLOC;
   p.first_team = l->first_team;
+  p.bar_arrivals = l->barrier_arrivals;
   p.total_teams = l->total_teams > 0 ? l->total_teams : l->teams;
   p.stats = stats;
   p.n_caps = n_caps;
@@ -667,6 +690,7 @@ int32_t launch_generic(const ompds_launch *l, const FixedLayout &lay,
     return OMPDS_ERR_INVALID;
   // the lean instantiation whenever nothing needs the general paths
   const bool lean = allow_lean && !l->log_events && !l->fail_dynamic_alloc &&
+                    l->barrier_arrivals == nullptr &&
                     l->list_allocator == OMPDS_LIST_SLAB && n_caps <= l->prealloc_entries;
   auto kern = lean ? generic_mode_kernel<Prog, true> : generic_mode_kernel<Prog, false>;
   if (smem > 48 * 1024)

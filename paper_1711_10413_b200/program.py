@@ -358,7 +358,7 @@ def run_program(prog: Program, buffers, prealloc_entries: int = L.DEFAULT_PREALL
                 fail_dynamic_alloc: bool = False, depot_capacity: int = -1,
                 max_events: int = 0, stream=None, list_allocator: int = L.LIST_SLAB,
                 first_team: int = 0, total_teams: int = 0, teams: int = 0,
-                step_limit: int = 0):
+                step_limit: int = 0, barrier_arrivals=None):
     """Launches the program: `buffers` are int32 CUDA tensors, one per mapped
     array, in host declaration order.  Returns regions.Outputs."""
     import torch
@@ -372,7 +372,8 @@ def run_program(prog: Program, buffers, prealloc_entries: int = L.DEFAULT_PREALL
     out = RG.Outputs(teams or prog.teams, buffers[0].device if buffers else "cuda", max_events)
     launch = RG.make_launch(teams or prog.teams, prog.workers, prealloc_entries,
                             fail_dynamic_alloc, depot_capacity, max_events > 0, max_events,
-                            stream, list_allocator, first_team, total_teams)
+                            stream, list_allocator, first_team, total_teams,
+                            barrier_arrivals)
     L.check(L.lib().ompds_run_program(C.byref(launch), C.byref(desc), out.stats_ptr(),
                                       out.events_ptr()), "ompds_run_program")
     out.used_on(stream)

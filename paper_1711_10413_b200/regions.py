@@ -53,15 +53,23 @@ def make_launch(teams: int, workers: int, prealloc_entries: int = L.DEFAULT_PREA
                 log_events: bool = False, max_events: int = 0,
                 stream: Optional[torch.cuda.Stream] = None,
                 list_allocator: int = L.LIST_SLAB, first_team: int = 0,
-                total_teams: int = 0) -> L.Launch:
+                total_teams: int = 0,
+                barrier_arrivals: Optional[torch.Tensor] = None) -> L.Launch:
     cur = torch.cuda.current_stream()
     if stream is not None and stream.cuda_stream != cur.cuda_stream:
         # outputs/inputs prepared on the current stream must be ready first
         stream.wait_stream(cur)
     s = stream.cuda_stream if stream is not None else cur.cuda_stream
+    if barrier_arrivals is not None:
+        _require_cuda(barrier_arrivals)
+        if barrier_arrivals.dtype != torch.int32 or \
+                barrier_arrivals.numel() < teams * (workers + L.RESERVED_WARP):
+            raise ValueError("barrier_arrivals: int32, teams x (workers + 32)")
     return L.Launch(teams, workers, prealloc_entries, 1 if fail_dynamic_alloc else 0,
                     depot_capacity, 1 if log_events else 0, max_events if log_events else 0,
-                    C.c_void_p(s), list_allocator, first_team, total_teams, 0)
+                    C.c_void_p(s), list_allocator, first_team, total_teams, 0,
+                    C.c_void_p(barrier_arrivals.data_ptr()) if barrier_arrivals is not None
+                    else None)
 
 
 def _used_on(stream: Optional[torch.cuda.Stream], *ts) -> None:

@@ -42,7 +42,7 @@ def test_struct_sizes_match_the_c_abi():
     assert C.sizeof(P.FrameVar) == 32
     assert C.sizeof(P.DepotSlot) == 32
     assert C.sizeof(P.DepotLayout) == 32
-    assert C.sizeof(P.Launch) == 56
+    assert C.sizeof(P.Launch) == 64
     assert C.sizeof(P.TeamStats) == 56
     assert C.sizeof(P.OverheadProbe) == 96
 
@@ -220,7 +220,7 @@ def test_team_range_outside_the_grid_is_rejected(first, teams, total):
     """ompds_launch.first_team/total_teams (team-range sharding) are validated
     before anything touches a GPU."""
     import ctypes as C
-    launch = P.Launch(teams, 32, 20, 0, -1, 0, 0, None, 0, first, total, 0)
+    launch = P.Launch(teams, 32, 20, 0, -1, 0, 0, None, 0, first, total, 0, None)
     rc = P.lib().ompds_run_regions(C.byref(launch), 0, 1, C.c_void_p(16), None, None)
     assert rc == P.ERR_INVALID
 
@@ -263,7 +263,7 @@ def test_element_misaligned_pointers_are_rejected_before_a_gpu():
     """16-byte-unaligned views are served (element-wise variant); pointers
     not aligned to the element itself are invalid."""
     import ctypes as C
-    launch = P.Launch(2, 32, 20, 0, -1, 0, 0, None, 0, 0, 0, 0)
+    launch = P.Launch(2, 32, 20, 0, -1, 0, 0, None, 0, 0, 0, 0, None)
     coef = (C.c_double * 8)()
     rc = P.lib().ompds_run_stream(C.byref(launch), 1, 10, C.c_void_p(4100), C.c_void_p(8192),
                                   coef, None, None)

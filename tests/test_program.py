@@ -251,7 +251,7 @@ def test_verifier_rejects_malformed_programs():
     # the same descriptor is refused by ompds_run_program before the launch
     import ctypes as C
     desc, _keep = PG.describe(_mutants(prog)[0][1], [16])
-    launch = L.Launch(1, 32, 20, 0, -1, 0, 0, None, 0, 0, 0, 0)
+    launch = L.Launch(1, 32, 20, 0, -1, 0, 0, None, 0, 0, 0, 0, None)
     assert L.lib().ompds_run_program(C.byref(launch), C.byref(desc), None, None) == L.ERR_INVALID
 
 
@@ -297,6 +297,44 @@ def test_gpu_runs_reference_programs_bit_exact():
             assert sum(s.dynamic_alloc_bytes for s in st) == sim["dynamic_alloc_bytes"]
             assert sum(s.dynamic_allocs for s in st) == sim["dynamic_allocs"]
             assert sum(s.dynamic_frees for s in st) == sim["dynamic_frees"]
+            n += 1
+    assert n > 150
+
+
+@pytest.mark.gpu
+def test_gpu_per_thread_barrier_entries_match_the_simulator():
+    """SimStats::BarrierEntries (Simulator.h:42-55) for every thread of every
+    team of every reference program: each worker's handoff arrivals equal
+    the simulator's per-thread count (2R+1), the master's protocol barriers
+    equal its entries (2R; on the GPU it adds the explicit termination
+    release that stands in for the simulator's master exit,
+    Simulator.cpp:475-478), and the reserved warp's idle lanes -- which the
+    simulator never lets enter a barrier (SimulatorTests.cpp:85-93) -- arrive
+    only at the master's handoff barriers, in lockstep with it, never at one
+    of their own (hardware barriers count every lane of a warp that is
+    resident: DESIGN.md §2)."""
+    import torch
+    n = 0
+    for p in programs():
+        for t, w, run in launches(p):
+            sim = run["sim"]
+            ref = sim.get("barrier_entries")
+            assert ref and len(ref) == t, p["stem"]
+            prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], t, w)
+            bufs = [torch.full((sz,), init, dtype=torch.int32, device="cuda")
+                    for _, sz, init in prog.buffers]
+            arr = torch.full((t * (w + 32),), -1, dtype=torch.int32, device="cuda")
+            out = PG.run_program(prog, bufs, barrier_arrivals=arr)
+            got = arr.view(t, w + 32).cpu().tolist()
+            st = out.team_stats()
+            for team in range(t):
+                r, g = ref[team], got[team]
+                assert len(r) == w + 32
+                assert g[:w] == r[:w], (p["stem"], t, w, team)           # workers
+                assert st[team].master_barriers == r[w]                   # master protocol
+                assert g[w] == r[w] + 1                                   # + termination
+                assert r[w + 1:] == [0] * 31                              # reference idle
+                assert g[w + 1:] == [g[w]] * 31, (p["stem"], team)        # shadow the master
             n += 1
     assert n > 150
 
