@@ -345,7 +345,11 @@ typedef struct ompds_gpu_spec { /* GpuSpec Occupancy.h:24-31 */
                                       B200 (256 per warp, as ncu's
                                       occupancy_limit_registers counts);
                                       0 = exact (the reference model)     */
-  int32_t reserved0;
+  int32_t reg_partitions;          /* the register file is split evenly over
+                                      this many SM sub-partitions and a warp
+                                      takes all its registers from one: 4 on
+                                      B200 (16K registers per SMSP); 0 = one
+                                      pool (the reference model)           */
 } ompds_gpu_spec;
 
 typedef struct ompds_occupancy { /* OccupancyResult Occupancy.h:62-68 */

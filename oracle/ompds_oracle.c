@@ -333,15 +333,22 @@ int32_t orc_layout_build(const ompds_frame_var *vars, int32_t n_vars,
 
 static int64_t mn(int64_t a, int64_t b) { return a < b ? a : b; }
 
+/* Occupancy.cpp:77-88; B200 row (EXTENSION): registers per warp in
+ * allocation units, each warp inside one register sub-partition. */
+static int64_t o_teams_by_regs(const ompds_gpu_spec *g, int32_t regs, int32_t threads) {
+  if (regs <= 0 || threads <= 0) return 0;
+  if (g->reg_alloc_unit <= 0) return g->registers_per_sm / ((int64_t)regs * threads);
+  int64_t u = g->reg_alloc_unit;
+  int64_t warp_regs = (((int64_t)regs + u - 1) / u) * u * g->warp_size;
+  int64_t warps = ((int64_t)threads + g->warp_size - 1) / g->warp_size;
+  int64_t parts = g->reg_partitions > 0 ? g->reg_partitions : 1;
+  int64_t per_part = (g->registers_per_sm / parts) / warp_regs;
+  return parts * per_part / warps;
+}
+
 int32_t orc_occupancy_for(const ompds_gpu_spec *g, int64_t fp, int32_t regs,
                           int32_t threads, ompds_occupancy *o) {
-  int64_t per_team_regs = (int64_t)regs * threads;
-  if (g->reg_alloc_unit > 0) { /* per warp, regs rounded up to the unit */
-    int64_t u = g->reg_alloc_unit;
-    int64_t warps = ((int64_t)threads + g->warp_size - 1) / g->warp_size;
-    per_team_regs = (((int64_t)regs + u - 1) / u * u) * g->warp_size * warps;
-  }
-  o->teams_by_regs = per_team_regs > 0 ? g->registers_per_sm / per_team_regs : 0;
+  o->teams_by_regs = o_teams_by_regs(g, regs, threads);
   int64_t per = fp > 0 ? fp + g->reserved_smem_per_block : 0;
   o->teams_by_smem = per > 0 ? g->shared_bytes_per_sm / per : 0;
   o->potential = mn(o->teams_by_regs, g->max_blocks_per_sm);
@@ -355,9 +362,11 @@ int32_t orc_occupancy_for(const ompds_gpu_spec *g, int64_t fp, int32_t regs,
 int64_t orc_max_regs_for_teams(const ompds_gpu_spec *g, int64_t teams, int32_t threads) {
   if (teams <= 0 || threads <= 0) return g->max_regs_per_thread;
   if (g->reg_alloc_unit > 0) {
-    int64_t warps = ((int64_t)threads + g->warp_size - 1) / g->warp_size;
-    int64_t r = g->registers_per_sm / (teams * warps * g->warp_size);
-    return mn(r / g->reg_alloc_unit * g->reg_alloc_unit, g->max_regs_per_thread);
+    int64_t r;
+    for (r = g->max_regs_per_thread / g->reg_alloc_unit * g->reg_alloc_unit; r > 0;
+         r -= g->reg_alloc_unit)
+      if (o_teams_by_regs(g, (int32_t)r, threads) >= teams) break;
+    return r;
   }
   return mn(g->registers_per_sm / (teams * threads), g->max_regs_per_thread);
 }

@@ -85,7 +85,7 @@ class GpuSpec(C.Structure):
                 ("max_blocks_per_sm", C.c_int64), ("warp_size", C.c_int32),
                 ("max_regs_per_thread", C.c_int32), ("max_threads_per_sm", C.c_int64),
                 ("reserved_smem_per_block", C.c_int64), ("reg_alloc_unit", C.c_int32),
-                ("reserved0", C.c_int32)]
+                ("reg_partitions", C.c_int32)]
 
 
 class Occupancy(C.Structure):

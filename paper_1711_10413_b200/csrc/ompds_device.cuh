@@ -52,20 +52,29 @@ enum Role : int { kMaster = OMPDS_ROLE_MASTER, kWorker = OMPDS_ROLE_WORKER };
 // Byte offsets inside the runtime-private span.  Exactly 49 bytes, the
 // reference's RuntimePrivateBytes (DeviceRuntime.h:31), so the team region
 // footprint is depot + 8*PreallocEntries + 49 as in Simulator.cpp:281-284.
+// The phase, Active and the staged region's retired count share one 32-bit
+// state word, so a worker reads everything a fetch needs with two 8-byte
+// aligned loads and a retirement or staging is a handful of stores.
 struct Rt {
   static constexpr int kArgs = 0;      // u64 args list (generic address)
-  static constexpr int kWorkFn = 8;    // i32 staged work function, -1 none
-  static constexpr int kNArgs = 12;    // i32 staged nargs
-  static constexpr int kWorkers = 16;  // i32 Workers
-  static constexpr int kActive = 20;   // i32 Active
+  static constexpr int kState = 8;     // u32 state word: phase << 24 |
+                                       //   retired << 12 | Active (12 bits
+                                       //   each: W <= 992)
+  static constexpr int kPhase = 11;    // u8 phase = the state word's top byte
+  static constexpr int kWorkFn = 12;   // i32 staged work function, -1 none
+  static constexpr int kNArgs = 16;    // i32 staged nargs
+  static constexpr int kWorkers = 20;  // i32 Workers
   static constexpr int kHeapTop = 24;  // u32 bytes in use in the global slab
   static constexpr int kDynAllocs = 28;// u32
   static constexpr int kDynFrees = 32; // u32
   static constexpr int kTrap = 36;     // i32 first trap code
   static constexpr int kDynBytes = 40; // u32 dynamic args bytes allocated
   static constexpr int kEvents = 44;   // u32 events logged
-  static constexpr int kPhase = 48;    // u8 phase
+  static constexpr int kSpare = 48;    // u8 unused
   static constexpr int kBytes = 49;
+  static constexpr uint32_t kActiveMask = 0xfffu;
+  static constexpr int kRetiredShift = 12;
+  static constexpr int kPhaseShift = 24;
 };
 static_assert(Rt::kBytes == OMPDS_RUNTIME_PRIVATE_BYTES, "rt span");
 
@@ -134,11 +143,12 @@ struct TeamCtx {
     return *reinterpret_cast<T *>(rt + off);
   }
   __device__ __forceinline__ uint8_t &phase() const { return at<uint8_t>(Rt::kPhase); }
-  // The 32-bit word at kActive: low 16 bits = Active (fetched - retired),
-  // high 16 bits = participants retired from the staged region (warp path).
-  __device__ __forceinline__ uint32_t &active_word() const { return at<uint32_t>(Rt::kActive); }
+  // The state word: bits 0-11 Active (fetched - retired), bits 12-23 the
+  // participants retired from the staged region (warp path), bits 24-31 the
+  // phase.
+  __device__ __forceinline__ uint32_t &active_word() const { return at<uint32_t>(Rt::kState); }
   __device__ __forceinline__ int32_t active() const {
-    return static_cast<int32_t>(active_word() & 0xffffu);
+    return static_cast<int32_t>(active_word() & Rt::kActiveMask);
   }
   __device__ __forceinline__ void *&args() const { return at<void *>(Rt::kArgs); }
   __device__ __forceinline__ int32_t &work_fn() const { return at<int32_t>(Rt::kWorkFn); }
@@ -242,52 +252,61 @@ struct PrepareState {
   int32_t active;
 };
 __device__ __forceinline__ PrepareState load_prepare_state(const TeamCtx &t) {
-  const uint32_t rt = t.rt_s;
-  uint32_t ph, aw;
-  asm volatile("ld.shared.u8 %0, [%2+48];\n\t"
-               "ld.shared.u32 %1, [%2+20];"
-               : "=r"(ph), "=r"(aw)
-               : "r"(rt)
-               : "memory");
-  static_assert(Rt::kPhase == 48 && Rt::kActive == 20, "rt layout");
-  return PrepareState{static_cast<uint8_t>(ph), static_cast<int32_t>(aw & 0xffffu)};
+  uint32_t sw;
+  asm volatile("ld.shared.u32 %0, [%1+8];" : "=r"(sw) : "r"(t.rt_s) : "memory");
+  static_assert(Rt::kState == 8, "rt layout");
+  return PrepareState{static_cast<uint8_t>(sw >> Rt::kPhaseShift),
+                      static_cast<int32_t>(sw & Rt::kActiveMask)};
 }
 struct StagedState {
   uint8_t phase;
   int32_t fn;
   int32_t nargs;
-  int32_t workers;
-  void **args;
-  void *win; // this lane's window entry (prefetch), or nullptr
+  void **args; // the staged list (loaded only when the caller needs it)
+  void *win;   // this lane's window entry (prefetch), or nullptr
 };
-// `win_off`: shared address of this lane's window entry, 0 = none.
+// `win_off`: shared address of this lane's window entry, 0 = none.  kArgs:
+// also load the list pointer (a list past the window is possible); without
+// it the list is the window (the lean instantiation's guarantee).
+template <bool kArgs = true>
 __device__ __forceinline__ StagedState load_staged_state(const TeamCtx &t,
                                                          uint32_t win_off) {
   const uint32_t rt = t.rt_s;
-  uint32_t ph, fn, na, wk;
-  unsigned long long args, win = 0;
-  static_assert(Rt::kArgs == 0 && Rt::kWorkFn == 8 && Rt::kNArgs == 12 &&
-                    Rt::kWorkers == 16, "rt layout");
-  if (win_off)
-    asm volatile("ld.shared.u8 %0, [%7+48];\n\t"
-                 "ld.shared.u64 %4, [%7];\n\t"
-                 "ld.shared.v2.u32 {%1, %2}, [%7+8];\n\t"
-                 "ld.shared.u32 %3, [%7+16];\n\t"
-                 "ld.shared.u64 %5, [%6];"
-                 : "=r"(ph), "=r"(fn), "=r"(na), "=r"(wk), "=l"(args), "=l"(win)
+  uint32_t sw, fn, na;
+  unsigned long long args = 0, win = 0;
+  static_assert(Rt::kArgs == 0 && Rt::kState == 8 && Rt::kWorkFn == 12 &&
+                    Rt::kNArgs == 16, "rt layout");
+  if (kArgs && win_off)
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%6+8];\n\t"
+                 "ld.shared.u32 %2, [%6+16];\n\t"
+                 "ld.shared.u64 %3, [%6];\n\t"
+                 "ld.shared.u64 %4, [%5];"
+                 : "=r"(sw), "=r"(fn), "=r"(na), "=l"(args), "=l"(win)
+                 : "r"(win_off), "r"(rt)
+                 : "memory");
+  else if (kArgs)
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%4+8];\n\t"
+                 "ld.shared.u32 %2, [%4+16];\n\t"
+                 "ld.shared.u64 %3, [%4];"
+                 : "=r"(sw), "=r"(fn), "=r"(na), "=l"(args)
+                 : "r"(rt)
+                 : "memory");
+  else if (win_off)
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%5+8];\n\t"
+                 "ld.shared.u32 %2, [%5+16];\n\t"
+                 "ld.shared.u64 %3, [%4];"
+                 : "=r"(sw), "=r"(fn), "=r"(na), "=l"(win)
                  : "r"(win_off), "r"(rt)
                  : "memory");
   else
-    asm volatile("ld.shared.u8 %0, [%5+48];\n\t"
-                 "ld.shared.u64 %4, [%5];\n\t"
-                 "ld.shared.v2.u32 {%1, %2}, [%5+8];\n\t"
-                 "ld.shared.u32 %3, [%5+16];"
-                 : "=r"(ph), "=r"(fn), "=r"(na), "=r"(wk), "=l"(args)
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%3+8];\n\t"
+                 "ld.shared.u32 %2, [%3+16];"
+                 : "=r"(sw), "=r"(fn), "=r"(na)
                  : "r"(rt)
                  : "memory");
-  return StagedState{static_cast<uint8_t>(ph), static_cast<int32_t>(fn),
-                     static_cast<int32_t>(na), static_cast<int32_t>(wk),
-                     reinterpret_cast<void **>(args), reinterpret_cast<void *>(win)};
+  void **list = kArgs ? reinterpret_cast<void **>(args) : t.window;
+  return StagedState{static_cast<uint8_t>(sw >> Rt::kPhaseShift), static_cast<int32_t>(fn),
+                     static_cast<int32_t>(na), list, reinterpret_cast<void *>(win)};
 }
 
 //===----------------------------------------------------------------------===//
@@ -405,8 +424,7 @@ __device__ __forceinline__ void retire_last(const TeamCtx &t) {
   t.work_fn() = -1;
   t.args() = nullptr;
   t.nargs() = 0;
-  t.active_word() = 0;
-  t.phase() = kIdle;
+  t.active_word() = uint32_t(kIdle) << Rt::kPhaseShift; // Active, retired 0
 }
 
 // __kmpc_kernel_end_parallel: a worker retires; the last one frees the
@@ -451,7 +469,6 @@ struct Fetch {
   int32_t nargs;
   int32_t status;
   void *win;         // this lane's window entry, loaded speculatively
-  int32_t workers;   // the team's Workers (kernel_init), read with the state
 };
 
 #ifndef OMPDS_PREFETCH_WINDOW
@@ -466,6 +483,8 @@ struct WarpMask {
   uint32_t n;       // their count
   uint32_t leader;  // lowest participating lane (does the warp's bookkeeping)
   bool is_leader;
+  bool sole;        // this warp holds all W participants (W = the launch's
+                    // thread_limit, which kernel_init records as Workers)
   // Also loop-invariant for a team, so hoisted with the mask (of(t, mine)):
   bool no_events;   // no event log: the fetch/retire fast paths apply
   uint32_t win_off; // shared address of this lane's window entry (0: none)
@@ -475,12 +494,14 @@ struct WarpMask {
     m.n = __popc(m.ballot);
     m.leader = m.ballot ? __ffs(m.ballot) - 1 : 0;
     m.is_leader = m.ballot != 0 && lane_id() == m.leader;
+    m.sole = false;
     m.no_events = false; // general paths only (still correct)
     m.win_off = 0;
     return m;
   }
-  __device__ __forceinline__ static WarpMask of(const TeamCtx &t, bool mine) {
+  __device__ __forceinline__ static WarpMask of(const TeamCtx &t, bool mine, int32_t workers) {
     WarpMask m = of(mine);
+    m.sole = m.n == static_cast<uint32_t>(workers);
     m.no_events = t.events == nullptr;
 #if OMPDS_PREFETCH_WINDOW
     if (static_cast<int32_t>(lane_id()) < t.prealloc)
@@ -498,33 +519,34 @@ __device__ __forceinline__ void red_add_if(uint32_t saddr, uint32_t v, bool p) {
                "r"(static_cast<uint32_t>(p))
                : "memory");
 }
-// retire of a region whose list is the window: args = null, work_fn = -1,
-// nargs = 0, Active word = 0, phase = Idle (retire_last's window case).
+// retire of a region whose list is the window: args = null, state = Idle
+// (Active and retired 0), work_fn = -1, nargs = 0 (retire_last's window case).
 __device__ __forceinline__ void retire_window_if(const TeamCtx &t, bool p) {
   const uint32_t rt = t.rt_s;
-  static_assert(Rt::kArgs == 0 && Rt::kWorkFn == 8 && Rt::kNArgs == 12 &&
-                    Rt::kActive == 20 && Rt::kPhase == 48, "rt layout");
+  static_assert(Rt::kArgs == 0 && Rt::kState == 8 && Rt::kWorkFn == 12 && Rt::kNArgs == 16,
+                "rt layout");
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t"
                "@q st.shared.u64 [%0], %2;\n\t"
                "@q st.shared.v2.u32 [%0+8], {%3, %4};\n\t"
-               "@q st.shared.u32 [%0+20], %4;\n\t"
-               "@q st.shared.u8 [%0+48], %5;\n\t}" ::"r"(rt),
-               "r"(static_cast<uint32_t>(p)), "l"(0ull), "r"(0xffffffffu), "r"(0u),
-               "r"(static_cast<uint32_t>(kIdle))
+               "@q st.shared.u32 [%0+16], %5;\n\t}" ::"r"(rt),
+               "r"(static_cast<uint32_t>(p)), "l"(0ull),
+               "r"(uint32_t(kIdle) << Rt::kPhaseShift), "r"(0xffffffffu), "r"(0u)
                : "memory");
 }
-// staging of a region (stage_region's stores), predicated on `p`.
+// staging of a region (stage_region's stores), predicated on `p`: the
+// state word becomes Staged with Active and retired 0 (prepare requires an
+// idle team).
 __device__ __forceinline__ void stage_region_if(const TeamCtx &t, int32_t fn,
                                                 int32_t nargs, void **list, bool p) {
   const uint32_t rt = t.rt_s;
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t"
                "@q st.shared.u64 [%0], %2;\n\t"
                "@q st.shared.v2.u32 [%0+8], {%3, %4};\n\t"
-               "@q st.shared.u8 [%0+48], %5;\n\t}" ::"r"(rt),
+               "@q st.shared.u32 [%0+16], %5;\n\t}" ::"r"(rt),
                "r"(static_cast<uint32_t>(p)),
                "l"(reinterpret_cast<unsigned long long>(list)),
-               "r"(static_cast<uint32_t>(fn)), "r"(static_cast<uint32_t>(nargs)),
-               "r"(static_cast<uint32_t>(kStaged))
+               "r"(uint32_t(kStaged) << Rt::kPhaseShift), "r"(static_cast<uint32_t>(fn)),
+               "r"(static_cast<uint32_t>(nargs))
                : "memory");
 }
 
@@ -536,7 +558,6 @@ __device__ __forceinline__ void stage_region_if(const TeamCtx &t, int32_t fn,
 __device__ __forceinline__ Fetch fetch_from(const StagedState &st) {
   Fetch f;
   f.win = st.win;
-  f.workers = st.workers;
   f.status = OMPDS_OK;
   f.fn = st.fn;
   f.args = st.args;
@@ -548,20 +569,20 @@ __device__ __forceinline__ bool fetch_is_fast(const StagedState &st,
   return st.phase == kStaged && m.no_events;
 }
 // The fast fetch's bookkeeping, branch-free: Active += n by the warp's
-// leader -- a plain store when this warp holds every participant (Active is
-// 0 between regions and no other warp fetches), otherwise one
-// fire-and-forget shared atomic.
+// leader -- a plain store of the state word (Staged, Active = n) when this
+// warp holds every participant (Active is 0 between regions and no other
+// warp fetches), otherwise one fire-and-forget shared atomic.
 __device__ __forceinline__ void fetch_account_fast(const TeamCtx &t,
-                                                   const StagedState &st,
+                                                   const StagedState &,
                                                    const WarpMask &m) {
-  const bool sole = m.n == static_cast<uint32_t>(st.workers);
   asm volatile("{\n\t.reg .pred qs, qm;\n\t"
-               "setp.ne.u32 qs, %2, 0;\n\t"
-               "setp.ne.u32 qm, %3, 0;\n\t"
-               "@qs st.shared.u32 [%0], %1;\n\t"
-               "@qm red.shared.add.u32 [%0], %1;\n\t}" ::"r"(t.rt_s + Rt::kActive),
-               "r"(m.n), "r"(static_cast<uint32_t>(m.is_leader && sole)),
-               "r"(static_cast<uint32_t>(m.is_leader && !sole))
+               "setp.ne.u32 qs, %3, 0;\n\t"
+               "setp.ne.u32 qm, %4, 0;\n\t"
+               "@qs st.shared.u32 [%0], %2;\n\t"
+               "@qm red.shared.add.u32 [%0], %1;\n\t}" ::"r"(t.rt_s + Rt::kState),
+               "r"(m.n), "r"((uint32_t(kStaged) << Rt::kPhaseShift) | m.n),
+               "r"(static_cast<uint32_t>(m.is_leader && m.sole)),
+               "r"(static_cast<uint32_t>(m.is_leader && !m.sole))
                : "memory");
 }
 // Every other case of the reference's kernel_parallel for a warp:
@@ -617,7 +638,7 @@ __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
 }
 __device__ __forceinline__ Fetch begin_parallel_warp(const TeamCtx &t,
                                                      bool mine) {
-  return begin_parallel_warp(t, WarpMask::of(mine), mine);
+  return begin_parallel_warp(t, WarpMask::of(t, mine, t.at<int32_t>(Rt::kWorkers)), mine);
 }
 
 // What a worker warp needs to retire the region it fetched, packed in one
@@ -630,8 +651,7 @@ __device__ __forceinline__ uint32_t retire_plan(const TeamCtx &t,
                                                 const Fetch &f) {
   // the list is the window iff nargs <= PreallocEntries (the placement law
   // of prepare_parallel, DeviceRuntime.cpp:61-74): a 32-bit compare
-  return (m.n << 8) | (m.is_leader ? 1u : 0u) |
-         (m.n == static_cast<uint32_t>(f.workers) ? 2u : 0u) |
+  return (m.n << 8) | (m.is_leader ? 1u : 0u) | (m.sole ? 2u : 0u) |
          (f.nargs <= t.prealloc ? 4u : 0u) | (m.no_events ? 8u : 0u);
 }
 
@@ -658,8 +678,7 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
       // Active -= n); the join barrier orders every retirement before the
       // master, which observes retired == W and completes the last
       // retirement (complete_region) -- no returning atomic on any worker.
-      red_add_if(t.rt_s + Rt::kActive,
-                 (n << 16) - n, leader);
+      red_add_if(t.rt_s + Rt::kState, (n << Rt::kRetiredShift) - n, leader);
     }
     return;
   }
@@ -689,21 +708,22 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
 #endif
   if (leader) {
     const uint32_t w = static_cast<uint32_t>(t.at<int32_t>(Rt::kWorkers));
-    // retired += n (high half), Active -= n (low half; >= n: our own fetch).
-    // acq_rel at CTA scope: every participant's reads of the staged region
-    // happen-before the last retiree's bookkeeping writes (retire_last).
+    // retired += n, Active -= n (>= n: our own fetch); the phase byte is
+    // untouched (the 12-bit fields never carry).  acq_rel at CTA scope: every
+    // participant's reads of the staged region happen-before the last
+    // retiree's bookkeeping writes (retire_last).
     uint32_t old;
     asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
                  : "=r"(old)
-                 : "r"(t.rt_s + Rt::kActive),
-                   "r"((n << 16) - n)
+                 : "r"(t.rt_s + Rt::kState),
+                   "r"((n << Rt::kRetiredShift) - n)
                  : "memory");
-    const uint32_t retired = (old >> 16) + n;
+    const uint32_t before = (old >> Rt::kRetiredShift) & Rt::kActiveMask;
+    const uint32_t retired = before + n;
     if (t.events) {
       int64_t ev = t.log_reserve(n);
       for (uint32_t k = 0; k < n; ++k)
-        t.log_at(ev + k, OMPDS_EV_RETIRE, -1,
-                 int64_t(w) - int64_t((old >> 16) + k + 1), 0);
+        t.log_at(ev + k, OMPDS_EV_RETIRE, -1, int64_t(w) - int64_t(before + k + 1), 0);
     }
     if (retired == w) // this warp retired the region's last participant
       retire_last(t);
@@ -720,7 +740,7 @@ __device__ __forceinline__ void end_parallel_window(const TeamCtx &t, uint32_t p
     __syncwarp(); // every lane's fetch reads before the leader's reset
     retire_window_if(t, leader);
   } else {
-    red_add_if(t.rt_s + Rt::kActive, (n << 16) - n, leader);
+    red_add_if(t.rt_s + Rt::kState, (n << Rt::kRetiredShift) - n, leader);
   }
 }
 // Master warp, after the join barrier of a region it staged with the window
@@ -747,7 +767,7 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
 }
 __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t, bool mine,
                                                   const Fetch &f) {
-  end_parallel_warp(t, WarpMask::of(mine), f);
+  end_parallel_warp(t, WarpMask::of(t, mine, t.at<int32_t>(Rt::kWorkers)), f);
 }
 
 //===----------------------------------------------------------------------===//

@@ -456,7 +456,9 @@ __global__ void OMPDS_GENERIC_LB
         p.warp_ovf ? p.warp_ovf + (size_t(blockIdx.x) * worker_warps + warp) * p.warp_ovf_bytes
                    : nullptr;
     w.ds.init(slot, p.warp_slot_bytes, ovf, p.warp_ovf ? p.warp_ovf_bytes : 0);
-    const WarpMask wm = WarpMask::of(t, w.mine); // loop-invariant participation
+    // loop-invariant participation (Workers = the launch's W, which the
+    // master's kernel_init records)
+    const WarpMask wm = WarpMask::of(t, w.mine, p.workers);
     // barrier arrivals of this lane (SimStats::BarrierEntries), counted only
     // by the general instantiation when the launch asks for them
     int32_t arrivals = 0;
@@ -466,7 +468,7 @@ __global__ void OMPDS_GENERIC_LB
       bar_sync(kBarHandoff, team_threads); // await.work
       arrivals += count;
       OMPDS_TL(rr, 5);
-      const StagedState st = load_staged_state(t, wm.win_off);
+      const StagedState st = load_staged_state<!kLean>(t, wm.win_off);
       Fetch f;
       if (__builtin_expect(fetch_is_fast(st, wm), 1)) {
         fetch_account_fast(t, st, wm); // a staged region, no event log

@@ -253,9 +253,10 @@ int32_t ompds_gpu_spec_get(const char *name, ompds_gpu_spec *out) {
       {"k40-48k", {49152, 65536, 16, 32, 255, 0, 0, 0, 0}},
       {"p100", {65536, 65536, 32, 32, 255, 0, 0, 0, 0}},
       // B200 (sm_100a): 228 KB smem per SM with 1 KB reserved per CTA,
-      // 64K registers allocated per warp in units of 256 (8 per thread),
-      // 32 CTAs and 2048 threads per SM.
-      {"b200", {233472, 65536, 32, 32, 255, 2048, 1024, 8, 0}},
+      // 64K registers in 4 sub-partitions of 16K, allocated per warp in
+      // units of 256 (8 per thread) from one sub-partition, 32 CTAs and
+      // 2048 threads per SM.
+      {"b200", {233472, 65536, 32, 32, 255, 2048, 1024, 8, 4}},
   };
   for (const Row &r : rows)
     if (std::strcmp(r.name, name) == 0) {
@@ -265,25 +266,30 @@ int32_t ompds_gpu_spec_get(const char *name, ompds_gpu_spec *out) {
   return OMPDS_ERR_INVALID;
 }
 
-// Registers a team of `threads` occupies: exact regs x threads in the
-// reference model; on hardware with an allocation unit, per warp (threads
-// rounded up to warps) with regs rounded up to the unit.
-static int64_t ompds_team_registers(const ompds_gpu_spec *g, int32_t regs,
-                                    int32_t threads) {
+// Teams of `threads` threads that fit the register file.  Reference model:
+// registers_per_sm / (regs x threads).  With an allocation unit: per warp,
+// regs rounded up to the unit; with sub-partitions: each warp takes its
+// registers from one sub-partition, so whole warps are counted per
+// sub-partition first (a 40-register 64-thread team: 16K / 1280 = 12 warps
+// per SMSP, 48 per SM = 24 teams, not 65536 / 2560 = 25).
+static int64_t ompds_teams_by_regs(const ompds_gpu_spec *g, int32_t regs, int32_t threads) {
+  if (regs <= 0 || threads <= 0)
+    return 0;
   if (g->reg_alloc_unit <= 0)
-    return int64_t(regs) * threads;
+    return g->registers_per_sm / (int64_t(regs) * threads);
   const int64_t u = g->reg_alloc_unit;
-  const int64_t r = (int64_t(regs) + u - 1) / u * u;
+  const int64_t per_warp = (int64_t(regs) + u - 1) / u * u * g->warp_size;
   const int64_t warps = (int64_t(threads) + g->warp_size - 1) / g->warp_size;
-  return r * g->warp_size * warps;
+  const int64_t parts = g->reg_partitions > 0 ? g->reg_partitions : 1;
+  const int64_t warps_per_sm = parts * ((g->registers_per_sm / parts) / per_warp);
+  return warps_per_sm / warps;
 }
 
 int32_t ompds_occupancy_for(const ompds_gpu_spec *g, int64_t footprint,
                             int32_t regs, int32_t threads, ompds_occupancy *o) {
   if (!g || !o)
     return OMPDS_ERR_INVALID;
-  const int64_t regs_per_team = ompds_team_registers(g, regs, threads);
-  o->teams_by_regs = regs_per_team > 0 ? g->registers_per_sm / regs_per_team : 0;
+  o->teams_by_regs = ompds_teams_by_regs(g, regs, threads);
   const int64_t per_team_smem = footprint > 0 ? footprint + g->reserved_smem_per_block : 0;
   o->teams_by_smem = per_team_smem > 0 ? g->shared_bytes_per_sm / per_team_smem : 0;
   o->potential = std::min(o->teams_by_regs, g->max_blocks_per_sm);
@@ -300,11 +306,11 @@ int64_t ompds_max_regs_for_teams(const ompds_gpu_spec *g, int64_t teams,
     return 0;
   if (teams <= 0 || threads <= 0)
     return g->max_regs_per_thread;
-  if (g->reg_alloc_unit > 0) { // per warp, rounded down to the unit
-    const int64_t warps = (int64_t(threads) + g->warp_size - 1) / g->warp_size;
-    const int64_t r = g->registers_per_sm / (teams * warps * g->warp_size);
-    return std::min<int64_t>(r / g->reg_alloc_unit * g->reg_alloc_unit,
-                             g->max_regs_per_thread);
+  if (g->reg_alloc_unit > 0) { // the largest unit multiple that still fits
+    int64_t r = g->max_regs_per_thread / g->reg_alloc_unit * g->reg_alloc_unit;
+    while (r > 0 && ompds_teams_by_regs(g, static_cast<int32_t>(r), threads) < teams)
+      r -= g->reg_alloc_unit;
+    return r;
   }
   return std::min<int64_t>(g->registers_per_sm / (teams * threads),
                            g->max_regs_per_thread);

@@ -179,10 +179,15 @@ def test_paper_footprints_and_capacity_law():
 
 def test_b200_occupancy_row():
     # 265-byte team region (config 1 loop layout) at 64 threads, 32 regs:
-    # the 32-CTA limit binds; at 40 regs the register file does (25).
+    # the 32-CTA limit binds; at 40 regs the register file does: 1280
+    # registers per warp, 12 warps in each 16K sub-partition = 24 teams (not
+    # 65536 / 2560 = 25: a 25th team per SM measured as a partial second
+    # wave, profiles/r2e_cfg1.json)
     o = occupancy.occupancy_for("b200", 265, 32, 64)
     assert o.actual == 32
-    assert occupancy.occupancy_for("b200", 265, 40, 64).actual == 25
+    assert occupancy.occupancy_for("b200", 265, 40, 64).actual == 24
+    assert occupancy.max_regs_for_teams("b200", 24, 64) == 40
+    assert occupancy.max_regs_for_teams("b200", 25, 64) == 32
     # 1024-thread teams: the 2048-threads/SM limit binds (2 teams/SM).
     o = occupancy.occupancy_for("b200", 289, 32, 1024)
     assert o.potential == 2 and o.actual == 2
