@@ -677,6 +677,27 @@ def other_configs(RG, dev, stream, sms):
         e1.synchronize()
         times_o.append(e0.elapsed_time(e1))
     ms_o = statistics.median(times_o)
+    # the same bytes moved by a plain device copy of the same size (torch
+    # copy_ of 2^24 doubles, the same queued [evict; copy] timing): the
+    # practical ceiling for a 1:1 read/write stream this short
+    src = torch.ones(n2, dtype=torch.float64, device=dev)
+
+    def queued_copy(with_copy):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(200_000)
+            e0.record(stream)
+            for _ in range(K):
+                flush.sum()
+                if with_copy:
+                    a.copy_(src)
+            e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1)
+    queued_copy(True)
+    ms_copy = (statistics.median(queued_copy(True) for _ in range(3))
+               - statistics.median(queued_copy(False) for _ in range(3))) / K
+    del src
     out["config2_shared_array_overflow"] = {
         "elements": n2, "teams": t2, "workers": w2, "ms": round(ms_o, 4),
         "GBps": round(16 * n2 / ms_o / 1e6, 1), "depot_capacity": 0,
@@ -693,6 +714,8 @@ def other_configs(RG, dev, stream, sms):
         "regs_per_thread": ptxas_regs("SharedArrayProgIdEELb1E"),
         "staging": "cp.async.bulk (TMA) of d[256] into the depot slot",
         "roofline_frac": None,
+        "same_size_copy_GBps_queued": round(16 * n2 / ms_copy / 1e6, 1),
+        "frac_of_same_size_copy": round(ms_copy / ms_queued, 4),
         "l2": "evicted before every launch by reading a 256 MB buffer"}
     del a, flush
     # config 3: nested regions (depth 3) on per-warp data-sharing stacks;

@@ -207,7 +207,10 @@ template <class T> struct SharedArrayProg {
       for (int k = 0; k < V; ++k)
         e[k] = e[k] + de[k];
     };
-    constexpr int U = 4; // 16-byte units of a[] in flight per thread
+#ifndef OMPDS_CONFIG2_UNITS
+#define OMPDS_CONFIG2_UNITS 4
+#endif
+    constexpr int U = OMPDS_CONFIG2_UNITS; // 16-byte units of a[] in flight per thread
     int64_t u = gid;
     for (; u + (U - 1) * pool < units; u += U * pool) {
       Vec v[U];
@@ -220,10 +223,21 @@ template <class T> struct SharedArrayProg {
         st_stream(av + u + k * pool, v[k]);
       }
     }
-    for (; u < units; u += pool) {
-      Vec v = av[u];
-      body(v, u);
-      av[u] = v;
+    // the last partial round: its (< U) units are still issued together --
+    // a unit at a time would pay the full memory latency once per unit at
+    // the end of every thread's range (a few microseconds per launch)
+    if (u < units) {
+      Vec v[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (u + k * pool < units)
+          v[k] = ld_stream(av + u + k * pool);
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (u + k * pool < units) {
+          body(v[k], u + k * pool);
+          st_stream(av + u + k * pool, v[k]);
+        }
     }
     for (int64_t i = units * V + gid; i < a.n; i += pool)
       a.a[i] = a.a[i] + d[i & (kLen - 1)];
