@@ -319,6 +319,134 @@ class _Compiler:
                        kl["total_shared"], kl["total_local"], priv, self.teams, self.workers)
 
 
+# ---------------------------------------------------------------------------
+# Frame variables from the AST (the input of the frame pipeline,
+# ompds_layout_build), for programs the reference frontend cannot compile
+# (nested regions).  Order and groups follow the reference's lowering and
+# codegen (AstLowering.cpp:23-52, 322-345, 375-400;
+# Codegen.cpp:413-430; LoweringPasses.cpp:270-280): the kernel frame group
+# (0) holds the referenced unmapped host scalars in host order, then the
+# target body's declarations and sequential loop counters in source order
+# (function 0), then __omp_worker's wf.addr / args.addr (function 1, 8 B,
+# pinned); region r owns groups 1 + 2r (its outlined function: a
+# parallel-for's counter, then the body's declarations in source order) and
+# 2 + 2r (its wrapper, no allocas).  A variable escapes when a region
+# captures it: a kernel variable any region references, or -- EXTENSION --
+# a region local a nested region references.  Liveness is not derived (no
+# IR), so these layouts are the O0 pipeline's (no stack coloring).
+# Regions are numbered in lowering order: the kernel's in source order,
+# then each region's nested ones as its body is lowered.
+# ---------------------------------------------------------------------------
+
+def _names_in(x, out):
+    if isinstance(x, dict):
+        if x.get("kind") in ("var", "index", "assign"):
+            out.add(x.get("name"))
+        for v in x.values():
+            _names_in(v, out)
+    elif isinstance(x, list):
+        for v in x:
+            _names_in(v, out)
+    return out
+
+
+def _decls(body, out):
+    """Declarations (name, elements) of a statement list in source order,
+    descending into blocks and sequential loops but not into regions."""
+    for st in body:
+        k = st["kind"]
+        if k == "decl":
+            out.append((st["name"], st.get("array_size", 1)))
+        elif k == "for":
+            out.append((st["counter"], 1))
+            _decls(st.get("body", []), out)
+        elif k == "block":
+            _decls(st.get("body", []), out)
+    return out
+
+
+def _regions_in(body, out):
+    """Region statements directly inside `body` (not inside other regions)."""
+    for st in body:
+        k = st["kind"]
+        if k in ("parallel", "parallel_for"):
+            out.append(st)
+        elif k in ("for", "block"):
+            _regions_in(st.get("body", []), out)
+    return out
+
+
+def _region_body(st):
+    return st["body"][0].get("body", []) if st["kind"] == "parallel_for" else st.get("body", [])
+
+
+def derive_frame_vars(ast: dict, kernel_name: str):
+    """(frame vars, group roots, group members) of `ast`; see above."""
+    from . import layout as LY
+    target = ast["target"]
+    maps = {m["name"] for m in target["maps"]}
+    refd = _names_in(target["body"], set())
+    kernel_decls = [(h["name"], 1) for h in ast["host"]
+                    if h["name"] not in maps and h["name"] in refd]
+    kernel_decls += _decls(target["body"], [])
+    # regions in lowering order, with their enclosing region (-1: the kernel)
+    regions = []
+    queue = [(st, -1) for st in _regions_in(target["body"], [])]
+    while queue:
+        st, parent = queue.pop(0)
+        r = len(regions)
+        regions.append((st, parent))
+        queue += [(n, r) for n in _regions_in(_region_body(st), [])]
+
+    def locals_of(st):
+        out = [(st["body"][0]["counter"], 1)] if st["kind"] == "parallel_for" else []
+        return _decls(_region_body(st), out)
+
+    # what each region references, including its nested regions' references
+    refs = [_names_in(st, set()) for st, _ in regions]
+    kernel_names = {n for n, _ in kernel_decls}
+    escapes_k = set()
+    escapes_r = [set() for _ in regions]
+    for r, (st, parent) in enumerate(regions):
+        own = {n for n, _ in locals_of(st)}
+        # a name resolves to the innermost enclosing scope that declares it
+        for name in refs[r]:
+            if name in own:
+                continue
+            p = parent
+            while p >= 0 and name not in {n for n, _ in locals_of(regions[p][0])}:
+                p = regions[p][1]
+            if p >= 0:
+                escapes_r[p].add(name)
+            elif name in kernel_names:
+                escapes_k.add(name)
+    fv = []
+    for name, el in kernel_decls:
+        fv.append(LY.FrameVar(name, 4 * el, 0, 0, name in escapes_k))
+    fv.append(LY.FrameVar("wf.addr", 8, 0, 1, False, True))
+    fv.append(LY.FrameVar("args.addr", 8, 0, 1, False, True))
+    roots = [kernel_name]
+    members = [[kernel_name, "__omp_worker"]]
+    for r, (st, _) in enumerate(regions):
+        for name, el in locals_of(st):
+            fv.append(LY.FrameVar(name, 4 * el, 1 + 2 * r, 0, name in escapes_r[r]))
+        roots += [f"__omp_outlined.{r}", f"__omp_outlined.{r}_wrapper"]
+        members += [[f"__omp_outlined.{r}"], [f"__omp_outlined.{r}_wrapper"]]
+    return fv, roots, members, [p for _, p in regions]
+
+
+def derive_layouts(ast: dict, kernel_name: str, pipeline: str = "o0"):
+    """The program's frame layouts (the shape compile_program takes) from
+    derive_frame_vars and the C-ABI frame pipeline."""
+    from . import layout as LY
+    fv, roots, _, _ = derive_frame_vars(ast, kernel_name)
+    lays = LY.build_layouts(fv, len(roots), pipeline)
+    return [{"root": r, "total_local": l.total_local, "total_shared": l.total_shared,
+             "has_shared_depot": l.has_shared_depot,
+             "slots": [{"offset": s.offset, "size": s.size, "align": s.align, "shared": s.shared,
+                        "owners": s.owners} for s in l.slots]} for r, l in zip(roots, lays)]
+
+
 def compile_program(ast: dict, layouts: Sequence[dict], kernel_root: str, teams: int,
                     workers: int) -> Program:
     """Lowers a reference AST (dumpAst JSON) + its frame layouts."""

@@ -239,3 +239,47 @@ def test_stream_checksum_equals_fill_stream_checksum_and_pins_the_fixture():
             acc = (acc + L.orc_stream_checksum(1, a, b, fx["seed_x"], fx["seed_y"],
                                                O.ptr(cf), 0)) & ((1 << 64) - 1)
         assert "%#018x" % acc == fx["checksums"][str(n)]
+
+
+def test_ast_oracle_reproduces_the_reference_oracle():
+    """oracle/ast_oracle.py (the checker for nested-region programs) is
+    pinned against the reference's own sequential oracle: for every corpus,
+    generated and analog program the reference compiles correctly, under
+    every recorded launch shape, the final mapped arrays are equal."""
+    import golden_util as G
+    from oracle import ast_oracle as AO
+    n = 0
+    for p in G.programs():
+        if p["stem"].startswith("gen_") and G.reference_broken(p):
+            continue
+        if "ast" not in p:
+            continue
+        tgt = p["ast"]["target"]
+        for run in p["runs"]:
+            o = run.get("oracle")
+            if not o or not o.get("ok"):
+                continue
+            t = run["teams"] if run["teams"] > 0 else (tgt.get("num_teams") or 1)
+            w = run["workers"] if run["workers"] > 0 else (tgt.get("thread_limit") or 32)
+            got = AO.run(p["ast"], t, w, p.get("inputs"))
+            want = {k: v for k, v in o["globals"].items() if k in got}
+            assert {k: got[k] for k in want} == want, (p["stem"], t, w)
+            n += 1
+    assert n >= 190
+
+
+def test_derived_frame_layouts_equal_the_reference_o0_layouts():
+    """program.derive_layouts (frame variables from the AST, for programs
+    the reference frontend cannot compile) reproduces the reference's O0
+    frame layouts of every program it compiles correctly."""
+    import golden_util as G
+    from paper_1711_10413_b200 import program as PG
+    keys = ("root", "total_local", "total_shared", "has_shared_depot", "slots")
+    n = 0
+    for p in G.programs():
+        if (p["stem"].startswith("gen_") and G.reference_broken(p)) or not p.get("layouts_o0"):
+            continue
+        got = [{k: g[k] for k in keys} for g in PG.derive_layouts(p["ast"], p["kernel"])]
+        assert got == [{k: g[k] for k in keys} for g in p["layouts_o0"]], p["stem"]
+        n += 1
+    assert n >= 112
