@@ -493,7 +493,14 @@ int32_t ompds_run_nested(const ompds_launch *launch, int32_t elem,
  * Variables live where the frame layout puts them (space): 0 team depot
  * (shared slot), 1 the master's local depot mirror, 2 the worker's private
  * frame, 3 capture j of the current region (via get-shared-variables),
- * 4 mapped buffer.  All host arrays below are copied per launch. */
+ * 4 mapped buffer.  All host arrays below are copied per launch.
+ * Nested regions (EXTENSION; the reference rejects them): a PARALLEL in a
+ * region body runs the child region serialized on the encountering thread
+ * (omp_get_thread_num() 0, one thread), its capture list published on the
+ * thread's data-sharing stack and read back with get-shared-variables; a
+ * GLOBALIZE region's private frame lives on that stack too.  Each worker
+ * lane has its own stack (1/32 of the warp's slot, then its slice of the
+ * warp's overflow chain): lanes of a warp may nest divergently. */
 typedef struct ompds_prog_var {
   int32_t space;  /* 0..4 as above                           */
   int32_t index;  /* byte offset (0..2), capture j, buffer k */
@@ -501,11 +508,19 @@ typedef struct ompds_prog_var {
   int32_t _pad;
 } ompds_prog_var;
 typedef struct ompds_prog_region {
-  int32_t entry;      /* pc of the region body            */
-  int32_t n_captures; /* nargs of its prepare_parallel    */
-  int32_t cap_begin;  /* into `captures` (var indices)    */
-  int32_t _pad;
+  int32_t entry;      /* pc of the region body                              */
+  int32_t n_captures; /* nargs of its prepare_parallel / nested list         */
+  int32_t cap_begin;  /* into `captures` (var indices in the encountering
+                         context: the master's, or the parent region's)      */
+  int32_t parent;     /* -1: staged by the master; else the region whose body
+                         encounters it (EXTENSION, nested: serialized on the
+                         encountering thread); parent < index     */
+  int32_t frame_bytes;/* its private frame (outlined group TotalLocal)      */
+  int32_t flags;      /* OMPDS_REGION_GLOBALIZE: the frame holds locals a
+                         nested region captures, so each activation's frame
+                         is pushed on the thread's data-sharing stack        */
 } ompds_prog_region;
+#define OMPDS_REGION_GLOBALIZE 1
 typedef struct ompds_program {
   const int32_t *code;
   int64_t n_code;
@@ -525,6 +540,10 @@ typedef struct ompds_program {
                            before the team traps OMPDS_TRAP_STEP_LIMIT;
                            <= 0: 20,000,000 (SimOptions::StepLimit's
                            default, Simulator.h:37)                     */
+  int64_t stack_slot_bytes;     /* per worker warp: shared-memory slot of the
+                                   lanes' data-sharing stacks (1/32 each);
+                                   0 when no region nests or globalizes  */
+  int64_t stack_overflow_bytes; /* per worker warp: global overflow chain  */
 } ompds_program;
 
 /* Checks a program without a GPU (ompds_run_program runs the same check

@@ -148,7 +148,10 @@ class ProgVar(C.Structure):
 
 class ProgRegion(C.Structure):
     _fields_ = [("entry", C.c_int32), ("n_captures", C.c_int32), ("cap_begin", C.c_int32),
-                ("_pad", C.c_int32)]
+                ("parent", C.c_int32), ("frame_bytes", C.c_int32), ("flags", C.c_int32)]
+
+
+REGION_GLOBALIZE = 1
 
 
 class Program(C.Structure):
@@ -158,7 +161,8 @@ class Program(C.Structure):
                 ("n_captures", C.c_int32), ("n_buffers", C.c_int32),
                 ("buffers", C.POINTER(C.c_void_p)), ("total_shared", C.c_int64),
                 ("total_local", C.c_int64), ("priv_bytes", C.c_int64),
-                ("step_limit", C.c_int64)]
+                ("step_limit", C.c_int64), ("stack_slot_bytes", C.c_int64),
+                ("stack_overflow_bytes", C.c_int64)]
 
 
 AllocFn = C.CFUNCTYPE(C.c_uint64, C.c_int64, C.c_void_p)   # ompds_alloc_fn

@@ -56,7 +56,8 @@ def _stale() -> bool:
     return any(os.path.getmtime(s) > t for s in SOURCES + HEADERS)
 
 
-EXAMPLE_SRC = os.path.join(os.path.dirname(HERE), "examples", "reduction_region.cu")
+EXAMPLE_SRCS = [os.path.join(os.path.dirname(HERE), "examples", f)
+                for f in ("reduction_region.cu", "nested_region.cu")]
 EXAMPLE_LIB = os.path.join(OUT_DIR, "libompds_example.so")
 
 
@@ -65,9 +66,9 @@ def build_example(force: bool = False) -> str:
     against the runtime headers and linked to libompds_b200.so."""
     if not force and os.path.exists(EXAMPLE_LIB) and all(
             os.path.getmtime(f) <= os.path.getmtime(EXAMPLE_LIB)
-            for f in [EXAMPLE_SRC, LIB] + HEADERS):
+            for f in EXAMPLE_SRCS + [LIB] + HEADERS):
         return EXAMPLE_LIB
-    cmd = [nvcc()] + NVCC_FLAGS + ["-I", CSRC, "-o", EXAMPLE_LIB + ".tmp", EXAMPLE_SRC,
+    cmd = [nvcc()] + NVCC_FLAGS + ["-I", CSRC, "-o", EXAMPLE_LIB + ".tmp"] + EXAMPLE_SRCS + [
                                    "-L", OUT_DIR, "-lompds_b200", "-Xlinker", "-rpath,$ORIGIN"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

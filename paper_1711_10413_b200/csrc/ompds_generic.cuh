@@ -404,6 +404,51 @@ struct Worker {
     if (arrivals)
       ++*arrivals;
   }
+
+  // The warp's data-sharing stack for region code (__kmpc_data_sharing_
+  // push_stack / _pop_stack, Simulator.cpp:439-479's activation frames):
+  // one frame of `bytes_per_lane` bytes for each of the warp's 32 lanes,
+  // lane l's part at f.base + l * bytes_per_lane -- in the warp's
+  // shared-memory slot while it fits, else on its global overflow chain.
+  // Warp-collective (every lane calls it, in the same order).
+  __device__ __forceinline__ Frame push_frame(int64_t bytes_per_lane) {
+    return ds.push(bytes_per_lane, kWarp);
+  }
+  __device__ __forceinline__ int32_t pop_frame(const Frame &f) { return ds.pop(f); }
+
+  // A parallel region nested in this region's body (EXTENSION; the paper's
+  // runtime-managed stack for nesting): serialized on each lane -- a team of
+  // one, like the LLVM device runtime's __kmpc_serialized_parallel.  Each
+  // lane's `nargs` capture addresses addr_of(j) are published in a list
+  // frame on the warp's data-sharing stack (begin-sharing-variables; lane
+  // l's list at base + 8*nargs*l), `body(NestedVars)` runs and reads them
+  // back (get-shared-variables), then the list frame is popped.  The
+  // encountering level's locals a nested region captures must themselves
+  // live on the stack (push_frame) -- the globalization the frame pipeline
+  // marks with the escape bit.  Warp-collective; returns 0 or
+  // OMPDS_TRAP_STACK_OVERFLOW / _UNDERFLOW.
+  struct NestedVars {
+    void **list;
+    int32_t nargs;
+    __device__ __forceinline__ void *get(int j) const { return list[j]; }
+  };
+  template <class AddrOf, class Body>
+  __device__ __forceinline__ int32_t parallel_serialized(int32_t nargs, AddrOf addr_of,
+                                                         Body body) {
+    Frame f{};
+    f.offset = -1;
+    void **list = nullptr;
+    if (nargs > 0) {
+      f = ds.push(int64_t(nargs) * 8, kWarp);
+      if (f.status != OMPDS_OK)
+        return f.status;
+      list = reinterpret_cast<void **>(f.base) + size_t(lane_id()) * nargs;
+      for (int32_t j = 0; j < nargs; ++j)
+        list[j] = addr_of(j);
+    }
+    body(NestedVars{list, nargs});
+    return nargs > 0 ? ds.pop(f) : OMPDS_OK;
+  }
 };
 
 // kLean: the instantiation for launches with no event log, no allocation

@@ -544,6 +544,7 @@ enum : int32_t { SP_DEPOT, SP_MLOCAL, SP_PRIV, SP_CAPTURE, SP_GLOBAL };
 constexpr int kVmStack = 32;
 constexpr int kVmPriv = 256;    // bytes of a worker's private frame
 constexpr int kVmCaps = 128;    // captures per region
+constexpr int kVmMaxNest = 3;   // nested activations below a worker's region
 
 struct VmCtx {
   int64_t steps_left; // operations this thread may still execute
@@ -555,6 +556,13 @@ struct VmCtx {
   unsigned char *priv;
   void *const *caps;
   int32_t tid, team, nthreads, nteams;
+  // region code only (nested regions, EXTENSION)
+  const ompds_prog_region *regions = nullptr;
+  const int32_t *cap_tab = nullptr;
+  DsStack *ds = nullptr;         // this thread's data-sharing stack
+  unsigned char *pool = nullptr; // kVmMaxNest private frames (not globalized)
+  int32_t priv_bytes = kVmPriv;  // the current activation's frame
+  int32_t rid = -1;              // the current region, -1: the master
 };
 
 // Resolves element `idx` of variable `v`; nullptr when out of bounds.
@@ -574,18 +582,53 @@ __device__ __forceinline__ int32_t *vm_addr(const VmCtx &c, int32_t v,
   return reinterpret_cast<int32_t *>(base) + idx;
 }
 
-// Runs from *pc until END (returns 0), PARALLEL (returns 1, region in *r)
-// or a trap (returns the trap code, negated).
+// A serialized nested region's activation (EXTENSION): what the encountering
+// activation resumes with, and the two data-sharing stack frames it pushed
+// (the capture list -- __kmpc_begin_sharing_variables -- and, for a
+// GLOBALIZE region, its private frame).
+struct VmAct {
+  int32_t pc, rid, tid, nthreads, priv_bytes;
+  unsigned char *priv;
+  void *const *caps;
+  Frame list, frame;
+};
+
+// Runs from *pc until END (returns 0), a PARALLEL of the master's code
+// (returns 1, region in *r) or a trap (returns the trap code, negated).  A
+// PARALLEL inside region code runs the nested region right here, serialized
+// on this thread: a team of one (omp_get_thread_num() 0), its capture list
+// published on the thread's data-sharing stack, its frame pushed there when
+// the region globalizes its locals; END returns to the encountering region.
 __device__ int32_t vm_run(VmCtx &c, int32_t *pc_io, int32_t *r) {
   int32_t st[kVmStack];
   int sp = 0;
   int32_t pc = *pc_io;
+  VmAct act[kVmMaxNest];
+  int depth = 0;
   for (;;) {
     if (--c.steps_left < 0) // a runaway program (Simulator.cpp:819-822)
       return -OMPDS_TRAP_STEP_LIMIT;
     const int32_t op = c.code[pc++];
     switch (op) {
     case OP_END:
+      if (depth > 0) { // leave a nested region: pop its frames, resume
+        VmAct &a = act[--depth];
+        int32_t s = OMPDS_OK;
+        if (a.frame.offset >= 0)
+          s = c.ds->pop(a.frame);
+        if (a.list.offset >= 0 && s == OMPDS_OK)
+          s = c.ds->pop(a.list);
+        if (s != OMPDS_OK)
+          return -s;
+        pc = a.pc;
+        c.rid = a.rid;
+        c.tid = a.tid;
+        c.nthreads = a.nthreads;
+        c.priv = a.priv;
+        c.priv_bytes = a.priv_bytes;
+        c.caps = a.caps;
+        break;
+      }
       *pc_io = pc;
       return 0;
     case OP_PUSH: st[sp++] = c.code[pc++]; break;
@@ -630,12 +673,61 @@ __device__ int32_t vm_run(VmCtx &c, int32_t *pc_io, int32_t *r) {
         pc = target;
       break;
     }
-    case OP_PARALLEL:
-      *r = c.code[pc++];
-      *pc_io = pc;
-      return 1;
-    case OP_ZERO_PRIV:
-      for (int i = 0; i < kVmPriv; i += 4)
+    case OP_PARALLEL: {
+      const int32_t rr = c.code[pc++];
+      if (c.rid < 0) { // the master's region: staged through the protocol
+        *r = rr;
+        *pc_io = pc;
+        return 1;
+      }
+      // nested region, serialized on this thread (the verifier guarantees
+      // regions[rr].parent == c.rid, an empty operand stack, and the depth)
+      if (depth >= kVmMaxNest || c.ds == nullptr)
+        return -OMPDS_ERR_INVALID;
+      const ompds_prog_region R = c.regions[rr];
+      VmAct &a = act[depth];
+      a.pc = pc;
+      a.rid = c.rid;
+      a.tid = c.tid;
+      a.nthreads = c.nthreads;
+      a.priv = c.priv;
+      a.priv_bytes = c.priv_bytes;
+      a.caps = c.caps;
+      a.list.offset = -1;
+      a.frame.offset = -1;
+      // begin-sharing-variables: the list of the captures' addresses in the
+      // encountering activation, on this thread's data-sharing stack
+      void **list = nullptr;
+      if (R.n_captures > 0) {
+        a.list = c.ds->push(int64_t(R.n_captures) * 8, 1);
+        if (a.list.status != OMPDS_OK)
+          return -OMPDS_TRAP_STACK_OVERFLOW;
+        list = reinterpret_cast<void **>(a.list.base);
+        for (int32_t j = 0; j < R.n_captures; ++j)
+          list[j] = vm_addr(c, c.cap_tab[R.cap_begin + j], 0);
+      }
+      unsigned char *frame = c.pool + depth * kVmPriv;
+      if (R.flags & OMPDS_REGION_GLOBALIZE) {
+        a.frame = c.ds->push(R.frame_bytes, 1);
+        if (a.frame.status != OMPDS_OK) {
+          if (a.list.offset >= 0)
+            c.ds->pop(a.list);
+          return -OMPDS_TRAP_STACK_OVERFLOW;
+        }
+        frame = a.frame.base;
+      }
+      ++depth;
+      c.rid = rr;
+      c.tid = 0;       // a team of one
+      c.nthreads = 1;
+      c.caps = list;   // get-shared-variables of the nested region
+      c.priv = frame;
+      c.priv_bytes = R.frame_bytes;
+      pc = R.entry;
+      break;
+    }
+    case OP_ZERO_PRIV: // the activation's frame starts zero-filled (pushActivation)
+      for (int i = 0; i < c.priv_bytes; i += 4)
         *reinterpret_cast<int32_t *>(c.priv + i) = 0;
       break;
     default:
@@ -691,11 +783,40 @@ struct ProgramProg {
       caps[j] = sv.get(j);
     if (!w.mine)
       return;
+    const ompds_prog_region R = a.regions[fn];
+    // This lane's data-sharing stack (nested regions, globalized frames):
+    // 1/32 of the warp's slot and of its overflow chain, so lanes that nest
+    // divergently never share a frame.
+    const uint32_t lane = lane_id();
+    const uint32_t slot_l = (w.ds.slot_cap / kWarp) & ~7u, ovf_l = (w.ds.ovf_cap / kWarp) & ~7u;
+    DsStack lds;
+    lds.init(w.ds.slot + lane * slot_l, slot_l, w.ds.ovf ? w.ds.ovf + lane * ovf_l : nullptr,
+             w.ds.ovf ? ovf_l : 0);
     alignas(16) unsigned char priv[kVmPriv];
-    VmCtx c{a.step_limit, a.code, a.vars, a.bufs, nullptr, nullptr, priv, caps,
+    alignas(16) unsigned char pool[kVmMaxNest * kVmPriv];
+    unsigned char *frame = priv;
+    Frame f{};
+    f.offset = -1;
+    if (R.flags & OMPDS_REGION_GLOBALIZE) { // its locals are captured below it
+      f = lds.push(R.frame_bytes, 1);
+      if (f.status != OMPDS_OK) {
+        w.t->trap(f.status);
+        return;
+      }
+      frame = f.base;
+    }
+    VmCtx c{a.step_limit, a.code, a.vars, a.bufs, nullptr, nullptr, frame, caps,
             w.wid, w.team, w.workers, w.teams};
-    int32_t pc = a.regions[fn].entry, r = 0;
-    const int32_t ev = vm_run(c, &pc, &r);
+    c.regions = a.regions;
+    c.cap_tab = a.caps;
+    c.ds = &lds;
+    c.pool = pool;
+    c.priv_bytes = R.frame_bytes;
+    c.rid = fn;
+    int32_t pc = R.entry, r = 0;
+    int32_t ev = vm_run(c, &pc, &r);
+    if (ev == 0 && f.offset >= 0)
+      ev = -lds.pop(f);
     if (ev < 0)
       w.t->trap(-ev);
   }
@@ -1073,8 +1194,8 @@ bool vm_has_arg(int32_t op) {
 
 // `reg`: the region whose body addresses the variable (nullptr: the
 // master's sequential code).
-bool vm_var_ok(const ompds_program *pr, int32_t v, bool master,
-               const ompds_prog_region *reg) {
+bool vm_var_ok(const ompds_program *pr, int32_t v, const ompds_prog_region *reg) {
+  const bool master = reg == nullptr;
   if (v < 0 || v >= pr->n_vars)
     return false;
   const ompds_prog_var d = pr->vars[v];
@@ -1088,24 +1209,36 @@ bool vm_var_ok(const ompds_program *pr, int32_t v, bool master,
   switch (d.space) {
   case SP_DEPOT: return master && end <= pr->total_shared;
   case SP_MLOCAL: return master && end <= std::max<int64_t>(pr->total_local, 4);
-  case SP_PRIV: return !master && end <= kVmPriv;
+  case SP_PRIV: return !master && end <= reg->frame_bytes; // the region's own frame
   case SP_CAPTURE: {
-    // capture j of the region: it aliases the master variable the region
-    // publishes as entry j, so it may not extend past that variable
-    if (master || reg == nullptr || d.index >= reg->n_captures)
+    // capture j of the region: it aliases the variable the encountering
+    // context publishes as entry j, so it may not extend past it
+    if (master || d.index >= reg->n_captures)
       return false;
     const int32_t src = pr->captures[reg->cap_begin + d.index];
-    if (src < 0 || src >= pr->n_vars || pr->vars[src].space == SP_CAPTURE)
-      return false;
-    return d.count <= pr->vars[src].count;
+    return src >= 0 && src < pr->n_vars && d.count <= pr->vars[src].count;
   }
   case SP_GLOBAL: return d.index < pr->n_buffers;
   default: return false;
   }
 }
 
+// A capture published for region `g` by its encountering context: the
+// master's depot / local mirror (top-level regions), or a variable of the
+// parent region's activation -- its frame or one of its own captures
+// (nested regions).  Mapped buffers are never captures.
+bool vm_capture_ok(const ompds_program *pr, const ompds_prog_region &g, int32_t v) {
+  if (v < 0 || v >= pr->n_vars)
+    return false;
+  const int32_t sp = pr->vars[v].space;
+  if (g.parent < 0)
+    return (sp == SP_DEPOT || sp == SP_MLOCAL) && vm_var_ok(pr, v, nullptr);
+  return (sp == SP_PRIV || sp == SP_CAPTURE) && vm_var_ok(pr, v, &pr->regions[g.parent]);
+}
+
 bool vm_walk(const ompds_program *pr, const std::vector<int8_t> &start, int32_t entry,
-             bool master, const ompds_prog_region *reg) {
+             int32_t rid) {
+  const ompds_prog_region *reg = rid >= 0 ? &pr->regions[rid] : nullptr;
   const int64_t n = pr->n_code;
   const int32_t *code = pr->code;
   std::vector<int32_t> depth(size_t(n), -1);
@@ -1136,17 +1269,20 @@ bool vm_walk(const ompds_program *pr, const std::vector<int8_t> &start, int32_t 
     case OP_JMP: work.push_back({arg, d}); continue;
     case OP_JNLT: need = 2; delta = -2; break;
     case OP_PARALLEL:
-      if (!master || d != 0 || arg < 0 || arg >= pr->n_regions)
+      // an empty operand stack, and a region whose encountering context is
+      // this one: the master's code stages top-level regions, a region's
+      // body runs its own nested children (EXTENSION)
+      if (d != 0 || arg < 0 || arg >= pr->n_regions || pr->regions[arg].parent != rid)
         return false;
       break;
     case OP_ZERO_PRIV:
-      if (master)
+      if (!reg)
         return false;
       break;
     default: return false;
     }
     if ((op == OP_LOAD || op == OP_STORE || op == OP_LOADX || op == OP_STOREX) &&
-        !vm_var_ok(pr, arg, master, reg))
+        !vm_var_ok(pr, arg, reg))
       return false;
     if (d < need || d + delta > kVmStack)
       return false;
@@ -1167,18 +1303,29 @@ bool verify_program(const ompds_program *pr) {
     if (pc > n)
       return false;
   }
+  bool stacked = false; // some region nests or globalizes: needs the stacks
   for (int32_t r = 0; r < pr->n_regions; ++r) {
     const ompds_prog_region &g = pr->regions[r];
     if (g.cap_begin < 0 || int64_t(g.cap_begin) + g.n_captures > pr->n_captures ||
-        (g.n_captures > 0 && !pr->captures))
+        (g.n_captures > 0 && !pr->captures) || g.parent < -1 || g.parent >= r ||
+        g.frame_bytes < 0 || g.frame_bytes > kVmPriv || (g.frame_bytes & 3) ||
+        (g.flags & ~OMPDS_REGION_GLOBALIZE))
       return false;
+    int32_t nest = 0; // activations below the worker's region (parents form a tree)
+    for (int32_t p = g.parent; p >= 0; p = pr->regions[p].parent)
+      ++nest;
+    if (nest > kVmMaxNest)
+      return false;
+    stacked |= g.parent >= 0 || (g.flags & OMPDS_REGION_GLOBALIZE);
     for (int32_t j = 0; j < g.n_captures; ++j)
-      if (!vm_var_ok(pr, pr->captures[g.cap_begin + j], true, nullptr))
+      if (!vm_capture_ok(pr, g, pr->captures[g.cap_begin + j]))
         return false;
-    if (!vm_walk(pr, start, g.entry, false, &g))
+    if (!vm_walk(pr, start, g.entry, r))
       return false;
   }
-  return vm_walk(pr, start, 0, true, nullptr);
+  if (stacked && pr->stack_slot_bytes <= 0 && pr->stack_overflow_bytes <= 0)
+    return false;
+  return vm_walk(pr, start, 0, -1);
 }
 
 } // namespace
@@ -1190,7 +1337,9 @@ int32_t ompds_program_verify(const ompds_program *pr) {
       pr->n_captures < 0 || pr->n_buffers < 0 || pr->total_shared < 0 ||
       (pr->total_shared & 7) != 0 || /* the args window and runtime span follow
                                         the depot at 8-byte aligned offsets */
-      pr->total_local < 0 || pr->priv_bytes > kVmPriv)
+      pr->total_local < 0 || pr->priv_bytes > kVmPriv || pr->stack_slot_bytes < 0 ||
+      pr->stack_slot_bytes > 64 * 1024 || pr->stack_overflow_bytes < 0 ||
+      pr->stack_overflow_bytes > (int64_t(1) << 24))
     return OMPDS_ERR_INVALID;
   if ((pr->n_regions > 0 && !pr->regions) || (pr->n_vars > 0 && !pr->vars) ||
       (pr->n_buffers > 0 && !pr->buffers))
@@ -1244,8 +1393,9 @@ int32_t ompds_run_program(const ompds_launch *launch, const ompds_program *pr,
   // `host` (pageable) before cudaMemcpyAsync returned, and the next launch's
   // copy into the same workspace buffer is ordered behind this kernel by the
   // stream (ensure_buffer synchronizes the stream before it ever frees it).
-  return launch_generic<ProgramProg>(launch, lay, 0, a, stats, events, 0, 0,
-                                     /*allow_lean=*/false);
+  // per worker warp: the lanes' data-sharing stacks (nested regions)
+  return launch_generic<ProgramProg>(launch, lay, 0, a, stats, events, pr->stack_slot_bytes,
+                                     pr->stack_overflow_bytes, /*allow_lean=*/false);
 }
 
 int32_t ompds_run_stream_host(const ompds_launch *launch, int32_t elem,

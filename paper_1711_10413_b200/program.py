@@ -45,7 +45,10 @@ class CompileError(Exception):
 @dataclass
 class Region:
     entry: int
-    captures: List[int]  # kernel var-table indices, in capture order
+    captures: List[int]  # var-table indices in the encountering context, in capture order
+    parent: int = -1     # -1: staged by the master; else the encountering region (nested)
+    frame_bytes: int = 0  # its outlined function's frame (TotalLocal)
+    globalize: bool = False  # its frame holds locals a nested region captures
 
 
 @dataclass
@@ -60,6 +63,10 @@ class Program:
     priv_bytes: int
     teams: int
     workers: int
+
+    def nested(self) -> bool:
+        """Some region nests or globalizes: the lanes need data-sharing stacks."""
+        return any(r.parent >= 0 or r.globalize for r in self.regions)
 
 
 def _layout_slots(layouts, root) -> Dict[str, Tuple[int, bool]]:
@@ -97,7 +104,20 @@ class _Compiler:
         # kernel-scope variables in alloca emission order (AstLowering.cpp:23-52)
         self.kvars: Dict[str, int] = {}
         self.kelems: Dict[str, int] = {}
-        self.region_count = 0
+        # the region tree in lowering order (derive_frame_vars's numbering):
+        # AST statement -> (region id, parent id), and each region's captures
+        # (names from enclosing scopes its subtree references), precomputed
+        # so a parent captures what its nested regions need
+        self.rid_of: Dict[int, int] = {}
+        self.tree: List[Tuple[dict, int]] = []
+        queue = [(st, -1) for st in _regions_in(ast["target"]["body"], [])]
+        while queue:
+            st, parent = queue.pop(0)
+            self.rid_of[id(st)] = len(self.tree)
+            self.tree.append((st, parent))
+            queue += [(n, len(self.tree) - 1) for n in _regions_in(_region_body(st), [])]
+        self.cap_names: List[List[str]] = []
+        self.nested_src: Dict[int, List[int]] = {}
 
     # -- variable table ----------------------------------------------------
     def _var(self, name, space, off, elems):
@@ -122,14 +142,12 @@ class _Compiler:
         """Var-table index of `name` in `scope` (a dict for region code)."""
         if scope is not None and name in scope["locals"]:
             return scope["locals"][name]
-        if name in self.kvars:
-            if scope is None:
-                return self.kvars[name]
-            # a kernel variable referenced from a region is a capture
-            caps = scope["caps"]
-            if name not in caps:
-                caps[name] = None
+        if scope is not None and name in scope["capnames"]:
+            # a variable of an enclosing scope (the kernel's, or -- nested --
+            # an enclosing region's) referenced from a region is a capture
             return scope["capvar"](name)
+        if name in self.kvars and scope is None:
+            return self.kvars[name]
         if name in self.global_idx:
             return self._global_var(name)
         raise CompileError(f"unresolved {name}")
@@ -224,11 +242,14 @@ class _Compiler:
             self.emit(OP_LOAD, v, OP_PUSH, 1, OP_ADD, OP_STORE, v, OP_JMP, top)
             self.code[patch] = len(self.code)
         elif k in ("parallel", "parallel_for"):
+            r = self.rid_of[id(s)]
             if scope is not None:
-                raise CompileError("nested parallel regions (use ompds_run_nested)")
-            r = self.region_count
-            self.region_count += 1
-            self.regions.append(Region(-1, []))
+                # nested (EXTENSION): the encountering region publishes the
+                # addresses of the nested region's captures from its own
+                # activation -- its locals or its own captures
+                if self.tree[r][1] != scope["rid"]:
+                    raise CompileError("region tree mismatch")
+                self.nested_src[r] = [self.resolve(n, scope) for n in self.cap_names[r]]
             self.emit(OP_PARALLEL, r)
             self.pending.append((r, s))
         elif k == "block":
@@ -245,25 +266,77 @@ class _Compiler:
         scope["locals"][name] = v
         return v
 
+    def _capture_names(self):
+        """Per region: the names of enclosing-scope variables its subtree
+        references, in capture order -- kernel variables in kernel alloca
+        order (Codegen.cpp:173-201), then (nested regions, EXTENSION) the
+        enclosing regions' locals, outermost region first, each in its
+        declaration order."""
+        local_names = []
+        for st, _ in self.tree:
+            ls = [st["body"][0]["counter"]] if st["kind"] == "parallel_for" else []
+            local_names.append([n for n, _ in _decls(_region_body(st), [(x, 1) for x in ls])])
+        # names declared anywhere in a region's subtree (its own locals and
+        # its nested regions'): references to them are not captures of it
+        below = [set(ln) for ln in local_names]
+        for r in reversed(range(len(self.tree))):
+            p = self.tree[r][1]
+            if p >= 0:
+                below[p] |= below[r]
+        out = []
+        for r, (st, parent) in enumerate(self.tree):
+            refs = _names_in(st, set()) - below[r] - set(self.global_idx)
+            chain = []  # ancestors, outermost first
+            p = parent
+            while p >= 0:
+                chain.insert(0, p)
+                p = self.tree[p][1]
+            keyed = []
+            for name in refs:
+                home = next((p for p in reversed(chain) if name in local_names[p]), None)
+                if home is not None:
+                    keyed.append(((1, chain.index(home), local_names[home].index(name)), name))
+                elif name in self.kvars:
+                    keyed.append(((0, self.kvars[name], 0), name))
+                else:
+                    raise CompileError(f"unresolved {name}")
+            out.append([n for _, n in sorted(keyed)])
+        return out
+
     def region(self, r, s):
         root = f"__omp_outlined.{r}"
-        scope = {"locals": {}, "caps": {}, "pslots": _layout_slots(self.layouts, root)}
+        parent = self.tree[r][1]
+        group = next((g for g in self.layouts if g["root"] == root), None)
+        scope = {"locals": {}, "caps": {}, "pslots": _layout_slots(self.layouts, root), "rid": r}
+        names = self.cap_names[r]
         capvars: Dict[str, int] = {}
 
         def capvar(name):
             if name not in capvars:
-                capvars[name] = self._var("&" + name, SP_CAPTURE, -1, self.kelems[name])
+                if name not in names:
+                    raise CompileError(f"{name} is not a capture of region {r}")
+                src = self.kvars.get(name)
+                elems = self.kelems[name] if src is not None and parent < 0 else \
+                    self._elems_of_capture(r, name)
+                capvars[name] = self._var("&" + name, SP_CAPTURE, names.index(name), elems)
             return capvars[name]
 
         scope["capvar"] = capvar
+        scope["capnames"] = set(names)
         entry = len(self.code)
         self.emit(OP_ZERO_PRIV)
         if s["kind"] == "parallel_for":
             loop = s["body"][0]
             v = self._priv_var(loop["counter"], 1, scope)
-            # start = init + (team * nt + tid); stride = nt * nteams
             self.expr(loop["init"], scope, True)
-            self.emit(OP_TEAM, OP_NTHREADS, OP_MUL, OP_TID, OP_ADD, OP_ADD, OP_STORE, v)
+            if parent < 0:
+                # start = init + (team * nt + tid); stride = nt * nteams
+                # (AstLowering.cpp:429-462)
+                self.emit(OP_TEAM, OP_NTHREADS, OP_MUL, OP_TID, OP_ADD, OP_ADD, OP_STORE, v)
+            else:
+                # nested: the team of one runs every iteration (start = init +
+                # tid, stride = nt, with tid 0 and nt 1)
+                self.emit(OP_TID, OP_ADD, OP_STORE, v)
             top = len(self.code)
             self.emit(OP_LOAD, v)
             self.expr(loop["bound"], scope, True)
@@ -271,21 +344,36 @@ class _Compiler:
             patch = len(self.code) - 1
             for b in loop.get("body", []):
                 self.stmt(b, scope, True)
-            self.emit(OP_LOAD, v, OP_NTHREADS, OP_NTEAMS, OP_MUL, OP_ADD, OP_STORE, v, OP_JMP, top)
+            if parent < 0:
+                self.emit(OP_LOAD, v, OP_NTHREADS, OP_NTEAMS, OP_MUL, OP_ADD, OP_STORE, v,
+                          OP_JMP, top)
+            else:
+                self.emit(OP_LOAD, v, OP_NTHREADS, OP_ADD, OP_STORE, v, OP_JMP, top)
             self.code[patch] = len(self.code)
         else:
             for b in s.get("body", []):
                 self.stmt(b, scope, True)
         self.emit(OP_END)
-        # captures in kernel alloca order (Codegen.cpp:173-201)
-        order = sorted(capvars, key=lambda n: self.kvars[n])
-        for j, name in enumerate(order):
-            sp, _, el = self.vars[capvars[name]]
-            self.vars[capvars[name]] = (SP_CAPTURE, j, el)
-        self.regions[r] = Region(entry, [self.kvars[n] for n in order])
+        self.scopes[r] = scope
+        caps = [self.kvars[n] for n in names] if parent < 0 else None
+        self.regions[r] = Region(entry, caps, parent,
+                                 group["total_local"] if group else 0,
+                                 bool(group and any(sl["shared"] for sl in group["slots"])))
+
+    def _elems_of_capture(self, r, name):
+        """Elements of the variable a nested region's capture aliases."""
+        p = self.tree[r][1]
+        while p >= 0:
+            sc = self.scopes.get(p)
+            if sc is not None and name in sc["locals"]:
+                return self.vars[sc["locals"][name]][2]
+            p = self.tree[p][1]
+        return self.kelems[name]
 
     def compile(self) -> Program:
         self.pending = []
+        self.scopes: Dict[int, dict] = {}
+        self.regions = [Region(-1, []) for _ in self.tree]
         # unmapped host scalars referenced by the target become kernel allocas
         # initialised with their host value (AstLowering.cpp:31-37)
         refd = set()
@@ -311,8 +399,14 @@ class _Compiler:
         for s in self.ast["target"]["body"]:
             self.stmt(s, None, False)
         self.emit(OP_END)
-        for r, s in self.pending:
+        self.cap_names = self._capture_names()
+        i = 0
+        while i < len(self.pending):  # nested regions are appended as found
+            r, s = self.pending[i]
             self.region(r, s)
+            i += 1
+        for r, src in self.nested_src.items():
+            self.regions[r].captures = src
         kl = next(g for g in self.layouts if g["root"] == self.kernel_root)
         priv = max([g["total_local"] for g in self.layouts if g["root"] != self.kernel_root] + [0])
         return Program(self.code, self.vars, self.var_names, self.regions, self.buffers,
@@ -453,16 +547,30 @@ def compile_program(ast: dict, layouts: Sequence[dict], kernel_root: str, teams:
     return _Compiler(ast, layouts, kernel_root, teams, workers).compile()
 
 
-def describe(prog: Program, buffer_ptrs, step_limit: int = 0):
+# Per worker warp, for programs with nested regions: the lanes' data-sharing
+# stacks (a 1/32 share of each per lane).
+STACK_SLOT_BYTES = 4096
+STACK_OVERFLOW_BYTES = 32768
+
+
+def describe(prog: Program, buffer_ptrs, step_limit: int = 0,
+             stack_slot_bytes: Optional[int] = None,
+             stack_overflow_bytes: Optional[int] = None):
     """The ompds_program descriptor of `prog` (and the ctypes arrays it
     points into, which must outlive it)."""
+    nested = prog.nested()
+    if stack_slot_bytes is None:
+        stack_slot_bytes = STACK_SLOT_BYTES if nested else 0
+    if stack_overflow_bytes is None:
+        stack_overflow_bytes = STACK_OVERFLOW_BYTES if nested else 0
     code = (C.c_int32 * max(len(prog.code), 1))(*prog.code)
     vars_ = (L.ProgVar * max(len(prog.vars), 1))(*[L.ProgVar(s, o, n, 0) for s, o, n in prog.vars])
     caps = [c for r in prog.regions for c in r.captures]
     regs = []
     k = 0
     for r in prog.regions:
-        regs.append(L.ProgRegion(r.entry, len(r.captures), k, 0))
+        regs.append(L.ProgRegion(r.entry, len(r.captures), k, r.parent, r.frame_bytes,
+                                 L.REGION_GLOBALIZE if r.globalize else 0))
         k += len(r.captures)
     regs_a = (L.ProgRegion * max(len(regs), 1))(*regs)
     caps_a = (C.c_int32 * max(len(caps), 1))(*caps)
@@ -471,7 +579,8 @@ def describe(prog: Program, buffer_ptrs, step_limit: int = 0):
                      n_regions=len(regs), regions=regs_a, captures=caps_a, n_captures=len(caps),
                      n_buffers=len(buffer_ptrs), buffers=bufs, total_shared=prog.total_shared,
                      total_local=prog.total_local, priv_bytes=prog.priv_bytes,
-                     step_limit=step_limit)
+                     step_limit=step_limit, stack_slot_bytes=stack_slot_bytes,
+                     stack_overflow_bytes=stack_overflow_bytes)
     return desc, (code, vars_, regs_a, caps_a, bufs)
 
 
@@ -486,7 +595,9 @@ def run_program(prog: Program, buffers, prealloc_entries: int = L.DEFAULT_PREALL
                 fail_dynamic_alloc: bool = False, depot_capacity: int = -1,
                 max_events: int = 0, stream=None, list_allocator: int = L.LIST_SLAB,
                 first_team: int = 0, total_teams: int = 0, teams: int = 0,
-                step_limit: int = 0, barrier_arrivals=None):
+                step_limit: int = 0, barrier_arrivals=None,
+                stack_slot_bytes: Optional[int] = None,
+                stack_overflow_bytes: Optional[int] = None):
     """Launches the program: `buffers` are int32 CUDA tensors, one per mapped
     array, in host declaration order.  Returns regions.Outputs."""
     import torch
@@ -496,7 +607,8 @@ def run_program(prog: Program, buffers, prealloc_entries: int = L.DEFAULT_PREALL
     for b, (name, n, _) in zip(buffers, prog.buffers):
         if b.dtype != torch.int32 or b.numel() != n or not b.is_cuda:
             raise ValueError(f"buffer {name}: int32[{n}] on cuda expected")
-    desc, _keep = describe(prog, [b.data_ptr() for b in buffers], step_limit)
+    desc, _keep = describe(prog, [b.data_ptr() for b in buffers], step_limit,
+                           stack_slot_bytes, stack_overflow_bytes)
     out = RG.Outputs(teams or prog.teams, buffers[0].device if buffers else "cuda", max_events)
     launch = RG.make_launch(teams or prog.teams, prog.workers, prealloc_entries,
                             fail_dynamic_alloc, depot_capacity, max_events > 0, max_events,

@@ -63,3 +63,39 @@ def test_example_region_program_matches_numpy(teams, workers, n):
         # 304-byte depot + 160 B window + 49 B runtime span
         assert (st.trap, st.master_barriers, st.barrier_releases, st.regions) == (0, 6, 7, 3)
         assert st.smem_bytes == 304 + 160 + 49 and st.depot_in_smem
+
+
+def _nested_lib():
+    lb = lib()
+    lb.example_nested.argtypes = [C.POINTER(L.Launch), C.c_void_p, C.c_int32, C.c_int64,
+                                  C.c_int64, C.c_void_p]
+    lb.example_nested.restype = C.c_int32
+    return lb
+
+
+def test_example_library_exports_the_nested_program():
+    assert hasattr(_nested_lib(), "example_nested")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("teams,workers,slot,ovf", [(1, 96, 4096, 4096), (37, 40, 4096, 4096),
+                                                    (148, 96, 0, 8192), (5, 33, 1024, 8192)])
+def test_example_nested_program_matches_the_config3_oracle(teams, workers, slot, ovf):
+    """Nested regions through the device API (push_frame / pop_frame /
+    parallel_serialized) compute the config-3 program exactly like the
+    C oracle (orc_nested) -- frames in the warps' shared-memory slots, on
+    the overflow chains, or spilling from one to the other."""
+    import torch
+    from oracle import oracle as O
+    from paper_1711_10413_b200 import regions as RG
+    regions = 4
+    a = torch.zeros(teams * workers, dtype=torch.float64, device="cuda")
+    res = RG.Outputs(teams, a.device, 0)
+    launch = RG.make_launch(teams, workers)
+    L.check(_nested_lib().example_nested(C.byref(launch), C.c_void_p(a.data_ptr()), regions,
+                                         slot, ovf, res.stats_ptr()), "example_nested")
+    torch.cuda.synchronize()
+    want = np.zeros(teams * workers)
+    O.lib().orc_nested(1, teams, workers, regions, O.ptr(want))
+    assert all(s.trap == 0 for s in res.team_stats())
+    assert np.array_equal(a.cpu().numpy(), want)

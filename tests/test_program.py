@@ -88,7 +88,7 @@ def simulate(prog: PG.Program, inputs):
             else:
                 d[o] = val
 
-        def run(pc, tid, caps, priv, nthreads):
+        def run(pc, tid, caps, priv, nthreads, in_region=False):
             st = []
             code = prog.code
             while True:
@@ -126,6 +126,13 @@ def simulate(prog: PG.Program, inputs):
                     b = st.pop(); a = st.pop()
                     if not a < b:
                         pc = t
+                elif op == PG.OP_PARALLEL and in_region:
+                    # nested region (EXTENSION): serialized, a team of one,
+                    # captures are addresses in this activation
+                    reg2 = prog.regions[code[pc]]
+                    pc += 1
+                    caps2 = [cell(None, v, 0, caps, priv) for v in reg2.captures]
+                    run(reg2.entry, 0, caps2, {}, 1, True)
                 elif op == PG.OP_PARALLEL:
                     return code[pc], pc + 1
                 elif op == PG.OP_ZERO_PRIV:
@@ -142,7 +149,7 @@ def simulate(prog: PG.Program, inputs):
                 sp, off, _ = prog.vars[v]
                 caps.append((depot if sp == PG.SP_DEPOT else mlocal, off))
             for w in range(prog.workers):
-                run(reg.entry, w, caps, {}, prog.workers)
+                run(reg.entry, w, caps, {}, prog.workers, True)
     return bufs
 
 
