@@ -1411,19 +1411,26 @@ int32_t ompds_run_stream_host(const ompds_launch *launch, int32_t elem,
   const int64_t esz = elem ? 8 : 4;
   const int64_t chunk = std::max<int64_t>(int64_t(1) << 23, round_up((n + 31) / 32, 1024));
   cudaStream_t st = static_cast<cudaStream_t>(launch->stream);
+  // copy streams and the per-chunk events are created once per thread and
+  // device and reused by later calls (the events only order this call's
+  // copies and launches; a call synchronises before it returns)
   static thread_local cudaStream_t h2d = nullptr, d2h = nullptr;
   static thread_local int dev_of = -1;
+  static thread_local std::vector<cudaEvent_t> ev;
   int dev = 0;
   OMPDS_CUDA(cudaGetDevice(&dev));
   if (h2d == nullptr || dev_of != dev) {
     OMPDS_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
     OMPDS_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+    ev.clear(); // events of another device are not reused
     dev_of = dev;
   }
   const int64_t nchunks = n == 0 ? 0 : (n + chunk - 1) / chunk;
-  std::vector<cudaEvent_t> ev(static_cast<size_t>(2 * nchunks + 1));
-  for (auto &e : ev)
+  while (ev.size() < static_cast<size_t>(2 * nchunks + 1)) {
+    cudaEvent_t e = nullptr;
     OMPDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ev.push_back(e);
+  }
   // copies must not start before the caller's prior work on `st`
   OMPDS_CUDA(cudaEventRecord(ev[2 * nchunks], st));
   OMPDS_CUDA(cudaStreamWaitEvent(h2d, ev[2 * nchunks], 0));
@@ -1447,8 +1454,6 @@ int32_t ompds_run_stream_host(const ompds_launch *launch, int32_t elem,
   }
   OMPDS_CUDA(cudaStreamSynchronize(d2h));
   OMPDS_CUDA(cudaStreamSynchronize(st));
-  for (auto &e : ev)
-    cudaEventDestroy(e);
   return s;
 }
 
