@@ -207,37 +207,58 @@ template <class T> struct SharedArrayProg {
       for (int k = 0; k < V; ++k)
         e[k] = e[k] + de[k];
     };
-#ifndef OMPDS_CONFIG2_UNITS
-#define OMPDS_CONFIG2_UNITS 4
+#ifndef OMPDS_CONFIG2_BLOCK
+#define OMPDS_CONFIG2_BLOCK 1
 #endif
-    constexpr int U = OMPDS_CONFIG2_UNITS; // 16-byte units of a[] in flight per thread
-    int64_t u = gid;
-    for (; u + (U - 1) * pool < units; u += U * pool) {
-      Vec v[U];
+#ifndef OMPDS_CONFIG2_ROUND
+#define OMPDS_CONFIG2_ROUND 4
+#endif
+    // The cyclic schedule over blocks of B consecutive 16-byte units per
+    // thread, R blocks (B x R units of a[]) in flight per round.
+    constexpr int B = OMPDS_CONFIG2_BLOCK, R = OMPDS_CONFIG2_ROUND;
+    const int64_t nblocks = units / B;
+    int64_t bk = gid;
+    for (; bk + (R - 1) * pool < nblocks; bk += R * pool) {
+      Vec v[R][B];
 #pragma unroll
-      for (int k = 0; k < U; ++k)
-        v[k] = ld_stream(av + u + k * pool);
+      for (int k = 0; k < R; ++k)
 #pragma unroll
-      for (int k = 0; k < U; ++k) {
-        body(v[k], u + k * pool);
-        st_stream(av + u + k * pool, v[k]);
-      }
-    }
-    // the last partial round: its (< U) units are still issued together --
-    // a unit at a time would pay the full memory latency once per unit at
-    // the end of every thread's range (a few microseconds per launch)
-    if (u < units) {
-      Vec v[U];
+        for (int j = 0; j < B; ++j)
+          v[k][j] = ld_stream(av + (bk + k * pool) * B + j);
 #pragma unroll
-      for (int k = 0; k < U; ++k)
-        if (u + k * pool < units)
-          v[k] = ld_stream(av + u + k * pool);
+      for (int k = 0; k < R; ++k)
 #pragma unroll
-      for (int k = 0; k < U; ++k)
-        if (u + k * pool < units) {
-          body(v[k], u + k * pool);
-          st_stream(av + u + k * pool, v[k]);
+        for (int j = 0; j < B; ++j) {
+          const int64_t u = (bk + k * pool) * B + j;
+          body(v[k][j], u);
+          st_stream(av + u, v[k][j]);
         }
+    }
+    // the last partial round: its blocks are still issued together -- a
+    // block at a time would pay the full memory latency once per block at
+    // the end of every thread's range (a few microseconds per launch)
+    if (bk < nblocks) {
+      Vec v[R][B];
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        if (bk + k * pool < nblocks)
+#pragma unroll
+          for (int j = 0; j < B; ++j)
+            v[k][j] = ld_stream(av + (bk + k * pool) * B + j);
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        if (bk + k * pool < nblocks)
+#pragma unroll
+          for (int j = 0; j < B; ++j) {
+            const int64_t u = (bk + k * pool) * B + j;
+            body(v[k][j], u);
+            st_stream(av + u, v[k][j]);
+          }
+    }
+    for (int64_t u = nblocks * B + gid; u < units; u += pool) { // units past the blocks
+      Vec v = av[u];
+      body(v, u);
+      av[u] = v;
     }
     for (int64_t i = units * V + gid; i < a.n; i += pool)
       a.a[i] = a.a[i] + d[i & (kLen - 1)];
