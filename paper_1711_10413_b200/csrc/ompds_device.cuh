@@ -52,17 +52,18 @@ enum Role : int { kMaster = OMPDS_ROLE_MASTER, kWorker = OMPDS_ROLE_WORKER };
 // Byte offsets inside the runtime-private span.  Exactly 49 bytes, the
 // reference's RuntimePrivateBytes (DeviceRuntime.h:31), so the team region
 // footprint is depot + 8*PreallocEntries + 49 as in Simulator.cpp:281-284.
-// The phase, Active and the staged region's retired count share one 32-bit
-// state word, so a worker reads everything a fetch needs with two 8-byte
-// aligned loads and a retirement or staging is a handful of stores.
+// The phase shares a 32-bit word with the staged work function, next to
+// nargs: a worker's fetch reads everything it needs with one 8-byte load,
+// and staging is two stores.  Active and the staged region's retired count
+// live in their own word, so the workers' bookkeeping atomics never touch a
+// word another lane of the warp is reading.
 struct Rt {
   static constexpr int kArgs = 0;      // u64 args list (generic address)
-  static constexpr int kState = 8;     // u32 state word: phase << 24 |
-                                       //   retired << 12 | Active (12 bits
-                                       //   each: W <= 992)
+  static constexpr int kState = 8;     // u32 phase << 24 | work fn (24-bit
+                                       //   two's complement, -1 = none)
   static constexpr int kPhase = 11;    // u8 phase = the state word's top byte
-  static constexpr int kWorkFn = 12;   // i32 staged work function, -1 none
-  static constexpr int kNArgs = 16;    // i32 staged nargs
+  static constexpr int kNArgs = 12;    // i32 staged nargs
+  static constexpr int kActive = 16;   // u32 retired << 16 | Active
   static constexpr int kWorkers = 20;  // i32 Workers
   static constexpr int kHeapTop = 24;  // u32 bytes in use in the global slab
   static constexpr int kDynAllocs = 28;// u32
@@ -72,10 +73,19 @@ struct Rt {
   static constexpr int kEvents = 44;   // u32 events logged
   static constexpr int kSpare = 48;    // u8 unused
   static constexpr int kBytes = 49;
-  static constexpr uint32_t kActiveMask = 0xfffu;
-  static constexpr int kRetiredShift = 12;
+  static constexpr uint32_t kActiveMask = 0xffffu;
+  static constexpr int kRetiredShift = 16;
   static constexpr int kPhaseShift = 24;
+  static constexpr uint32_t kFnMask = 0xffffffu;
 };
+// Work-function ids are 24-bit: [0, 2^23) (-1 = none).
+constexpr int32_t kMaxWorkFn = (1 << 23) - 1;
+__host__ __device__ constexpr uint32_t state_word(uint8_t phase, int32_t fn) {
+  return (uint32_t(phase) << Rt::kPhaseShift) | (uint32_t(fn) & Rt::kFnMask);
+}
+__host__ __device__ constexpr int32_t state_fn(uint32_t w) {
+  return static_cast<int32_t>(w << 8) >> 8; // sign-extend the low 24 bits
+}
 static_assert(Rt::kBytes == OMPDS_RUNTIME_PRIVATE_BYTES, "rt span");
 
 __host__ __device__ constexpr int64_t round_up(int64_t v, int64_t a) {
@@ -143,15 +153,20 @@ struct TeamCtx {
     return *reinterpret_cast<T *>(rt + off);
   }
   __device__ __forceinline__ uint8_t &phase() const { return at<uint8_t>(Rt::kPhase); }
-  // The state word: bits 0-11 Active (fetched - retired), bits 12-23 the
-  // participants retired from the staged region (warp path), bits 24-31 the
-  // phase.
-  __device__ __forceinline__ uint32_t &active_word() const { return at<uint32_t>(Rt::kState); }
+  // The word at kActive: low 16 bits = Active (fetched - retired), high 16
+  // bits = participants retired from the staged region (warp path).
+  __device__ __forceinline__ uint32_t &active_word() const { return at<uint32_t>(Rt::kActive); }
   __device__ __forceinline__ int32_t active() const {
     return static_cast<int32_t>(active_word() & Rt::kActiveMask);
   }
   __device__ __forceinline__ void *&args() const { return at<void *>(Rt::kArgs); }
-  __device__ __forceinline__ int32_t &work_fn() const { return at<int32_t>(Rt::kWorkFn); }
+  __device__ __forceinline__ int32_t work_fn() const {
+    return state_fn(at<uint32_t>(Rt::kState));
+  }
+  __device__ __forceinline__ void set_work_fn(int32_t fn) const {
+    uint32_t &w = at<uint32_t>(Rt::kState);
+    w = (w & ~Rt::kFnMask) | (uint32_t(fn) & Rt::kFnMask);
+  }
   __device__ __forceinline__ int32_t &nargs() const { return at<int32_t>(Rt::kNArgs); }
 
   __device__ __forceinline__ bool args_dynamic() const {
@@ -252,11 +267,15 @@ struct PrepareState {
   int32_t active;
 };
 __device__ __forceinline__ PrepareState load_prepare_state(const TeamCtx &t) {
-  uint32_t sw;
-  asm volatile("ld.shared.u32 %0, [%1+8];" : "=r"(sw) : "r"(t.rt_s) : "memory");
-  static_assert(Rt::kState == 8, "rt layout");
+  uint32_t sw, aw;
+  asm volatile("ld.shared.u32 %0, [%2+8];\n\t"
+               "ld.shared.u32 %1, [%2+16];"
+               : "=r"(sw), "=r"(aw)
+               : "r"(t.rt_s)
+               : "memory");
+  static_assert(Rt::kState == 8 && Rt::kActive == 16, "rt layout");
   return PrepareState{static_cast<uint8_t>(sw >> Rt::kPhaseShift),
-                      static_cast<int32_t>(sw & Rt::kActiveMask)};
+                      static_cast<int32_t>(aw & Rt::kActiveMask)};
 }
 struct StagedState {
   uint8_t phase;
@@ -272,40 +291,35 @@ template <bool kArgs = true>
 __device__ __forceinline__ StagedState load_staged_state(const TeamCtx &t,
                                                          uint32_t win_off) {
   const uint32_t rt = t.rt_s;
-  uint32_t sw, fn, na;
+  uint32_t sw, na;
   unsigned long long args = 0, win = 0;
-  static_assert(Rt::kArgs == 0 && Rt::kState == 8 && Rt::kWorkFn == 12 &&
-                    Rt::kNArgs == 16, "rt layout");
+  static_assert(Rt::kArgs == 0 && Rt::kState == 8 && Rt::kNArgs == 12, "rt layout");
   if (kArgs && win_off)
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%6+8];\n\t"
-                 "ld.shared.u32 %2, [%6+16];\n\t"
-                 "ld.shared.u64 %3, [%6];\n\t"
-                 "ld.shared.u64 %4, [%5];"
-                 : "=r"(sw), "=r"(fn), "=r"(na), "=l"(args), "=l"(win)
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%5+8];\n\t"
+                 "ld.shared.u64 %2, [%5];\n\t"
+                 "ld.shared.u64 %3, [%4];"
+                 : "=r"(sw), "=r"(na), "=l"(args), "=l"(win)
                  : "r"(win_off), "r"(rt)
                  : "memory");
   else if (kArgs)
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%4+8];\n\t"
-                 "ld.shared.u32 %2, [%4+16];\n\t"
-                 "ld.shared.u64 %3, [%4];"
-                 : "=r"(sw), "=r"(fn), "=r"(na), "=l"(args)
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%3+8];\n\t"
+                 "ld.shared.u64 %2, [%3];"
+                 : "=r"(sw), "=r"(na), "=l"(args)
                  : "r"(rt)
                  : "memory");
   else if (win_off)
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%5+8];\n\t"
-                 "ld.shared.u32 %2, [%5+16];\n\t"
-                 "ld.shared.u64 %3, [%4];"
-                 : "=r"(sw), "=r"(fn), "=r"(na), "=l"(win)
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%4+8];\n\t"
+                 "ld.shared.u64 %2, [%3];"
+                 : "=r"(sw), "=r"(na), "=l"(win)
                  : "r"(win_off), "r"(rt)
                  : "memory");
   else
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%3+8];\n\t"
-                 "ld.shared.u32 %2, [%3+16];"
-                 : "=r"(sw), "=r"(fn), "=r"(na)
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2+8];"
+                 : "=r"(sw), "=r"(na)
                  : "r"(rt)
                  : "memory");
   void **list = kArgs ? reinterpret_cast<void **>(args) : t.window;
-  return StagedState{static_cast<uint8_t>(sw >> Rt::kPhaseShift), static_cast<int32_t>(fn),
+  return StagedState{static_cast<uint8_t>(sw >> Rt::kPhaseShift), state_fn(sw),
                      static_cast<int32_t>(na), list, reinterpret_cast<void *>(win)};
 }
 
@@ -368,8 +382,7 @@ __device__ __forceinline__ void stage_region(const TeamCtx &t, int32_t fn,
                                              int64_t nargs, void **list) {
   t.args() = list;
   t.nargs() = static_cast<int32_t>(nargs);
-  t.work_fn() = fn;
-  t.phase() = kStaged;
+  t.at<uint32_t>(Rt::kState) = state_word(kStaged, fn);
 }
 
 // __kmpc_kernel_prepare_parallel / begin-sharing-variables: stages work
@@ -421,10 +434,10 @@ __device__ __forceinline__ void retire_last(const TeamCtx &t) {
     t.at<uint32_t>(Rt::kDynFrees) += 1;
     t.log(OMPDS_EV_DYNAMIC_FREE, -1, 0, bytes);
   }
-  t.work_fn() = -1;
+  t.at<uint32_t>(Rt::kState) = state_word(kIdle, -1);
   t.args() = nullptr;
   t.nargs() = 0;
-  t.active_word() = uint32_t(kIdle) << Rt::kPhaseShift; // Active, retired 0
+  t.active_word() = 0;
 }
 
 // __kmpc_kernel_end_parallel: a worker retires; the last one frees the
@@ -520,33 +533,30 @@ __device__ __forceinline__ void red_add_if(uint32_t saddr, uint32_t v, bool p) {
                : "memory");
 }
 // retire of a region whose list is the window: args = null, state = Idle
-// (Active and retired 0), work_fn = -1, nargs = 0 (retire_last's window case).
+// with work_fn -1, nargs = 0, Active and retired 0 (retire_last's window
+// case).
 __device__ __forceinline__ void retire_window_if(const TeamCtx &t, bool p) {
   const uint32_t rt = t.rt_s;
-  static_assert(Rt::kArgs == 0 && Rt::kState == 8 && Rt::kWorkFn == 12 && Rt::kNArgs == 16,
+  static_assert(Rt::kArgs == 0 && Rt::kState == 8 && Rt::kNArgs == 12 && Rt::kActive == 16,
                 "rt layout");
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t"
                "@q st.shared.u64 [%0], %2;\n\t"
                "@q st.shared.v2.u32 [%0+8], {%3, %4};\n\t"
-               "@q st.shared.u32 [%0+16], %5;\n\t}" ::"r"(rt),
-               "r"(static_cast<uint32_t>(p)), "l"(0ull),
-               "r"(uint32_t(kIdle) << Rt::kPhaseShift), "r"(0xffffffffu), "r"(0u)
+               "@q st.shared.u32 [%0+16], %4;\n\t}" ::"r"(rt),
+               "r"(static_cast<uint32_t>(p)), "l"(0ull), "r"(state_word(kIdle, -1)), "r"(0u)
                : "memory");
 }
-// staging of a region (stage_region's stores), predicated on `p`: the
-// state word becomes Staged with Active and retired 0 (prepare requires an
-// idle team).
+// staging of a region (stage_region's stores), predicated on `p`: two stores
+// (Active and retired are already 0 -- prepare requires an idle team).
 __device__ __forceinline__ void stage_region_if(const TeamCtx &t, int32_t fn,
                                                 int32_t nargs, void **list, bool p) {
   const uint32_t rt = t.rt_s;
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t"
                "@q st.shared.u64 [%0], %2;\n\t"
-               "@q st.shared.v2.u32 [%0+8], {%3, %4};\n\t"
-               "@q st.shared.u32 [%0+16], %5;\n\t}" ::"r"(rt),
+               "@q st.shared.v2.u32 [%0+8], {%3, %4};\n\t}" ::"r"(rt),
                "r"(static_cast<uint32_t>(p)),
                "l"(reinterpret_cast<unsigned long long>(list)),
-               "r"(uint32_t(kStaged) << Rt::kPhaseShift), "r"(static_cast<uint32_t>(fn)),
-               "r"(static_cast<uint32_t>(nargs))
+               "r"(state_word(kStaged, fn)), "r"(static_cast<uint32_t>(nargs))
                : "memory");
 }
 
@@ -569,19 +579,19 @@ __device__ __forceinline__ bool fetch_is_fast(const StagedState &st,
   return st.phase == kStaged && m.no_events;
 }
 // The fast fetch's bookkeeping, branch-free: Active += n by the warp's
-// leader -- a plain store of the state word (Staged, Active = n) when this
-// warp holds every participant (Active is 0 between regions and no other
-// warp fetches), otherwise one fire-and-forget shared atomic.
+// leader -- a plain store when this warp holds every participant (Active is
+// 0 between regions and no other warp fetches), otherwise one
+// fire-and-forget shared atomic.  The Active word is not one the fetch
+// reads, so no lane of the warp can observe the update early.
 __device__ __forceinline__ void fetch_account_fast(const TeamCtx &t,
                                                    const StagedState &,
                                                    const WarpMask &m) {
   asm volatile("{\n\t.reg .pred qs, qm;\n\t"
-               "setp.ne.u32 qs, %3, 0;\n\t"
-               "setp.ne.u32 qm, %4, 0;\n\t"
-               "@qs st.shared.u32 [%0], %2;\n\t"
-               "@qm red.shared.add.u32 [%0], %1;\n\t}" ::"r"(t.rt_s + Rt::kState),
-               "r"(m.n), "r"((uint32_t(kStaged) << Rt::kPhaseShift) | m.n),
-               "r"(static_cast<uint32_t>(m.is_leader && m.sole)),
+               "setp.ne.u32 qs, %2, 0;\n\t"
+               "setp.ne.u32 qm, %3, 0;\n\t"
+               "@qs st.shared.u32 [%0], %1;\n\t"
+               "@qm red.shared.add.u32 [%0], %1;\n\t}" ::"r"(t.rt_s + Rt::kActive),
+               "r"(m.n), "r"(static_cast<uint32_t>(m.is_leader && m.sole)),
                "r"(static_cast<uint32_t>(m.is_leader && !m.sole))
                : "memory");
 }
@@ -678,7 +688,7 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
       // Active -= n); the join barrier orders every retirement before the
       // master, which observes retired == W and completes the last
       // retirement (complete_region) -- no returning atomic on any worker.
-      red_add_if(t.rt_s + Rt::kState, (n << Rt::kRetiredShift) - n, leader);
+      red_add_if(t.rt_s + Rt::kActive, (n << Rt::kRetiredShift) - n, leader);
     }
     return;
   }
@@ -708,14 +718,14 @@ __device__ __forceinline__ void end_parallel_warp(const TeamCtx &t,
 #endif
   if (leader) {
     const uint32_t w = static_cast<uint32_t>(t.at<int32_t>(Rt::kWorkers));
-    // retired += n, Active -= n (>= n: our own fetch); the phase byte is
-    // untouched (the 12-bit fields never carry).  acq_rel at CTA scope: every
+    // retired += n (high half), Active -= n (low half; >= n: our own fetch).
+    // acq_rel at CTA scope: every
     // participant's reads of the staged region happen-before the last
     // retiree's bookkeeping writes (retire_last).
     uint32_t old;
     asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
                  : "=r"(old)
-                 : "r"(t.rt_s + Rt::kState),
+                 : "r"(t.rt_s + Rt::kActive),
                    "r"((n << Rt::kRetiredShift) - n)
                  : "memory");
     const uint32_t before = (old >> Rt::kRetiredShift) & Rt::kActiveMask;
@@ -740,7 +750,7 @@ __device__ __forceinline__ void end_parallel_window(const TeamCtx &t, uint32_t p
     __syncwarp(); // every lane's fetch reads before the leader's reset
     retire_window_if(t, leader);
   } else {
-    red_add_if(t.rt_s + Rt::kState, (n << Rt::kRetiredShift) - n, leader);
+    red_add_if(t.rt_s + Rt::kActive, (n << Rt::kRetiredShift) - n, leader);
   }
 }
 // Master warp, after the join barrier of a region it staged with the window

@@ -477,7 +477,7 @@ __global__ void OMPDS_GENERIC_LB
     smem[i] = 0;
   __syncthreads();
   if (threadIdx.x == 0)
-    t.work_fn() = -1;
+    t.set_work_fn(-1);
   __syncthreads();
 
   if (warp < worker_warps) {

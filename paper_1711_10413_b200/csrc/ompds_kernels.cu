@@ -861,7 +861,7 @@ __global__ void rt_replay_kernel(ompds_runtime_config cfg,
   const int64_t region = team_region_bytes(0, cfg.prealloc_entries);
   for (int64_t i = 0; i < region; ++i)
     smem[i] = 0;
-  t.work_fn() = -1;
+  t.set_work_fn(-1);
   int32_t fn_seq = 0;
   for (int32_t i = 0; i < n; ++i) {
     const ompds_rt_call c = calls[i];

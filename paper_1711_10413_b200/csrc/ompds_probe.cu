@@ -196,6 +196,11 @@ extern "C" int32_t ompds_probe_overheads(ompds_overhead_probe *io, void *stream)
   long long *dev = reinterpret_cast<long long *>(chain + round_up(chain_bytes, 256));
   ProbeArgs a{r.iterations, r.frame_bytes, r.lanes, r.max_depth, r.seed,
               static_cast<uint32_t>(kProbeSlot), chain, chain_bytes, 0u};
+  cudaError_t z = cudaMemsetAsync(dev, 0, sizeof h, st); // every slot defined
+  if (z != cudaSuccess) {
+    cudaFree(chain);
+    return cuda_fail(z, "ompds_probe_overheads");
+  }
   ProbeArgs warm = a; // the chain's first touch (TLB, L2) is not a push/pop cost
   warm.iters = a.iters < 256 ? a.iters : 256;
   probe_stack_kernel<3><<<1, 32, 0, st>>>(warm, dev);

@@ -242,10 +242,10 @@ int32_t ompds_team_create(const ompds_runtime_config *config, uint64_t prealloc_
     e = cudaHostAlloc(reinterpret_cast<void **>(&h->out), sizeof(StepOut), cudaHostAllocMapped);
   if (e == cudaSuccess)
     e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&h->out_dev), h->out, 0);
-  if (e == cudaSuccess) { // work_fn = -1 (no staged region), as generic kernels start
-    int32_t none = -1;
+  if (e == cudaSuccess) { // Uninitialized, work_fn = -1, as generic kernels start
+    const uint32_t none = state_word(kUninit, -1);
     e = cudaMemcpy(h->state + config->prealloc_entries * OMPDS_SHARED_ARG_ENTRY_BYTES +
-                       Rt::kWorkFn,
+                       Rt::kState,
                    &none, 4, cudaMemcpyHostToDevice);
   }
   if (e != cudaSuccess) {
@@ -280,7 +280,7 @@ int32_t ompds_team_kernel_init(ompds_team *h, int32_t role, int32_t workers) {
 
 int32_t ompds_team_prepare_parallel(ompds_team *h, int32_t role, int32_t fn, int64_t nargs,
                                     uint64_t *args_addr) {
-  if (!valid(h, role) || !args_addr || fn < 0)
+  if (!valid(h, role) || !args_addr || fn < 0 || fn > kMaxWorkFn)
     return OMPDS_ERR_INVALID;
   if (int32_t s = team_launch(h, kStepPrepareCheck, role, nargs))
     return s;

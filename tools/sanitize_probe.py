@@ -65,6 +65,30 @@ def main():
     for st in sts:
         RG.release_workspace(st)
     RG.probe_overheads(64)
+    RG.probe_overheads(64, frame_bytes=256, max_depth=4, lanes=8)
+    # nested region programs (per-lane data-sharing stacks, globalized frames)
+    import nested_programs as NP
+    for p in NP.corpus()[:4]:
+        lays = PG.derive_layouts(p["ast"], p["kernel"])
+        prog = PG.compile_program(p["ast"], lays, p["kernel"], p["teams"], p["workers"])
+        for slot, ovf in ((4096, 32768), (0, 32768)):
+            bufs = [torch.zeros(sz, dtype=torch.int32, device=dev) for _, sz, _ in prog.buffers]
+            PG.run_program(prog, bufs, stack_slot_bytes=slot, stack_overflow_bytes=ovf)
+    # per-thread barrier arrivals (general instantiation)
+    a = torch.zeros(2 * 40, dtype=torch.int32, device=dev)
+    arr = torch.zeros(2 * 72, dtype=torch.int32, device=dev)
+    RG.run_regions(a, 2, 40, 3, barrier_arrivals=arr)
+    # the stateful team handle (one launch per protocol call)
+    from paper_1711_10413_b200 import runtime as R
+    rt = R.TeamRuntime(R.RuntimeConfig(), 0x2000, R.RecordingHeap())
+    rt.kernelInit(R.MASTER, 2)
+    for nargs in (3, 25):
+        rt.prepareParallel(R.MASTER, "wf", nargs)
+        for _ in range(2):
+            rt.kernelParallel(R.WORKER)
+        for _ in range(2):
+            rt.endParallel(R.WORKER)
+    rt.kernelDeinit(R.MASTER)
     torch.cuda.synchronize()
     print("sanitize probe done")
 
