@@ -46,8 +46,14 @@ inline int32_t cuda_fail(cudaError_t e, const char *what) {
 // Launch parameters shared by every generic-mode kernel.
 //===----------------------------------------------------------------------===//
 
+#ifndef OMPDS_GENERIC_LB_THREADS
+#define OMPDS_GENERIC_LB_THREADS 1024 // any team up to 1024 threads ...
+#endif
+#ifndef OMPDS_GENERIC_LB_MIN
+#define OMPDS_GENERIC_LB_MIN 1 // ... so at most 64 registers
+#endif
 #ifndef OMPDS_GENERIC_LB
-#define OMPDS_GENERIC_LB __launch_bounds__(1024, 1)
+#define OMPDS_GENERIC_LB __launch_bounds__(OMPDS_GENERIC_LB_THREADS, OMPDS_GENERIC_LB_MIN)
 #endif
 
 constexpr int kMaxCaptures = 32;
