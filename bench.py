@@ -589,8 +589,23 @@ def regions_section(RG, torch, dist, dev, stream, sms, rank, world):
                  "same accesses at fixed addresses) per pair; bookkeeping = the push/pop "
                  "dependent chain with no frame access; handoff = release + join named "
                  "barriers between the master and one worker warp")
+    # the reference-facing boundary: one omplab::TeamRuntime operation
+    # through the stateful team handle (a launch + a stream sync each)
+    from paper_1711_10413_b200 import runtime as RT
+    rt = RT.TeamRuntime(RT.RuntimeConfig(), 0x2000, RT.RecordingHeap())
+    rt.kernelInit(RT.MASTER, 1)
+    n_calls = 0
+    t0 = time.perf_counter()
+    for _ in range(300):
+        rt.prepareParallel(RT.MASTER, "wf", 4)
+        rt.kernelParallel(RT.WORKER)
+        rt.endParallel(RT.WORKER)
+        n_calls += 3
+    handle_us = (time.perf_counter() - t0) / n_calls * 1e6
+    del rt
     return {"ns_per_region": round(ns_per_region, 1),
             "ns_per_region_int_analog": round(ns_int, 1),
+            "team_handle_us_per_call": round(handle_us, 2),
             "regions_per_s": round(1e9 / ns_per_region, 1),
             "sm_clock_mhz_around": [clk_before, clk_after],
             "smem_bytes_per_cta": smem1,

@@ -282,13 +282,20 @@ int32_t ompds_team_prepare_parallel(ompds_team *h, int32_t role, int32_t fn, int
                                     uint64_t *args_addr) {
   if (!valid(h, role) || !args_addr || fn < 0 || fn > kMaxWorkFn)
     return OMPDS_ERR_INVALID;
-  if (int32_t s = team_launch(h, kStepPrepareCheck, role, nargs))
-    return s;
-  if (h->out->status != OMPDS_OK)
-    return h->out->status;
+  // A list that fits the window (or a FailDynamicAlloc team, whose heap is
+  // never asked) needs no allocator call: one launch does the whole
+  // prepare.  Otherwise a first launch runs the checks, then the heap is
+  // asked, then the region is staged with its block.
+  const bool may_alloc = nargs > h->cfg.prealloc_entries && !h->cfg.fail_dynamic_alloc;
+  if (may_alloc) {
+    if (int32_t s = team_launch(h, kStepPrepareCheck, role, nargs))
+      return s;
+    if (h->out->status != OMPDS_OK)
+      return h->out->status;
+  }
   uint64_t block = 0;
   int64_t bytes = 0;
-  if (h->out->need_alloc) {
+  if (may_alloc && h->out->need_alloc) {
     bytes = h->out->need_bytes;
     block = h->alloc ? h->alloc(bytes, h->user) : 0;
     if (block == 0) // Heap.allocate returned 0 (DeviceRuntime.cpp:67-69)
