@@ -263,7 +263,7 @@ __device__ __forceinline__ TeamCtx make_team(unsigned char *smem,
 // compiler cannot sink a later load below a branch on an earlier one (one
 // shared-memory round trip instead of a chain).
 struct PrepareState {
-  uint8_t phase;
+  uint32_t phase;
   int32_t active;
 };
 __device__ __forceinline__ PrepareState load_prepare_state(const TeamCtx &t) {
@@ -274,11 +274,10 @@ __device__ __forceinline__ PrepareState load_prepare_state(const TeamCtx &t) {
                : "r"(t.rt_s)
                : "memory");
   static_assert(Rt::kState == 8 && Rt::kActive == 16, "rt layout");
-  return PrepareState{static_cast<uint8_t>(sw >> Rt::kPhaseShift),
-                      static_cast<int32_t>(aw & Rt::kActiveMask)};
+  return PrepareState{sw >> Rt::kPhaseShift, static_cast<int32_t>(aw & Rt::kActiveMask)};
 }
 struct StagedState {
-  uint8_t phase;
+  uint32_t phase; // the state word's top byte (uint32: one compare, no byte sign-extension)
   int32_t fn;
   int32_t nargs;
   void **args; // the staged list (loaded only when the caller needs it)
@@ -319,7 +318,7 @@ __device__ __forceinline__ StagedState load_staged_state(const TeamCtx &t,
                  : "r"(rt)
                  : "memory");
   void **list = kArgs ? reinterpret_cast<void **>(args) : t.window;
-  return StagedState{static_cast<uint8_t>(sw >> Rt::kPhaseShift), state_fn(sw),
+  return StagedState{sw >> Rt::kPhaseShift, state_fn(sw),
                      static_cast<int32_t>(na), list, reinterpret_cast<void *>(win)};
 }
 
@@ -345,7 +344,7 @@ __device__ inline int32_t kernel_init(const TeamCtx &t, int role,
 // The phase checks of prepareParallel in the reference's order
 // (DeviceRuntime.cpp:46-60), as a pure function of the team state so a warp
 // can evaluate them on broadcast loads.
-__device__ __forceinline__ int32_t prepare_check(uint8_t ph, int32_t active,
+__device__ __forceinline__ int32_t prepare_check(uint32_t ph, int32_t active,
                                                  int64_t nargs) {
   if (ph == kUninit)
     return OMPDS_TRAP_PREPARE_BEFORE_INIT;
@@ -576,7 +575,7 @@ __device__ __forceinline__ Fetch fetch_from(const StagedState &st) {
 }
 __device__ __forceinline__ bool fetch_is_fast(const StagedState &st,
                                               const WarpMask &m) {
-  return st.phase == kStaged && m.no_events;
+  return st.phase == uint32_t(kStaged) && m.no_events;
 }
 // The fast fetch's bookkeeping, branch-free: Active += n by the warp's
 // leader -- a plain store when this warp holds every participant (Active is
@@ -600,7 +599,7 @@ __device__ __forceinline__ void fetch_account_fast(const TeamCtx &t,
 __device__ OMPDS_GENERAL_INLINE Fetch fetch_general(const TeamCtx &t, const StagedState &st,
                                             const WarpMask &m, bool mine) {
   Fetch f = fetch_from(st);
-  const uint8_t ph = st.phase;
+  const uint32_t ph = st.phase;
   if (ph == kTerminated) {
     f.fn = -1;
     f.args = nullptr;
