@@ -184,3 +184,35 @@ def test_handle_calls_are_constant_time():
     late = time.perf_counter() - t0
     assert late < 3 * early, (early, late)
     assert len(rt.events()) == 1 + 3 * 1010
+
+
+def test_handle_rejects_bad_arguments_and_traps_leave_state():
+    """C-ABI edge cases of the team handle: an out-of-range role or work
+    function id is OMPDS_ERR_INVALID before any launch; a trapped call
+    leaves the phase, counters and event log exactly as they were."""
+    import ctypes as C
+    lib = P.lib()
+    rt = live(workers=2)
+    h = rt._h
+    addr = C.c_uint64()
+    assert lib.ompds_team_prepare_parallel(h, 7, 0, 1, C.byref(addr)) == P.ERR_INVALID
+    assert lib.ompds_team_prepare_parallel(h, R.MASTER, 1 << 23, 1, C.byref(addr)) == \
+        P.ERR_INVALID
+    assert lib.ompds_team_prepare_parallel(h, R.MASTER, -1, 1, C.byref(addr)) == P.ERR_INVALID
+    n_events = len(rt.events())
+    # traps: fetch with nothing staged, end with nothing active, worker deinit
+    assert rt.kernelParallel(R.WORKER)[0].trap_reason == \
+        "protocol error: kernel_parallel with no staged region"
+    assert rt.endParallel(R.WORKER).trap_reason == \
+        "protocol error: end_parallel with no active region"
+    assert rt.kernelDeinit(R.WORKER).trap_reason == \
+        "protocol error: kernel_deinit from a worker thread"
+    assert len(rt.events()) == n_events and not rt.terminated()
+    # the largest work-function id (24-bit field in the state word) round-trips
+    big = (1 << 23) - 1
+    assert lib.ompds_team_prepare_parallel(h, R.MASTER, big, 3, C.byref(addr)) == 0
+    fn = C.c_int32()
+    part = C.c_int32()
+    assert lib.ompds_team_kernel_parallel(h, R.WORKER, C.byref(fn), C.byref(addr),
+                                          C.byref(part)) == 0
+    assert fn.value == big and part.value == 1 and addr.value == 0x2000
