@@ -276,6 +276,18 @@ __device__ __forceinline__ PrepareState load_prepare_state(const TeamCtx &t) {
   static_assert(Rt::kState == 8 && Rt::kActive == 16, "rt layout");
   return PrepareState{sw >> Rt::kPhaseShift, static_cast<int32_t>(aw & Rt::kActiveMask)};
 }
+// The fast path of prepare_parallel reads only the phase: the protocol
+// keeps Idle => Active == 0 (Active rises only while a region is Staged, and
+// the retirement that brings it back to 0 is the one that returns the team
+// to Idle -- DeviceRuntime.cpp:81-128), so "Idle" already implies "no region
+// in flight"; the general path loads Active too and checks both in the
+// reference's order.
+__device__ __forceinline__ uint32_t load_phase(const TeamCtx &t) {
+  uint32_t sw;
+  asm volatile("ld.shared.u32 %0, [%1+8];" : "=r"(sw) : "r"(t.rt_s) : "memory");
+  static_assert(Rt::kState == 8, "rt layout");
+  return sw >> Rt::kPhaseShift;
+}
 struct StagedState {
   uint32_t phase; // the state word's top byte (uint32: one compare, no byte sign-extension)
   int32_t fn;

@@ -225,9 +225,8 @@ struct Master {
     // The common case of prepare_parallel in one branch: every check passes,
     // the list fits the window and no event log is kept.  Everything else
     // (traps, a global list, events) takes parallel_general.
-    const PrepareState st = load_prepare_state(t);
-    if (__builtin_expect(st.phase == kIdle && st.active == 0 && nargs >= 0 &&
-                             nargs <= fast_nargs, 1)) {
+    const uint32_t phase = load_phase(t); // Idle implies Active == 0
+    if (__builtin_expect(phase == uint32_t(kIdle) && nargs >= 0 && nargs <= fast_nargs, 1)) {
       __syncwarp(); // every lane has read the state before the master stages
       OMPDS_TL(regions, 1);
       stage_region_if(t, fn, nargs, t.window, leader);
@@ -253,8 +252,10 @@ struct Master {
       regions += 1;
       return OMPDS_OK;
     }
-    if (lean)
+    if (lean) {
+      const PrepareState st = load_prepare_state(t);
       return parallel_refused(prepare_check(st.phase, st.active, nargs));
+    }
     return parallel_general(fn, nargs, addr_of);
   }
 

@@ -183,11 +183,43 @@ template <class T> struct SharedArrayProg {
     __syncwarp();
     m.parallel(0, 1);
   }
+  using Vec = typename std::conditional<sizeof(T) == 8, double2, int4>::type;
+  // d[] read through the captured pointer: 16-byte shared-memory loads when
+  // the depot (and so d[]) is in the team's smem slot -- the placement
+  // decision's common side -- else generic loads (the depot on the chain).
+  struct SmemD {
+    uint32_t base;
+    __device__ __forceinline__ Vec vec(int k) const {
+      Vec v;
+      if constexpr (sizeof(T) == 8)
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y)
+                     : "r"(base + 8u * uint32_t(k)));
+      else
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "r"(base + 4u * uint32_t(k)));
+      return v;
+    }
+  };
+  struct GenericD {
+    const T *p;
+    __device__ __forceinline__ Vec vec(int k) const {
+      return *reinterpret_cast<const Vec *>(p + k);
+    }
+  };
   __device__ static void region(int32_t, const SharedVars &sv, const Worker &w,
                                 const Args &a) {
     const T *d = static_cast<const T *>(sv.get(0));
     if (!w.mine)
       return;
+    if (__isShared(d))
+      stream(SmemD{static_cast<uint32_t>(__cvta_generic_to_shared(d))}, d, w, a);
+    else
+      stream(GenericD{d}, d, w, a);
+  }
+  template <class DA>
+  __device__ static __forceinline__ void stream(const DA &da, const T *d, const Worker &w,
+                                                const Args &a) {
     // the shard's own element range: local team indices (config 5 shards
     // elements across GPUs; each launch sees its slice)
     const int64_t gid = int64_t(w.local_team) * w.workers + w.wid;
@@ -195,13 +227,12 @@ template <class T> struct SharedArrayProg {
     // Cyclic schedule over 16-byte units (AstLowering.cpp:429-462 applied
     // to vectors; the body is element-wise, so results are identical).
     constexpr int V = 16 / sizeof(T);
-    using Vec = typename std::conditional<sizeof(T) == 8, double2, int4>::type;
     const int64_t units = a.n / V;
     Vec *av = reinterpret_cast<Vec *>(a.a);
     auto body = [&](Vec &v, int64_t u) {
       T *e = reinterpret_cast<T *>(&v);
       const int base = static_cast<int>((u * V) & (kLen - 1));
-      const Vec dv = *reinterpret_cast<const Vec *>(d + base);
+      const Vec dv = da.vec(base);
       const T *de = reinterpret_cast<const T *>(&dv);
 #pragma unroll
       for (int k = 0; k < V; ++k)
