@@ -203,10 +203,21 @@ def cpu_baseline(n_sample, threads):
         if el > 10.0 or reps >= 60:  # ~10 s of CPU work
             break
     gbs = BYTES_PER_ELEM * n_sample * reps / el / 1e9
+    # the regions/s half: the config-1 body (1 team x 32 workers, 4 shared
+    # scalars, 10^4 regions) as the port runs it -- sequential, one thread
+    # (orc_regions: the semantics only, no protocol to execute)
+    R = 10_000
+    a = np.zeros(32)
+    t0 = time.perf_counter()
+    L.orc_regions(1, 1, 32, R, O.ptr(a))
+    ns_region = (time.perf_counter() - t0) / R * 1e9
     return {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
             "cpu_model": cpu_model(),
             "sample": f"{n_sample} fp64 elements x {reps} passes of the config-4 body "
-                      f"(oracle/ompds_oracle.c orc_stream, OpenMP {threads} threads)"}
+                      f"(oracle/ompds_oracle.c orc_stream, OpenMP {threads} threads)",
+            "regions": {"ns_per_region": round(ns_region, 1), "cores": 1,
+                        "sample": f"config 1 body, 1 team x 32 workers, {R} regions "
+                                  "(orc_regions, sequential; no runtime protocol)"}}
 
 
 def run_reference(args):
