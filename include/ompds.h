@@ -556,8 +556,10 @@ typedef struct ompds_program {
 int32_t ompds_program_verify(const ompds_program *prog);
 
 /* Runs a verified program (asynchronous on launch->stream; the descriptor
- * and its arrays may be freed when the call returns).  Not capturable into
- * a CUDA graph: the tables are staged from pageable host memory. */
+ * and its arrays may be freed when the call returns).  The tables are copied
+ * to the stream's workspace only when they differ from the last ones staged
+ * there, so after one eager launch the same program (same tables and
+ * buffers) can be captured into a CUDA graph. */
 int32_t ompds_run_program(const ompds_launch *launch, const ompds_program *prog,
                           ompds_team_stats *stats_dev, ompds_event *events_dev);
 

@@ -596,6 +596,11 @@ struct WsBuffers {
   unsigned char *buf[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t bytes[4] = {0, 0, 0, 0};
   std::vector<unsigned char *> retired;
+  // the region-program tables last copied into buf[2] (ompds_run_program
+  // skips the copy when a launch stages the same bytes again, so launches
+  // of a staged program can be captured into a CUDA graph)
+  std::vector<unsigned char> staged;
+  unsigned char *staged_at = nullptr;
 };
 struct Workspace {
   std::mutex mu;
@@ -620,6 +625,22 @@ inline int32_t ensure_buffer(int which, size_t bytes, unsigned char **out,
   }
   *out = w.buf[which];
   return OMPDS_OK;
+}
+
+// Whether `tables` are already the contents of `dev` (buffer 2 of the
+// stream's set); records them as such when not (the caller copies).
+inline bool tables_staged(void *stream, const std::vector<unsigned char> &tables,
+                          unsigned char *dev) {
+  std::lock_guard<std::mutex> lk(g_ws.mu);
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess)
+    return false;
+  WsBuffers &w = g_ws.sets[{d, stream}];
+  if (w.staged_at == dev && w.staged == tables)
+    return true;
+  w.staged = tables;
+  w.staged_at = dev;
+  return false;
 }
 
 inline int32_t release_workspace(void *stream) {

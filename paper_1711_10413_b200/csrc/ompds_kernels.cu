@@ -1431,7 +1431,29 @@ int32_t ompds_run_program(const ompds_launch *launch, const ompds_program *pr,
   if (s)
     return s;
   cudaStream_t st = static_cast<cudaStream_t>(launch->stream);
-  OMPDS_CUDA(cudaMemcpyAsync(dev, host.data(), total, cudaMemcpyHostToDevice, st));
+  // Copied only when they differ from what this stream's buffer holds (the
+  // copy is ordered before the kernel by the stream; earlier launches on the
+  // stream that read the old tables are ordered before the copy).  A
+  // program launched again with the same tables and buffers therefore
+  // issues no copy, so it can be captured into a CUDA graph after one
+  // eager launch.
+  if (!tables_staged(launch->stream, host, dev)) {
+    // a copy from this pageable buffer must not be captured: a graph would
+    // replay it from freed memory
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    OMPDS_CUDA(cudaStreamIsCapturing(st, &cap));
+    if (cap != cudaStreamCaptureStatusNone) {
+      tables_staged(launch->stream, {}, nullptr);
+      std::snprintf(g_last_error, sizeof(g_last_error),
+                    "ompds_run_program: launch the program once outside the capture first");
+      return OMPDS_ERR_INVALID;
+    }
+    cudaError_t e = cudaMemcpyAsync(dev, host.data(), total, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) {
+      tables_staged(launch->stream, {}, nullptr); // forget: the copy failed
+      return cuda_fail(e, "ompds_run_program: table copy");
+    }
+  }
   FixedLayout lay;
   lay.total_shared = pr->total_shared;
   ProgramProg::Args a{reinterpret_cast<const int32_t *>(dev),
@@ -1442,10 +1464,10 @@ int32_t ompds_run_program(const ompds_launch *launch, const ompds_program *pr,
                       std::max<int64_t>(pr->total_local, 4),
                       pr->step_limit > 0 ? pr->step_limit : int64_t(20000000)};
   // Asynchronous like the other launchers: the tables were copied out of
-  // `host` (pageable) before cudaMemcpyAsync returned, and the next launch's
+  // `host` (pageable) before cudaMemcpyAsync returned, and a later launch's
   // copy into the same workspace buffer is ordered behind this kernel by the
-  // stream (ensure_buffer synchronizes the stream before it ever frees it).
-  // per worker warp: the lanes' data-sharing stacks (nested regions)
+  // stream (superseded workspace buffers are retired, never freed early).
+  // Per worker warp: the lanes' data-sharing stacks (nested regions).
   return launch_generic<ProgramProg>(launch, lay, 0, a, stats, events, pr->stack_slot_bytes,
                                      pr->stack_overflow_bytes, /*allow_lean=*/false);
 }

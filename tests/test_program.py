@@ -550,3 +550,39 @@ def test_gpu_runaway_programs_hit_the_step_limit():
     assert [s.trap for s in out.team_stats()] == [0] * t
     for (name, _, _), b in zip(prog.buffers, bufs):
         assert b.cpu().tolist() == run["sim"]["globals"][name]
+
+
+@pytest.mark.gpu
+def test_gpu_program_launches_replay_from_a_cuda_graph():
+    """After one eager launch has staged a program's tables on a stream, the
+    same launch issues no table copy and can be captured into a CUDA graph;
+    every replay is one more run of the program (two_regions adds c to a[]
+    twice per run).  Capturing a program whose tables are not staged is
+    refused instead of recording a copy from freed host memory."""
+    import torch
+    p = next(x for x in G.load("corpus") if x["stem"] == "two_regions")
+    t, w, run = launches(p)[0]
+    prog = PG.compile_program(p["ast"], our_layouts(p), p["kernel"], t, w)
+    s = torch.cuda.Stream()
+    buf = torch.zeros(prog.buffers[0][1], dtype=torch.int32, device="cuda")
+    with torch.cuda.stream(s):
+        PG.run_program(prog, [buf], stream=s)
+    s.synchronize()
+    one = buf.clone()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        PG.run_program(prog, [buf], stream=s)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert buf.cpu().tolist() == (one * 4).cpu().tolist()
+    # a different program (other tables) cannot be captured before it is staged
+    p2 = next(x for x in G.load("corpus") if x["stem"] == "shared_scalar")
+    t2, w2, _ = launches(p2)[0]
+    prog2 = PG.compile_program(p2["ast"], our_layouts(p2), p2["kernel"], t2, w2)
+    buf2 = torch.zeros(prog2.buffers[0][1], dtype=torch.int32, device="cuda")
+    g2 = torch.cuda.CUDAGraph()
+    from paper_1711_10413_b200 import _lib as L
+    with pytest.raises(L.OmpdsError):
+        with torch.cuda.graph(g2, stream=s):
+            PG.run_program(prog2, [buf2], stream=s)
