@@ -136,13 +136,18 @@ def ptxas_registers(log_path: str) -> dict:
     return out
 
 
-# (kernel key substring, config, threads per team, team footprint bytes)
+# (kernel instantiation, what it runs, threads per team, team region bytes);
+# "ELb1E" = the lean instantiation the config launchers use, "ELb0E" = the
+# general one (event log / allocation hook / spilled lists / programs)
 B200_KERNELS = [
-    ("RegionsProgIiE", "config1 int (loop layout)", 64, 56 + 160 + 49),
-    ("SharedArrayProgIdE", "config2 f64", 512, 2072 + 160 + 49),
-    ("NestedProgIdE", "config3 f64 (2 KB warp slots x 3)", 128, 96 * 0 + 304 + 3 * 2048),
-    ("StreamProgIdE", "config4 f64", 128, 80 + 160 + 49),
-    ("ProgramProgE", "reference programs (scalars_4 footprint)", 128, 48 + 160 + 49),
+    ("RegionsProgIiEELb1E", "config1 int (loop layout) lean", 64, 56 + 160 + 49),
+    ("RegionsProgIdEELb1E", "config1 int+f64 (loop layout) lean", 64, 56 + 160 + 49),
+    ("RegionsProgIdEELb0E", "config1 general", 64, 56 + 160 + 49),
+    ("SharedArrayProgIdEELb1E", "config2 f64 lean", 512, 2072 + 160 + 49),
+    ("NestedProgIdEELb1E", "config3 f64 (2 KB warp slots x 3) lean", 128,
+     96 * 0 + 304 + 3 * 2048),
+    ("StreamProgIdEELb1E", "config4 f64 lean", 128, 80 + 160 + 49),
+    ("ProgramProgELb0E", "reference programs (scalars_4 footprint)", 128, 48 + 160 + 49),
 ]
 
 

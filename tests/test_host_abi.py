@@ -212,12 +212,15 @@ def test_b200_kernel_occupancy_table_from_ptxas_log():
     log = os.path.join(ROOT, "paper_1711_10413_b200", "_build", "ptxas.log")
     csv = occupancy.b200_kernel_occupancy_csv(log)
     rows = [r.split(",") for r in csv.strip().splitlines()[1:]]
-    assert {r[0] for r in rows} >= {"RegionsProgIiE", "StreamProgIdE", "SharedArrayProgIdE"}
+    assert {r[0] for r in rows} >= {"RegionsProgIiEELb1E", "StreamProgIdEELb1E",
+                                    "SharedArrayProgIdEELb1E"}
     for r in rows:
         regs, thr = int(r[2]), int(r[3])
-        # teams_by_regs: per-warp allocation, registers rounded up to 8
+        # teams_by_regs: per-warp allocation, registers rounded up to 8, each
+        # warp inside one of the four 16K-register sub-partitions
         warps = (thr + 31) // 32
-        assert int(r[5]) == 65536 // (((regs + 7) // 8 * 8) * 32 * warps)
+        per_part = 16384 // (((regs + 7) // 8 * 8) * 32)
+        assert int(r[5]) == 4 * per_part // warps
 
 
 @pytest.mark.parametrize("first,teams,total", [(-1, 2, 4), (3, 2, 4), (1, 2, 0), (0, 2, -1)])
