@@ -546,16 +546,19 @@ def regions_section(RG, torch, dist, dev, stream, sms, rank, world):
     ai = torch.zeros(32, dtype=torch.int32, device=dev)
     ns_int = device_ms(stream, lambda: RG.run_regions(ai, 1, 32, R, stream=stream)) * 1e6 / R
     clk_after = RG.probe_overheads(1024, stream=stream)["sm_clock_mhz"]
-    # the same protocol on every SM: as many 64-thread teams per SM as the
-    # kernel's registers allow (one wave; 18/SM at 52 registers, the B200 row
-    # of the occupancy model = ncu's launch__occupancy_limit_registers),
-    # 2000 regions each (tools/regs_ab.py: 16/SM 4.32, 18/SM 4.51 G regions/s;
-    # 20/SM runs in two waves, 3.1)
-    # With N ranks the team grid (N x 16 teams/SM) is sharded by range: rank r
-    # launches teams [r*T, (r+1)*T) of the N*T grid (first_team/total_teams),
-    # the whole-job rate is N*T*R2 over the slowest rank's time.
+    # the same protocol on every SM: 64-thread teams (the small-team
+    # instantiation, 32 registers, up to 32 teams/SM by the occupancy model),
+    # 22 per SM in one wave, 2000 regions each.  22 is the measured optimum
+    # (profiles/r2_cfg1_sweep_smallteam.json, tools/cfg1_sweep.py: 16/SM 5.86,
+    # 20/SM 6.36, 22/SM 6.43, 24/SM 6.39, 32/SM 5.95 G regions/s; even counts
+    # keep the 4 SM sub-partitions balanced, and past 24 teams the extra
+    # barrier-waiting warps cost more issue slots than they hide).
+    # With N ranks the team grid (N x T) is sharded by range: rank r launches
+    # teams [r*T, (r+1)*T) of the N*T grid (first_team/total_teams), the
+    # whole-job rate is N*T*R2 over the slowest rank's time.
     from paper_1711_10413_b200 import occupancy as OCC
-    per_sm1 = OCC.occupancy_for("b200", 265, ptxas_regs("RegionsProgIdEELb1E") or 52, 64).actual
+    per_sm1 = min(22, OCC.occupancy_for("b200", 265, ptxas_regs("RegionsProgIdEELb1ELb1E") or 52,
+                                        64).actual)
     R2, teams2 = 2000, sms * per_sm1
     a2 = torch.zeros(world * teams2 * 32, dtype=torch.float64, device=dev)
     rng = dict(first_team=rank * teams2, total_teams=world * teams2)
@@ -621,7 +624,7 @@ def regions_section(RG, torch, dist, dev, stream, sms, rank, world):
             "sm_clock_mhz_around": [clk_before, clk_after],
             "smem_bytes_per_cta": smem1,
             "teams_per_sm": per_sm1,
-            "regs_per_thread": ptxas_regs("RegionsProgIdEELb1E"),
+            "regs_per_thread": ptxas_regs("RegionsProgIdEELb1ELb1E"),
             "workload": "config 1: 1 team x 32 workers, 4 shared scalars (2 int, 2 double), "
                         f"{R} regions in a sequential loop",
             "aggregate_regions_per_s": round(agg_regions_per_s, 0),

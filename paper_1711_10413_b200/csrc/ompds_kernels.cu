@@ -25,6 +25,7 @@ namespace ompds {
 //===----------------------------------------------------------------------===//
 
 template <class T> struct RegionsProg {
+  static constexpr bool kSmallTeams = true; // config 1: 64-thread teams
   struct Args {
     T *a;
     int32_t regions;

@@ -137,12 +137,16 @@ def ptxas_registers(log_path: str) -> dict:
 
 
 # (kernel instantiation, what it runs, threads per team, team region bytes);
-# "ELb1E" = the lean instantiation the config launchers use, "ELb0E" = the
-# general one (event log / allocation hook / spilled lists / programs)
+# "ELb1ELb0E" = the lean instantiation the config launchers use, "ELb0ELb0E" =
+# the general one (event log / allocation hook / spilled lists / programs),
+# "ELb1ELb1E" = the lean small-team one (64 threads, 32 teams/SM bound) a
+# program opting into kSmallTeams gets for W <= 32
 B200_KERNELS = [
-    ("RegionsProgIiEELb1E", "config1 int (loop layout) lean", 64, 56 + 160 + 49),
-    ("RegionsProgIdEELb1E", "config1 int+f64 (loop layout) lean", 64, 56 + 160 + 49),
-    ("RegionsProgIdEELb0E", "config1 general", 64, 56 + 160 + 49),
+    ("RegionsProgIiEELb1ELb1E", "config1 int (loop layout) lean small-team", 64, 56 + 160 + 49),
+    ("RegionsProgIdEELb1ELb1E", "config1 int+f64 (loop layout) lean small-team", 64,
+     56 + 160 + 49),
+    ("RegionsProgIdEELb1ELb0E", "config1 lean W>32", 64, 56 + 160 + 49),
+    ("RegionsProgIdEELb0ELb0E", "config1 general", 64, 56 + 160 + 49),
     ("SharedArrayProgIdEELb1E", "config2 f64 lean", 512, 2072 + 160 + 49),
     ("NestedProgIdEELb1E", "config3 f64 (2 KB warp slots x 3) lean", 128,
      96 * 0 + 304 + 3 * 2048),

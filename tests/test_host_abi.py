@@ -212,7 +212,7 @@ def test_b200_kernel_occupancy_table_from_ptxas_log():
     log = os.path.join(ROOT, "paper_1711_10413_b200", "_build", "ptxas.log")
     csv = occupancy.b200_kernel_occupancy_csv(log)
     rows = [r.split(",") for r in csv.strip().splitlines()[1:]]
-    assert {r[0] for r in rows} >= {"RegionsProgIiEELb1E", "StreamProgIdEELb1E",
+    assert {r[0] for r in rows} >= {"RegionsProgIiEELb1ELb1E", "StreamProgIdEELb1E",
                                     "SharedArrayProgIdEELb1E"}
     for r in rows:
         regs, thr = int(r[2]), int(r[3])

@@ -39,10 +39,10 @@ def main():
         out[f"ns_per_region_1team_{dt}"] = dev_ms(lambda: RG.run_regions(a, 1, 32, R)) * 1e6 / R
     R2 = 2000
     agg = {}
-    for per_sm in (16, 18, 20, 21, 22, 24, 25, 26, 28, 32):
+    for per_sm in [int(x) for x in os.environ.get("PER_SM", "16,18,20,21,22,23,24,25,26,28,30,32").split(",")]:
         teams = sms * per_sm
         a = torch.zeros(teams * 32, dtype=torch.float64, device="cuda")
-        ms = dev_ms(lambda: RG.run_regions(a, teams, 32, R2), reps=3)
+        ms = dev_ms(lambda: RG.run_regions(a, teams, 32, R2), reps=7)
         agg[per_sm] = teams * R2 / (ms * 1e-3)
     out["regions_per_s_by_teams_per_sm"] = agg
     print(json.dumps(out, indent=1))
