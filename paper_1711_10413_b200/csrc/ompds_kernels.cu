@@ -140,6 +140,29 @@ __device__ __forceinline__ void st_stream(double2 *p, double2 v) {
   __stcs(p, v);
 }
 __device__ __forceinline__ void st_stream(int4 *p, int4 v) { __stcs(p, v); }
+// 32-byte vectors (sm_100: LDG/STG.E.EF.ENL2.256, one instruction per 32 B),
+// used when the arrays are 32-byte aligned.
+#ifndef OMPDS_WIDE_UNITS
+#define OMPDS_WIDE_UNITS 2 // 2: 32-byte units when aligned; 1: always 16-byte
+#endif
+struct alignas(32) Vec32 {
+  unsigned long long w[4];
+};
+__device__ __forceinline__ Vec32 ld_stream(const Vec32 *p) {
+  Vec32 r;
+  asm volatile("ld.global.cs.v4.u64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(r.w[0]), "=l"(r.w[1]), "=l"(r.w[2]), "=l"(r.w[3])
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(Vec32 *p, const Vec32 &v) {
+  asm volatile("st.global.cs.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(v.w[0]),
+               "l"(v.w[1]), "l"(v.w[2]), "l"(v.w[3])
+               : "memory");
+}
+
+// the config-2 staging transaction barrier (static shared memory, 8 bytes)
+__shared__ uint64_t stage_bar;
 
 template <class T> struct SharedArrayProg {
   static constexpr int kLen = 256;
@@ -148,25 +171,28 @@ template <class T> struct SharedArrayProg {
     int64_t n;
     const T *d_init; // nullptr: the master's own loop d[k] = 3k+1
   };
+  // cp.async.bulk needs a 16-byte aligned global source (and destination:
+  // the depot slot is 16-aligned in smem); any other d_init view is copied
+  // by the reserved warp like the overflow case below.
+  __device__ static __forceinline__ bool staged_by_tma(const Args &a, bool depot_in_smem) {
+    return a.d_init != nullptr && depot_in_smem &&
+           (reinterpret_cast<uintptr_t>(a.d_init) & 15u) == 0;
+  }
   __device__ static void master(Master &m, const Args &a) {
     T *d = reinterpret_cast<T *>(m.cap(0));
     constexpr uint32_t bytes = kLen * sizeof(T);
-    // cp.async.bulk needs a 16-byte aligned global source (and destination:
-    // the depot slot is 16-aligned in smem); any other d_init view is copied
-    // by the reserved warp like the overflow case below.
-    const bool tma_ok = (reinterpret_cast<uintptr_t>(a.d_init) & 15u) == 0;
-    if (a.d_init != nullptr && m.depot.in_smem && tma_ok) {
-      // TMA staging: the args window is idle until the first prepare, so
-      // its first 8 bytes host the transfer's mbarrier -- no extra smem.
-      uint64_t *bar = reinterpret_cast<uint64_t *>(m.t.window);
+    if (staged_by_tma(a, m.depot.in_smem)) {
+      // TMA staging, completed asynchronously: the master issues the bulk
+      // copy and goes straight on to prepare and release the region; the
+      // workers issue their first loads of a[] and then wait on the
+      // transaction barrier before the first read of d[] (the TMA latency
+      // overlaps theirs instead of delaying the release).  The mbarrier is
+      // 8 bytes of static shared memory beside the team region.
       if (m.leader) {
-        mbar_init(bar, 1);
+        mbar_init(&stage_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        mbar_expect_tx(bar, bytes);
-        bulk_g2s(d, a.d_init, bytes, bar);
-        mbar_wait(bar, 0);
-        mbar_inval(bar);
-        *bar = 0;
+        mbar_expect_tx(&stage_bar, bytes);
+        bulk_g2s(d, a.d_init, bytes, &stage_bar);
       }
       __syncwarp();
     } else if (a.d_init != nullptr) {
@@ -183,6 +209,12 @@ template <class T> struct SharedArrayProg {
       *reinterpret_cast<int32_t *>(m.depot.base + m.p->aux_off) = kLen;
     __syncwarp();
     m.parallel(0, 1);
+    // the copy has completed before any worker read d[]; a launch whose
+    // workers had no element still must not retire the CTA under it
+    if (staged_by_tma(a, m.depot.in_smem) && m.leader) {
+      mbar_wait(&stage_bar, 0);
+      mbar_inval(&stage_bar);
+    }
   }
   using Vec = typename std::conditional<sizeof(T) == 8, double2, int4>::type;
   // d[] read through the captured pointer: 16-byte shared-memory loads when
@@ -190,6 +222,11 @@ template <class T> struct SharedArrayProg {
   // decision's common side -- else generic loads (the depot on the chain).
   struct SmemD {
     uint32_t base;
+    bool staged; // d[] arrives by TMA: wait on the transaction barrier once
+    __device__ __forceinline__ void ready() const {
+      if (staged)
+        mbar_wait(&stage_bar, 0);
+    }
     __device__ __forceinline__ Vec vec(int k) const {
       Vec v;
       if constexpr (sizeof(T) == 8)
@@ -204,40 +241,52 @@ template <class T> struct SharedArrayProg {
   };
   struct GenericD {
     const T *p;
+    __device__ __forceinline__ void ready() const {}
     __device__ __forceinline__ Vec vec(int k) const {
       return *reinterpret_cast<const Vec *>(p + k);
     }
   };
   __device__ static void region(int32_t, const SharedVars &sv, const Worker &w,
                                 const Args &a) {
+    region_units<Vec>(sv, w, a);
+  }
+  template <class U>
+  __device__ static __forceinline__ void region_units(const SharedVars &sv, const Worker &w,
+                                                      const Args &a) {
     const T *d = static_cast<const T *>(sv.get(0));
     if (!w.mine)
       return;
     if (__isShared(d))
-      stream(SmemD{static_cast<uint32_t>(__cvta_generic_to_shared(d))}, d, w, a);
+      stream<U>(SmemD{static_cast<uint32_t>(__cvta_generic_to_shared(d)),
+                      staged_by_tma(a, true)},
+                d, w, a);
     else
-      stream(GenericD{d}, d, w, a);
+      stream<U>(GenericD{d}, d, w, a);
   }
-  template <class DA>
+  template <class U, class DA>
   __device__ static __forceinline__ void stream(const DA &da, const T *d, const Worker &w,
                                                 const Args &a) {
     // the shard's own element range: local team indices (config 5 shards
     // elements across GPUs; each launch sees its slice)
     const int64_t gid = int64_t(w.local_team) * w.workers + w.wid;
     const int64_t pool = int64_t(w.local_teams) * w.workers;
-    // Cyclic schedule over 16-byte units (AstLowering.cpp:429-462 applied
-    // to vectors; the body is element-wise, so results are identical).
-    constexpr int V = 16 / sizeof(T);
+    // Cyclic schedule over U-sized units (16 or 32 bytes; AstLowering.cpp:
+    // 429-462 applied to vectors; the body is element-wise, so results are
+    // identical).  d[] is read 16 bytes at a time.
+    constexpr int V = sizeof(U) / sizeof(T), V16 = 16 / sizeof(T);
     const int64_t units = a.n / V;
-    Vec *av = reinterpret_cast<Vec *>(a.a);
-    auto body = [&](Vec &v, int64_t u) {
+    U *av = reinterpret_cast<U *>(a.a);
+    auto body = [&](U &v, int64_t u) {
       T *e = reinterpret_cast<T *>(&v);
       const int base = static_cast<int>((u * V) & (kLen - 1));
-      const Vec dv = da.vec(base);
-      const T *de = reinterpret_cast<const T *>(&dv);
 #pragma unroll
-      for (int k = 0; k < V; ++k)
-        e[k] = e[k] + de[k];
+      for (int h = 0; h < V / V16; ++h) {
+        const Vec dv = da.vec(base + h * V16);
+        const T *de = reinterpret_cast<const T *>(&dv);
+#pragma unroll
+        for (int k = 0; k < V16; ++k)
+          e[h * V16 + k] = e[h * V16 + k] + de[k];
+      }
     };
 #ifndef OMPDS_CONFIG2_BLOCK
 #define OMPDS_CONFIG2_BLOCK 1
@@ -245,18 +294,24 @@ template <class T> struct SharedArrayProg {
 #ifndef OMPDS_CONFIG2_ROUND
 #define OMPDS_CONFIG2_ROUND 4
 #endif
+#ifndef OMPDS_CONFIG2_WIDE_ROUND
+#define OMPDS_CONFIG2_WIDE_ROUND 2
+#endif
     // The cyclic schedule over blocks of B consecutive 16-byte units per
     // thread, R blocks (B x R units of a[]) in flight per round.
-    constexpr int B = OMPDS_CONFIG2_BLOCK, R = OMPDS_CONFIG2_ROUND;
+    constexpr int B = OMPDS_CONFIG2_BLOCK;
+    constexpr int R = sizeof(U) == 32 ? OMPDS_CONFIG2_WIDE_ROUND : OMPDS_CONFIG2_ROUND;
     const int64_t nblocks = units / B;
     int64_t bk = gid;
+#pragma unroll 1
     for (; bk + (R - 1) * pool < nblocks; bk += R * pool) {
-      Vec v[R][B];
+      U v[R][B];
 #pragma unroll
       for (int k = 0; k < R; ++k)
 #pragma unroll
         for (int j = 0; j < B; ++j)
           v[k][j] = ld_stream(av + (bk + k * pool) * B + j);
+      da.ready(); // one phase check once d[] is in (the loads above are in flight)
 #pragma unroll
       for (int k = 0; k < R; ++k)
 #pragma unroll
@@ -270,13 +325,14 @@ template <class T> struct SharedArrayProg {
     // block at a time would pay the full memory latency once per block at
     // the end of every thread's range (a few microseconds per launch)
     if (bk < nblocks) {
-      Vec v[R][B];
+      U v[R][B];
 #pragma unroll
       for (int k = 0; k < R; ++k)
         if (bk + k * pool < nblocks)
 #pragma unroll
           for (int j = 0; j < B; ++j)
             v[k][j] = ld_stream(av + (bk + k * pool) * B + j);
+      da.ready();
 #pragma unroll
       for (int k = 0; k < R; ++k)
         if (bk + k * pool < nblocks)
@@ -287,13 +343,23 @@ template <class T> struct SharedArrayProg {
             st_stream(av + u, v[k][j]);
           }
     }
+    da.ready();
     for (int64_t u = nblocks * B + gid; u < units; u += pool) { // units past the blocks
-      Vec v = av[u];
+      U v = ld_stream(av + u);
       body(v, u);
-      av[u] = v;
+      st_stream(av + u, v);
     }
     for (int64_t i = units * V + gid; i < a.n; i += pool)
       a.a[i] = a.a[i] + d[i & (kLen - 1)];
+  }
+};
+
+// a[] 32-byte aligned: the same region over 32-byte units.
+template <class T> struct SharedArrayProgWide : SharedArrayProg<T> {
+  using Args = typename SharedArrayProg<T>::Args;
+  __device__ static void region(int32_t, const SharedVars &sv, const Worker &w,
+                                const Args &a) {
+    SharedArrayProg<T>::template region_units<Vec32>(sv, w, a);
   }
 };
 
@@ -306,6 +372,8 @@ template <class T> struct SharedArrayProgUnaligned : SharedArrayProg<T> {
     const T *d = static_cast<const T *>(sv.get(0));
     if (!w.mine)
       return;
+    if (__isShared(d) && SharedArrayProg<T>::staged_by_tma(a, true))
+      mbar_wait(&stage_bar, 0);
     const int64_t gid = int64_t(w.local_team) * w.workers + w.wid;
     const int64_t pool = int64_t(w.local_teams) * w.workers;
     constexpr int U = 8;
@@ -339,6 +407,10 @@ __device__ __forceinline__ int32_t stream_op(int32_t c1, int32_t x, int32_t y,
                                    static_cast<uint32_t>(x) +
                                static_cast<uint32_t>(s)));
 }
+
+#ifndef OMPDS_STREAM_BLOCK
+#define OMPDS_STREAM_BLOCK 2
+#endif
 
 template <class T> struct StreamProg {
   struct Args {
@@ -380,8 +452,12 @@ template <class T> struct StreamProg {
     captures(sv, &c1, &s);
     if (!w.mine)
       return;
-    constexpr int V = 16 / sizeof(T);
     using Vec = typename std::conditional<sizeof(T) == 8, double2, int4>::type;
+    sweep<Vec, OMPDS_STREAM_BLOCK>(c1, s, w, a);
+  }
+  template <class Vec, int K>
+  __device__ static __forceinline__ void sweep(T c1, T s, const Worker &w, const Args &a) {
+    constexpr int V = sizeof(Vec) / sizeof(T);
     // the shard's own element range: local team indices (config 5 shards
     // elements across GPUs; each launch sees its slice)
     const int64_t gid = int64_t(w.local_team) * w.workers + w.wid;
@@ -389,16 +465,13 @@ template <class T> struct StreamProg {
     const int64_t units = a.n / V;
     const Vec *xv = reinterpret_cast<const Vec *>(a.x);
     Vec *yv = reinterpret_cast<Vec *>(a.y);
-#ifndef OMPDS_STREAM_BLOCK
-#define OMPDS_STREAM_BLOCK 2
-#endif
     // The parallel-for's cyclic schedule (AstLowering.cpp:429-462) over
-    // blocks of K consecutive 16-byte units per thread (the body is
-    // element-wise, so results equal the element-cyclic schedule's): a warp
-    // moves 32 x K x 16 contiguous bytes of x and of y per iteration.  K = 2
-    // with 7 teams of 96 workers per SM measured 6.88 TB/s against 6.70 for
-    // the unit-cyclic, 2-deep schedule (tools/stream_geom_ab.py).
-    constexpr int K = OMPDS_STREAM_BLOCK;
+    // blocks of K consecutive units per thread (the body is element-wise, so
+    // results equal the element-cyclic schedule's): a warp moves
+    // 32 x K x sizeof(Vec) contiguous bytes of x and of y per iteration.
+    // K = 2 16-byte units with 7 teams of 96 workers per SM measured
+    // 6.88 TB/s against 6.70 for the unit-cyclic, 2-deep schedule
+    // (tools/stream_geom_ab.py).
     const int64_t blocks = units / K;
     for (int64_t b = gid; b < blocks; b += pool) {
       Vec xs[K], ys[K];
@@ -1124,18 +1197,24 @@ int32_t ompds_run_shared_array(const ompds_launch *launch, int32_t elem,
   int32_t s = build_fixed_layout({256 * esz}, 4, &lay);
   if (s)
     return s;
-  // 16-byte vectors when a[] allows them, else the element-wise loop
-  const bool vec = (reinterpret_cast<uintptr_t>(a) & 15) == 0;
+  // 32-byte vectors when a[] allows them, else 16-byte ones, else the
+  // element-wise loop
+  const uintptr_t al = reinterpret_cast<uintptr_t>(a);
+  const int vec = (al & 31) == 0 ? OMPDS_WIDE_UNITS : (al & 15) == 0 ? 1 : 0;
   if (elem == 0) {
     SharedArrayProg<int32_t>::Args args{static_cast<int32_t *>(a), n,
                                         static_cast<const int32_t *>(d_init)};
-    return vec ? launch_generic<SharedArrayProg<int32_t>>(launch, lay, 1, args, stats, events)
+    return vec == 2 ? launch_generic<SharedArrayProgWide<int32_t>>(launch, lay, 1, args, stats,
+                                                                   events)
+         : vec ? launch_generic<SharedArrayProg<int32_t>>(launch, lay, 1, args, stats, events)
                : launch_generic<SharedArrayProgUnaligned<int32_t>>(launch, lay, 1, args, stats,
                                                                    events);
   }
   SharedArrayProg<double>::Args args{static_cast<double *>(a), n,
                                      static_cast<const double *>(d_init)};
-  return vec ? launch_generic<SharedArrayProg<double>>(launch, lay, 1, args, stats, events)
+  return vec == 2 ? launch_generic<SharedArrayProgWide<double>>(launch, lay, 1, args, stats,
+                                                                events)
+       : vec ? launch_generic<SharedArrayProg<double>>(launch, lay, 1, args, stats, events)
              : launch_generic<SharedArrayProgUnaligned<double>>(launch, lay, 1, args, stats,
                                                                 events);
 }
@@ -1148,7 +1227,9 @@ int32_t ompds_run_stream(const ompds_launch *launch, int32_t elem, int64_t n,
       (reinterpret_cast<uintptr_t>(x) & (esz - 1)) ||
       (reinterpret_cast<uintptr_t>(y) & (esz - 1)))
     return OMPDS_ERR_INVALID;
-  // 16-byte vectors when both arrays allow them, else the element-wise loop
+  // 16-byte vectors when both arrays allow them, else the element-wise loop.
+  // (32-byte units measured 0.8 % slower here at 2^28: 6816 vs 6874 GB/s,
+  // profiles/r2t_wide_units_ab.txt; config 2 uses them.)
   const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
   static FixedLayout lay8;
   static std::once_flag once;

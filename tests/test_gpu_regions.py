@@ -571,6 +571,53 @@ def test_config2_d_init_view_not_16_byte_aligned(dtype, off):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("dtype,off_bytes", [(torch.float64, 0), (torch.float64, 16),
+                                             (torch.float64, 48), (torch.int32, 16),
+                                             (torch.int32, 32)])
+def test_config2_32_and_16_byte_aligned_views(dtype, off_bytes):
+    """a[] 32-byte aligned runs the 32-byte-unit body, 16-byte aligned the
+    16-byte one; d[] arrives by TMA and is read after the transaction
+    barrier while the first loads of a[] are in flight: both equal the
+    oracle bit for bit."""
+    n = 123_457
+    esz = torch.tensor([], dtype=dtype).element_size()
+    off = off_bytes // esz
+    base = torch.empty(n + 16, dtype=dtype, device=DEV)
+    assert base.data_ptr() % 256 == 0
+    RG.fill_uniform(base, 0x5eed01ac)
+    before = base.cpu().numpy().copy()
+    d_init = torch.arange(256, dtype=dtype, device=DEV) * 3 + 1
+    out = RG.run_shared_array(base[off:off + n], 2 * 148, 480, d_init=d_init)
+    torch.cuda.synchronize()
+    d = d_init.cpu().numpy()
+    want = before.copy()
+    if dtype == torch.float64:
+        want[off:off + n] = before[off:off + n] + d[np.arange(n) & 255]
+    else:
+        want[off:off + n] = (before[off:off + n].astype(np.int64)
+                             + d[np.arange(n) & 255]).astype(np.int32)
+    assert np.array_equal(base.cpu().numpy().view(np.uint8), want.view(np.uint8))
+    assert all(s.trap == 0 and s.depot_in_smem for s in out.team_stats())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [0, 1, 5, 300, 4096])
+def test_config2_tma_staging_with_idle_workers(n):
+    """Fewer elements than workers: most workers never read d[] (never wait
+    on the staging barrier); the master waits for the copy before its team
+    retires, and the elements that exist equal the oracle."""
+    a = torch.empty(n, dtype=torch.float64, device=DEV)
+    RG.fill_uniform(a, 0x5eed01ac)
+    d_init = torch.arange(256, dtype=torch.float64, device=DEV) * 3 + 1
+    out = RG.run_shared_array(a, 2 * 148, 480, d_init=d_init)
+    want = np.empty(n)
+    O.lib().orc_fill(1, O.ptr(want), n, 0x5eed01ac, 0)
+    O.lib().orc_shared_array(1, n, O.ptr(want))
+    assert np.array_equal(a.cpu().numpy(), want)
+    assert all(s.trap == 0 and s.regions == 1 for s in out.team_stats())
+
+
+@pytest.mark.gpu
 def test_graph_survives_a_larger_eager_launch():
     """A graph captured after one eager launch keeps replaying correctly after
     a later, larger eager launch on the same stream grew the workspace: the

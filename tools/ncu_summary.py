@@ -103,6 +103,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rep")
     ap.add_argument("--launches")
+    ap.add_argument("--group", action="store_true",
+                    help="with --launches: one row per kernel (launches, total, mean, share)")
     ap.add_argument("--name", required=True)
     ap.add_argument("--algo-bytes", type=float, default=0)
     ap.add_argument("--traffic-n", type=int, default=0,
@@ -122,6 +124,20 @@ def main():
         json.dump(s, sys.stdout, indent=1)
     if a.launches:
         s = summarise_launches(a.launches)
+        if a.group:
+            g = {}
+            for r in s:
+                e = g.setdefault(r["kernel"], [0, 0.0])
+                e[0] += 1
+                e[1] += r["ns"]
+            total = sum(v[1] for v in g.values()) or 1.0
+            with open(os.path.join(ROOT, "profiles", a.name + ".csv"), "w") as f:
+                w = csv.writer(f)
+                w.writerow(["kernel", "launches", "total_ns", "mean_ns", "share"])
+                for k, (n, t) in sorted(g.items(), key=lambda kv: -kv[1][1]):
+                    w.writerow([k, n, round(t), round(t / n), round(t / total, 4)])
+                    print(f"{t / total:7.4f} {n:5d} {t / n:>12.0f} {k[:90]}")
+            return
         with open(os.path.join(ROOT, "profiles", a.name + ".csv"), "w") as f:
             w = csv.writer(f)
             w.writerow(["kernel", "grid", "block", "ns", "share"])

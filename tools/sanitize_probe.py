@@ -24,6 +24,14 @@ def main():
         RG.run_shared_array(s, 4, 64, d_init=torch.arange(256, dtype=torch.float64,
                                                           device=dev), depot_capacity=cap)
     RG.run_shared_array(torch.zeros(1000, dtype=torch.int32, device=dev), 2, 33)
+    # TMA-staged d[] read after the transaction barrier: 32-byte units, a
+    # 16-byte aligned view (16-byte units), idle workers (n < workers)
+    dd = torch.arange(256, dtype=torch.float64, device=dev)
+    s = torch.zeros(4099, dtype=torch.float64, device=dev)
+    RG.run_shared_array(s[2:4002], 3, 96, d_init=dd)
+    RG.run_shared_array(s[:7], 3, 96, d_init=dd)
+    RG.run_shared_array(torch.zeros(1000, dtype=torch.int32, device=dev), 2, 64,
+                        d_init=torch.arange(256, dtype=torch.int32, device=dev))
     x = torch.ones(5003, dtype=torch.float64, device=dev)
     y = torch.ones(5003, dtype=torch.float64, device=dev)
     RG.run_stream(x, y, [k / 8 for k in range(1, 9)], 4, 96, max_events=512)
