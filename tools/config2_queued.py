@@ -12,7 +12,7 @@ d = torch.arange(256, dtype=torch.float64, device="cuda") * 3 + 1
 flush = torch.ones(64 << 20, dtype=torch.int32, device="cuda")
 s = torch.cuda.Stream()
 K = 20
-geoms = [(2, 480), (3, 480), (4, 480), (4, 224), (6, 224), (8, 224)]
+geoms = [tuple(int(v) for v in g.split("x")) for g in os.environ.get("GEOMS", "2x480,3x480,4x480,4x224,6x224,8x224").split(",")]
 out = []
 for k, w in geoms:
     go = RG.prepared_shared_array(a, 148 * k, w, d_init=d, stream=s)
