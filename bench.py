@@ -738,10 +738,12 @@ def other_configs(RG, dev, stream, sms):
         "GBps_queued": round(16 * n2 / ms_queued / 1e6, 1),
         "timing": "ms: median of 10 launches, each after an L2 eviction and bracketed by "
                   f"CUDA events; ms_queued: {K} x [L2 evict; region] minus {K} x [L2 evict], "
-                  "queued back to back (ncu's kernel duration: 42.6-43.2 us)",
+                  "queued back to back (ncu's kernel duration: 41.4 us, profiles/r2u_config2_ncu.json)",
         "smem_bytes_per_cta": st.smem_bytes, "depot_in_smem": st.depot_in_smem,
-        "regs_per_thread": ptxas_regs("SharedArrayProgIdEELb1E"),
-        "staging": "cp.async.bulk (TMA) of d[256] into the depot slot",
+        "regs_per_thread": ptxas_regs("SharedArrayProgWideIdEELb1E"),
+        "staging": ("cp.async.bulk (TMA) of d[256] into the depot slot, completed asynchronously "
+                    "(workers wait on the transaction barrier after their first loads of a[])"),
+        "units": "32-byte vectors (a[] 32-byte aligned)",
         "roofline_frac": None,
         "same_size_copy_GBps_queued": round(16 * n2 / ms_copy / 1e6, 1),
         "frac_of_same_size_copy": round(ms_copy / ms_queued, 4),

@@ -147,7 +147,9 @@ B200_KERNELS = [
      56 + 160 + 49),
     ("RegionsProgIdEELb1ELb0E", "config1 lean W>32", 64, 56 + 160 + 49),
     ("RegionsProgIdEELb0ELb0E", "config1 general", 64, 56 + 160 + 49),
-    ("SharedArrayProgIdEELb1E", "config2 f64 lean", 512, 2072 + 160 + 49),
+    ("SharedArrayProgWideIdEELb1E", "config2 f64 lean (32-byte units; a[] 32-byte aligned)", 512,
+     2072 + 160 + 49),
+    ("SharedArrayProgIdEELb1E", "config2 f64 lean (16-byte units)", 512, 2072 + 160 + 49),
     ("NestedProgIdEELb1E", "config3 f64 (2 KB warp slots x 3) lean", 128,
      96 * 0 + 304 + 3 * 2048),
     ("StreamProgIdEELb1E", "config4 f64 lean", 128, 80 + 160 + 49),
