@@ -548,16 +548,16 @@ def regions_section(RG, torch, dist, dev, stream, sms, rank, world):
     clk_after = RG.probe_overheads(1024, stream=stream)["sm_clock_mhz"]
     # the same protocol on every SM: 64-thread teams (the small-team
     # instantiation, 32 registers, up to 32 teams/SM by the occupancy model),
-    # 22 per SM in one wave, 2000 regions each.  22 is the measured optimum
-    # (profiles/r2_cfg1_sweep_smallteam.json, tools/cfg1_sweep.py: 16/SM 5.86,
-    # 20/SM 6.36, 22/SM 6.43, 24/SM 6.39, 32/SM 5.95 G regions/s; even counts
-    # keep the 4 SM sub-partitions balanced, and past 24 teams the extra
-    # barrier-waiting warps cost more issue slots than they hide).
+    # 20 per SM in one wave, 2000 regions each.  20 is the measured optimum
+    # (profiles/r2v_cfg1_sweep_preload.json, tools/cfg1_sweep.py: 16/SM 6.40,
+    # 18/SM 6.56, 20/SM 6.61, 22/SM 6.52, 24/SM 6.42, 32/SM 6.07 G regions/s;
+    # even counts keep the 4 SM sub-partitions balanced, and past ~20 teams
+    # the extra barrier-waiting warps cost more issue slots than they hide).
     # With N ranks the team grid (N x T) is sharded by range: rank r launches
     # teams [r*T, (r+1)*T) of the N*T grid (first_team/total_teams), the
     # whole-job rate is N*T*R2 over the slowest rank's time.
     from paper_1711_10413_b200 import occupancy as OCC
-    per_sm1 = min(22, OCC.occupancy_for("b200", 265, ptxas_regs("RegionsProgIdEELb1ELb1E") or 52,
+    per_sm1 = min(20, OCC.occupancy_for("b200", 265, ptxas_regs("RegionsProgIdEELb1ELb1E") or 52,
                                         64).actual)
     R2, teams2 = 2000, sms * per_sm1
     a2 = torch.zeros(world * teams2 * 32, dtype=torch.float64, device=dev)

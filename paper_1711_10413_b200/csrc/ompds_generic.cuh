@@ -57,6 +57,15 @@ inline int32_t cuda_fail(cudaError_t e, const char *what) {
 // kSmallTeams = true;` -- bounded to 64 threads and 32 teams per SM, so
 // ptxas fits it in 32 registers (config 1: no spills, 32 instead of 24
 // teams per SM fit, +7 % regions/s).
+// A program may ask the worker loop to load list entries 0..3 into every
+// lane together with the team state (`static constexpr bool
+// kPreloadEntries = true;`): its region then dereferences the captures it
+// needs directly (broadcast loads), with no shuffle step on the chain.
+template <class P, class = void> struct PreloadEntries : std::false_type {};
+template <class P>
+struct PreloadEntries<P, std::void_t<decltype(P::kPreloadEntries)>>
+    : std::integral_constant<bool, P::kPreloadEntries> {};
+
 template <class P, class = void> struct SmallTeams : std::false_type {};
 template <class P>
 struct SmallTeams<P, std::void_t<decltype(P::kSmallTeams)>>
@@ -409,6 +418,11 @@ struct Worker {
   int32_t nargs;
   int32_t region_index; // regions this warp ran before the current one
   uint32_t worker_threads; // 32 x worker warps (padding lanes included)
+  // Entries 0..3 of the list, loaded by every lane together with the team
+  // state when the program asks for them (kPreloadEntries) and the list is
+  // the window (the lean instantiation); pre_ok says they are valid.
+  void *pre[4];
+  bool pre_ok = false;
 
   // `#pragma omp barrier` inside the region: every worker of the team (the
   // master warp is parked at the join and does not take part); all lanes of
@@ -530,6 +544,21 @@ __global__ void __launch_bounds__(kSmall ? kSmallTeamThreads : OMPDS_GENERIC_LB_
       arrivals += count;
       OMPDS_TL(rr, 5);
       const StagedState st = load_staged_state<!kLean>(t, wm.win_off);
+      if constexpr (kLean && PreloadEntries<Prog>::value) {
+        unsigned long long e0, e1, e2, e3;
+        asm volatile("ld.shared.u64 %0, [%4];\n\t" // the window is 8-byte aligned
+                     "ld.shared.u64 %1, [%4+8];\n\t"
+                     "ld.shared.u64 %2, [%4+16];\n\t"
+                     "ld.shared.u64 %3, [%4+24];"
+                     : "=l"(e0), "=l"(e1), "=l"(e2), "=l"(e3)
+                     : "r"(t.window_s)
+                     : "memory");
+        w.pre[0] = reinterpret_cast<void *>(e0);
+        w.pre[1] = reinterpret_cast<void *>(e1);
+        w.pre[2] = reinterpret_cast<void *>(e2);
+        w.pre[3] = reinterpret_cast<void *>(e3);
+        w.pre_ok = true;
+      }
       Fetch f;
       if (__builtin_expect(fetch_is_fast(st, wm), 1)) {
         fetch_account_fast(t, st, wm); // a staged region, no event log

@@ -26,6 +26,7 @@ namespace ompds {
 
 template <class T> struct RegionsProg {
   static constexpr bool kSmallTeams = true; // config 1: 64-thread teams
+  static constexpr bool kPreloadEntries = true;
   struct Args {
     T *a;
     int32_t regions;
@@ -63,6 +64,19 @@ template <class T> struct RegionsProg {
     // first so its latency overlaps get-shared-variables.
     T *dst = a.a + size_t(w.team) * w.workers + w.wid;
     const T old = w.mine ? *dst : T(0);
+    if (w.pre_ok) {
+      // entries 0..3 came with the team state: every lane dereferences the
+      // captures itself (the same address across the warp: broadcast loads)
+      const int32_t c1 = *static_cast<const volatile int32_t *>(w.pre[0]);
+      const int32_t c2 = *static_cast<const volatile int32_t *>(w.pre[1]);
+      const T c3 = *static_cast<const volatile T *>(w.pre[2]);
+      const T c4 = *static_cast<const volatile T *>(w.pre[3]);
+      if (w.mine) {
+        T sum = (T(c1 + c2) + c3) + c4;
+        *dst = old + sum;
+      }
+      return;
+    }
     // get-shared-variables: lane j < 4 dereferences capture j once (slots
     // are 8-byte sized and aligned, so one 8-byte load covers an int or a
     // T slot), shuffles spread the four values.
