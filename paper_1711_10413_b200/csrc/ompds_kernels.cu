@@ -566,6 +566,7 @@ template <class T> struct StreamProgUnaligned : StreamProg<T> {
 //===----------------------------------------------------------------------===//
 
 template <class T> struct NestedProg {
+  static constexpr bool kPreloadEntries = true; // 2 captures: c and s[]
   struct Args {
     T *a;
     int32_t regions;
@@ -633,8 +634,8 @@ template <class T> struct NestedProg {
   }
   __device__ static void region(int32_t, const SharedVars &sv, Worker &w,
                                 const Args &a) {
-    const int32_t *cp = static_cast<const int32_t *>(sv.get(0));
-    const T *sp = static_cast<const T *>(sv.get(1));
+    const int32_t *cp = static_cast<const int32_t *>(w.pre_ok ? w.pre[0] : sv.get(0));
+    const T *sp = static_cast<const T *>(w.pre_ok ? w.pre[1] : sv.get(1));
     const uint32_t lane = lane_id();
     // c is shared with the master, which is parked at the join while the
     // region runs: one load serves the whole region.
