@@ -93,6 +93,27 @@ def test_config1_f64_and_int_match_oracle(teams, workers, regions):
                 (0, 2 * regions, 2 * regions + 1, regions)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("teams,workers,regions", [(1, 32, 5), (3, 40, 7), (148 * 20, 32, 20)])
+@pytest.mark.parametrize("depot_capacity", [0, -1])
+def test_config1_preloaded_entries_with_the_depot_in_smem_or_global(teams, workers, regions,
+                                                                    depot_capacity):
+    """Config 1 takes list entries 0-3 with the team state and dereferences
+    the captures with broadcast loads (kPreloadEntries): with the master's
+    depot in its smem slot the entries point into shared memory, with a
+    zero-byte slot into the team's global chain -- the same values either way,
+    on the small-team kernel (W = 32) and the general-size one (W = 40)."""
+    for dt, elem in ((torch.float64, 1), (torch.int32, 0)):
+        a = torch.zeros(teams * workers, dtype=dt, device=DEV)
+        out = RG.run_regions(a, teams, workers, regions, depot_capacity=depot_capacity)
+        want = np.zeros(teams * workers, dtype=np.float64 if elem else np.int32)
+        O.lib().orc_regions(elem, teams, workers, regions, O.ptr(want))
+        assert np.array_equal(a.cpu().numpy(), want)
+        for st in out.team_stats():
+            assert st.trap == 0 and st.regions == regions
+            assert st.depot_in_smem == (depot_capacity != 0)
+
+
 # --------------------------------------------------------------------------- config 2
 
 def test_config2_int_analog_matches_reference():

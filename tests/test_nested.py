@@ -82,6 +82,24 @@ def test_gpu_nested_values_and_stack_placement(elem, slot):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("elem", [0, 1])
+def test_gpu_nested_master_depot_on_the_global_chain(elem):
+    """The nested program's two captures (c, s[]) read through list entries
+    preloaded with the team state: with a zero-byte master slot they point
+    into the team's global chain; the values equal the oracle."""
+    import torch
+    from paper_1711_10413_b200 import regions as RG
+    teams, workers, regions = 7, 96, 4
+    dt = torch.float64 if elem else torch.int32
+    a = torch.zeros(teams * workers, dtype=dt, device="cuda")
+    out, _ = RG.run_nested(a, teams, workers, regions, depot_capacity=0)
+    want = np.zeros(teams * workers, dtype=np.float64 if elem else np.int32)
+    O.lib().orc_nested(elem, teams, workers, regions, O.ptr(want))
+    assert np.array_equal(a.cpu().numpy(), want)
+    assert all(s.trap == 0 and not s.depot_in_smem for s in out.team_stats())
+
+
+@pytest.mark.gpu
 def test_gpu_nested_overflow_chain_exhausted():
     import torch
     from paper_1711_10413_b200 import regions as RG
