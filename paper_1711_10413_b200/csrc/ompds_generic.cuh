@@ -96,6 +96,25 @@ __device__ __forceinline__ long long tl_clock() {
   } while (0)
 #endif
 
+// Per-team %globaltimer stamps (tools/team_times.cu only): [0] kernel entry,
+// [1] master before its first region, [2] before the first release, [3]
+// after the first join, [4] at the end of the master, [5] after the
+// prologue's zeroing barrier, [6] after kernel_init, for every team.
+#ifdef OMPDS_TEAM_TIMES
+__device__ long long g_team_times[OMPDS_TEAM_TIMES][8];
+#define OMPDS_TT(k)                                                            \
+  do {                                                                         \
+    long long g_;                                                              \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_)::"memory");          \
+    if ((threadIdx.x & 31) == 0 && blockIdx.x < OMPDS_TEAM_TIMES)              \
+      g_team_times[blockIdx.x][(k)] = g_; /* a store only: no load latency */  \
+  } while (0)
+#else
+#define OMPDS_TT(k)                                                            \
+  do {                                                                         \
+  } while (0)
+#endif
+
 struct TeamParams {
   int32_t workers;       // W
   int32_t prealloc;      // PreallocEntries
@@ -190,7 +209,9 @@ struct Master {
     if (leader)
       s = kernel_init(t, kMaster, p->workers);
     __syncwarp(); // the master's init writes before any lane reads the state
-    return sync_status(s);
+    s = sync_status(s);
+    OMPDS_TT(6);
+    return s;
   }
 
   // The kernel frame group's depot is the first frame of the master's
@@ -259,10 +280,12 @@ struct Master {
                        "l"(reinterpret_cast<unsigned long long>(addr_of(j)))
                        : "memory");
       OMPDS_TL(regions, 2);
+      OMPDS_TT(2);
       bar_sync(kBarHandoff, team_threads); // release the workers
       OMPDS_TL(regions, 3);
       bar_sync(kBarHandoff, team_threads); // join
       OMPDS_TL(regions, 4);
+      OMPDS_TT(3);
       if (join_completes)
         complete_region(t, leader);
       barriers += 2;
@@ -491,6 +514,27 @@ __global__ void __launch_bounds__(kSmall ? kSmallTeamThreads : OMPDS_GENERIC_LB_
     generic_mode_kernel(const __grid_constant__ TeamParams p,
                         const __grid_constant__ typename Prog::Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
+  if (threadIdx.x == 0)
+    OMPDS_TT(0);
+#ifndef OMPDS_WARM_PARAMS
+#define OMPDS_WARM_PARAMS 1
+#endif
+#if OMPDS_WARM_PARAMS
+  {
+    // Touch every 8-byte word of the launch parameters at once, one per
+    // thread: the SM's constant cache misses on them in parallel here
+    // instead of one line at a time as the prologue, kernel_init and the
+    // master's first prepare reach them.
+    constexpr uint32_t kP = sizeof(TeamParams) / 8, kA = sizeof(typename Prog::Args) / 8;
+    const uint32_t i = threadIdx.x;
+    if (i < kP + kA) {
+      const unsigned long long v =
+          i < kP ? reinterpret_cast<const unsigned long long *>(&p)[i]
+                 : reinterpret_cast<const unsigned long long *>(&a)[i - kP];
+      asm volatile("" ::"l"(v));
+    }
+  }
+#endif
   const uint32_t team_threads = blockDim.x;
   const int warp = threadIdx.x >> 5;
   const int worker_warps = static_cast<int>(team_threads >> 5) - 1;
@@ -509,6 +553,8 @@ __global__ void __launch_bounds__(kSmall ? kSmallTeamThreads : OMPDS_GENERIC_LB_
   if (threadIdx.x == 0)
     t.set_work_fn(-1);
   __syncthreads();
+  if (threadIdx.x == team_threads - 32)
+    OMPDS_TT(5);
 
   if (warp < worker_warps) {
     Worker w;
@@ -609,8 +655,11 @@ __global__ void __launch_bounds__(kSmall ? kSmallTeamThreads : OMPDS_GENERIC_LB_
     m.join_completes = completes_at_join(t, p.workers);
     m.fast_nargs = t.events == nullptr ? t.prealloc : -1;
     m.team_threads = team_threads;
-    if (m.init() == OMPDS_OK && m.push_depot() == OMPDS_OK)
+    if (m.init() == OMPDS_OK && m.push_depot() == OMPDS_OK) {
+      OMPDS_TT(1);
       Prog::master(m, a);
+    }
+    OMPDS_TT(4);
     m.finish();
   }
 }
@@ -623,7 +672,9 @@ __global__ void __launch_bounds__(kSmall ? kSmallTeamThreads : OMPDS_GENERIC_LB_
 // stream): buffer 0 holds the teams' overflow slabs (args lists, master
 // depot overflow), buffer 1 the worker warps' data-sharing overflow chains,
 // buffer 2 a region program's tables, buffer 3 the masters' local depot
-// mirrors.  Launches on one stream run in order, so they can share a set;
+// mirrors, buffer 4 the work counters of dynamically scheduled loops (zeroed
+// when allocated; each launch leaves them zero again).  Launches on one
+// stream run in order, so they can share a set;
 // launches on different streams (or devices) get their own.
 // A buffer that a larger launch supersedes is retired, not freed: a CUDA
 // graph captured from an earlier launch on the stream keeps pointing at it,
@@ -631,8 +682,9 @@ __global__ void __launch_bounds__(kSmall ? kSmallTeamThreads : OMPDS_GENERIC_LB_
 // invalidates graphs captured from launches on that stream).  Buffers grow by
 // at least 1.5x, so a stream retires O(log size) of them.
 struct WsBuffers {
-  unsigned char *buf[4] = {nullptr, nullptr, nullptr, nullptr};
-  size_t bytes[4] = {0, 0, 0, 0};
+  static constexpr int kBuffers = 5;
+  unsigned char *buf[kBuffers] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t bytes[kBuffers] = {0, 0, 0, 0, 0};
   std::vector<unsigned char *> retired;
   // the region-program tables last copied into buf[2] (ompds_run_program
   // skips the copy when a launch stages the same bytes again, so launches
@@ -646,6 +698,7 @@ struct Workspace {
 };
 inline Workspace g_ws;
 
+constexpr int kWorkCounters = 4;
 inline int32_t ensure_buffer(int which, size_t bytes, unsigned char **out,
                              void *stream = nullptr) {
   std::lock_guard<std::mutex> lk(g_ws.mu);
@@ -656,6 +709,8 @@ inline int32_t ensure_buffer(int which, size_t bytes, unsigned char **out,
     const size_t grow = std::max(bytes, w.bytes[which] + w.bytes[which] / 2);
     unsigned char *fresh = nullptr;
     OMPDS_CUDA(cudaMalloc(&fresh, grow));
+    if (which == kWorkCounters) // launches rely on finding them zero
+      OMPDS_CUDA(cudaMemset(fresh, 0, grow));
     if (w.buf[which]) // earlier launches (or captured graphs) may still use it
       w.retired.push_back(w.buf[which]);
     w.buf[which] = fresh;
@@ -692,7 +747,7 @@ inline int32_t release_workspace(void *stream) {
   for (unsigned char *b : it->second.retired)
     OMPDS_CUDA(cudaFree(b));
   it->second.retired.clear();
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < WsBuffers::kBuffers; ++k) {
     unsigned char *b = it->second.buf[k];
     it->second.buf[k] = nullptr;
     it->second.bytes[k] = 0;
