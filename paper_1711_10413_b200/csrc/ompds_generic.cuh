@@ -206,8 +206,10 @@ struct Master {
 
   __device__ __forceinline__ int32_t init() {
     int32_t s = 0;
-    if (leader)
+    if (leader) {
+      t.set_work_fn(-1); // the zeroed region's state word: no work function
       s = kernel_init(t, kMaster, p->workers);
+    }
     __syncwarp(); // the master's init writes before any lane reads the state
     s = sync_status(s);
     OMPDS_TT(6);
@@ -556,10 +558,8 @@ __global__ void __launch_bounds__(kSmall ? kSmallTeamThreads : OMPDS_GENERIC_LB_
     if (threadIdx.x < r - r16 * 16u)
       smem[r16 * 16u + threadIdx.x] = 0;
   }
-  __syncthreads();
-  if (threadIdx.x == 0)
-    t.set_work_fn(-1);
-  __syncthreads();
+  __syncthreads(); // (work_fn = -1 is set by the master's init: the workers
+                   // read the state only after its first release)
   if (threadIdx.x == team_threads - 32)
     OMPDS_TT(5);
 
