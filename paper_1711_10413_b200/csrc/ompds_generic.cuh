@@ -549,15 +549,8 @@ __global__ void __launch_bounds__(kSmall ? kSmallTeamThreads : OMPDS_GENERIC_LB_
       kLean ? 0 : p.max_events, kLean ? 0 : p.list_malloc);
   // Prologue: zero the team region (Simulator.cpp:286), runtime span last.
   const int64_t region = team_region_bytes(p.depot_cap, p.prealloc);
-  {
-    // 16-byte stores, then the last few bytes (the region is < 227 KB: 32-bit
-    // indices, and the launcher allocated exactly `region` bytes or more)
-    const uint32_t r = static_cast<uint32_t>(region), r16 = r / 16u;
-    for (uint32_t i = threadIdx.x; i < r16; i += team_threads)
-      reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
-    if (threadIdx.x < r - r16 * 16u)
-      smem[r16 * 16u + threadIdx.x] = 0;
-  }
+  for (int64_t i = threadIdx.x; i < region; i += team_threads)
+    smem[i] = 0;
   __syncthreads(); // (work_fn = -1 is set by the master's init: the workers
                    // read the state only after its first release)
   if (threadIdx.x == team_threads - 32)
