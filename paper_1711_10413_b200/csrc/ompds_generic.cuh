@@ -857,9 +857,12 @@ int32_t launch_generic(const ompds_launch *l, const FixedLayout &lay,
   if (smem > 227 * 1024)
     return OMPDS_ERR_INVALID;
   // the lean instantiation whenever nothing needs the general paths
+  // (a program that preloads list entries 0..3 needs a window of >= 4
+  // entries for them; smaller windows take the general instantiation)
   const bool lean = allow_lean && !l->log_events && !l->fail_dynamic_alloc &&
                     l->barrier_arrivals == nullptr &&
-                    l->list_allocator == OMPDS_LIST_SLAB && n_caps <= l->prealloc_entries;
+                    l->list_allocator == OMPDS_LIST_SLAB && n_caps <= l->prealloc_entries &&
+                    (!PreloadEntries<Prog>::value || l->prealloc_entries >= 4);
   auto kern = lean ? generic_mode_kernel<Prog, true> : generic_mode_kernel<Prog, false>;
   if constexpr (SmallTeams<Prog>::value)
     if (lean && threads == kSmallTeamThreads)

@@ -100,6 +100,23 @@ def test_gpu_nested_master_depot_on_the_global_chain(elem):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("prealloc", [2, 3, 4])
+def test_gpu_nested_small_windows(prealloc):
+    """The nested program stages 2 captures; with a window of fewer than 4
+    entries it runs on the general instantiation (no entry preload past the
+    window), with 4 or more on the lean one; the values equal the oracle."""
+    import torch
+    from paper_1711_10413_b200 import regions as RG
+    teams, workers, regions = 3, 64, 3
+    a = torch.zeros(teams * workers, dtype=torch.float64, device="cuda")
+    out, _ = RG.run_nested(a, teams, workers, regions, prealloc_entries=prealloc)
+    want = np.zeros(teams * workers, dtype=np.float64)
+    O.lib().orc_nested(1, teams, workers, regions, O.ptr(want))
+    assert np.array_equal(a.cpu().numpy(), want)
+    assert all(s.trap == 0 and s.regions == regions for s in out.team_stats())
+
+
+@pytest.mark.gpu
 def test_gpu_nested_overflow_chain_exhausted():
     import torch
     from paper_1711_10413_b200 import regions as RG
