@@ -75,6 +75,16 @@ constexpr int kSmallTeamsPerSM = 32;
 
 constexpr int kMaxCaptures = 32;
 
+// Lean instantiation: the master completes every region at the join and is
+// the phase's only writer between kernel_init and kernel_deinit, so it keeps
+// the phase in a register (no shared-memory read on its prepare) and the
+// workers keep no Active / retired accounting (no fetch or retire stores on
+// their side of the chain).  0 restores the worker-side accounting.
+#ifndef OMPDS_LEAN_JOIN_COMPLETES
+#define OMPDS_LEAN_JOIN_COMPLETES 1
+#endif
+constexpr bool kLeanJoinCompletes = OMPDS_LEAN_JOIN_COMPLETES != 0;
+
 // Region timeline (tools/timeline.cu only): clock64 stamps of the master's
 // and worker warp 0's steps for the first OMPDS_TIMELINE regions of team 0.
 #ifdef OMPDS_TIMELINE
@@ -184,7 +194,9 @@ struct Master {
   bool lean;           // the launch's lean instantiation (a compile-time constant
                        // after inlining): no event log, every list fits the
                        // window -- the general prepare path is compiled out
-  bool join_completes; // completes_at_join(): several worker warps, no event log
+  bool join_completes; // the master completes the region at the join:
+                       // completes_at_join() (several worker warps, no event
+                       // log), or any lean launch (kLeanJoinCompletes)
   int32_t fast_nargs;  // the fast prepare applies to nargs <= this: the
                        // window size without an event log, -1 with one
   uint32_t team_threads;
@@ -265,9 +277,14 @@ struct Master {
     // The common case of prepare_parallel in one branch: every check passes,
     // the list fits the window and no event log is kept.  Everything else
     // (traps, a global list, events) takes parallel_general.
-    const uint32_t phase = load_phase(t); // Idle implies Active == 0
+    // Idle implies Active == 0.  Lean: the master wrote the phase last
+    // (kernel_init, or the previous region's completion at the join; a
+    // refused prepare leaves it) -- Idle, without reading it back.
+    const bool lean_join = lean && kLeanJoinCompletes;
+    const uint32_t phase = lean_join ? uint32_t(kIdle) : load_phase(t);
     if (__builtin_expect(phase == uint32_t(kIdle) && nargs >= 0 && nargs <= fast_nargs, 1)) {
-      __syncwarp(); // every lane has read the state before the master stages
+      if (!lean_join)
+        __syncwarp(); // every lane has read the state before the master stages
       OMPDS_TL(regions, 1);
       stage_region_if(t, fn, nargs, t.window, leader);
       const uint32_t sa = t.window_s;
@@ -288,7 +305,9 @@ struct Master {
       bar_sync(kBarHandoff, team_threads); // join
       OMPDS_TL(regions, 4);
       OMPDS_TT(3);
-      if (join_completes)
+      if (lean_join)
+        retire_window_if(t, leader); // no lane reads the state back
+      else if (join_completes)
         complete_region(t, leader);
       barriers += 2;
       regions += 1;
@@ -607,7 +626,8 @@ __global__ void __launch_bounds__(kSmall ? kSmallTeamThreads : OMPDS_GENERIC_LB_
       }
       Fetch f;
       if (__builtin_expect(fetch_is_fast(st, wm), 1)) {
-        fetch_account_fast(t, st, wm); // a staged region, no event log
+        if constexpr (!(kLean && kLeanJoinCompletes))
+          fetch_account_fast(t, st, wm); // a staged region, no event log
         f = fetch_from(st);
       } else if constexpr (kLean) {
         if (st.phase == kTerminated)
@@ -635,10 +655,13 @@ __global__ void __launch_bounds__(kSmall ? kSmallTeamThreads : OMPDS_GENERIC_LB_
       OMPDS_TL(rr, 7);
       Prog::region(f.fn, sv, w, a);
       OMPDS_TL(rr, 8);
-      if constexpr (kLean)
-        end_parallel_window(t, plan); // every list is the window, no log
-      else
+      if constexpr (kLean) {
+        if constexpr (!kLeanJoinCompletes)
+          end_parallel_window(t, plan); // every list is the window, no log
+        // else: the master completes the region at the join
+      } else {
         end_parallel_warp(t, plan);
+      }
       OMPDS_TL(rr, 9);
       bar_sync(kBarHandoff, team_threads); // barrier.parallel (join)
       arrivals += count;
@@ -652,7 +675,7 @@ __global__ void __launch_bounds__(kSmall ? kSmallTeamThreads : OMPDS_GENERIC_LB_
     m.p = &p;
     m.leader = lane_id() == 0;
     m.lean = kLean;
-    m.join_completes = completes_at_join(t, p.workers);
+    m.join_completes = (kLean && kLeanJoinCompletes) || completes_at_join(t, p.workers);
     m.fast_nargs = t.events == nullptr ? t.prealloc : -1;
     m.team_threads = team_threads;
     if (m.init() == OMPDS_OK && m.push_depot() == OMPDS_OK) {
