@@ -52,17 +52,35 @@ struct StepOut {
   ompds_event events[kStepMaxEvents];
 };
 
+__device__ __noinline__ void team_step(ompds_runtime_config cfg, int32_t op, int32_t role,
+                                       int64_t arg, int32_t fn, uint64_t ext_list,
+                                       int64_t ext_bytes, unsigned char *smem, StepOut *out);
+
 // One protocol call against the team region saved in `state`
 // (team_region_bytes(0, prealloc) bytes: window, then the runtime span).
 __global__ void team_step_kernel(ompds_runtime_config cfg, int32_t op, int32_t role,
                                  int64_t arg, int32_t fn, uint64_t ext_list,
                                  int64_t ext_bytes, unsigned char *state, StepOut *out) {
   extern __shared__ __align__(16) unsigned char smem[];
-  if (threadIdx.x != 0)
-    return;
+  // The saved region moves between global and shared memory as 16-byte
+  // vectors spread over the warp (one memory latency, not one per byte);
+  // `state` and the dynamic shared memory are sized round_up(region, 16).
   const int64_t region = team_region_bytes(0, cfg.prealloc_entries);
-  for (int64_t i = 0; i < region; ++i)
-    smem[i] = state[i];
+  const int64_t nvec = (region + 15) / 16;
+  for (int64_t i = threadIdx.x; i < nvec; i += blockDim.x)
+    reinterpret_cast<uint4 *>(smem)[i] = reinterpret_cast<const uint4 *>(state)[i];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    team_step(cfg, op, role, arg, fn, ext_list, ext_bytes, smem, out);
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < nvec; i += blockDim.x)
+    reinterpret_cast<uint4 *>(state)[i] = reinterpret_cast<const uint4 *>(smem)[i];
+}
+
+// The protocol call itself, on the region in shared memory (one thread).
+__device__ __noinline__ void team_step(ompds_runtime_config cfg, int32_t op, int32_t role,
+                                       int64_t arg, int32_t fn, uint64_t ext_list,
+                                       int64_t ext_bytes, unsigned char *smem, StepOut *out) {
   ompds_event ev[kStepMaxEvents];
   // A dynamic list is the caller's block: the team "slab" is exactly that
   // block, so alloc_args_list returns it and the last retirement's
@@ -149,8 +167,6 @@ __global__ void team_step_kernel(ompds_runtime_config cfg, int32_t op, int32_t r
   o.summary.n_events = static_cast<int32_t>(ev_total + logged);
   if (args_word == reinterpret_cast<uint64_t>(t.window))
     args_word = kWindowMark; // smem addresses do not outlive the launch
-  for (int64_t i = 0; i < region; ++i)
-    state[i] = smem[i];
   *out = o;
 }
 
@@ -183,7 +199,7 @@ int32_t team_launch(ompds_team *h, int32_t op, int32_t role, int64_t arg, int32_
   OMPDS_CUDA(cudaGetDevice(&prev));
   if (prev != h->device)
     OMPDS_CUDA(cudaSetDevice(h->device));
-  team_step_kernel<<<1, 32, h->region, h->stream>>>(h->cfg, op, role, arg, fn, ext_list,
+  team_step_kernel<<<1, 32, round_up(h->region, 16), h->stream>>>(h->cfg, op, role, arg, fn, ext_list,
                                                     ext_bytes, h->state, h->out_dev);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess)
@@ -237,7 +253,7 @@ int32_t ompds_team_create(const ompds_runtime_config *config, uint64_t prealloc_
   if (e == cudaSuccess)
     e = cudaMalloc(&h->state, round_up(h->region, 16));
   if (e == cudaSuccess) // the simulator zero-fills team memory (Simulator.cpp:286)
-    e = cudaMemset(h->state, 0, h->region);
+    e = cudaMemset(h->state, 0, round_up(h->region, 16));
   if (e == cudaSuccess)
     e = cudaHostAlloc(reinterpret_cast<void **>(&h->out), sizeof(StepOut), cudaHostAllocMapped);
   if (e == cudaSuccess)
