@@ -557,8 +557,10 @@ def regions_section(RG, torch, dist, dev, stream, sms, rank, world):
     # teams [r*T, (r+1)*T) of the N*T grid (first_team/total_teams), the
     # whole-job rate is N*T*R2 over the slowest rank's time.
     from paper_1711_10413_b200 import occupancy as OCC
-    per_sm1 = min(20, OCC.occupancy_for("b200", 265, ptxas_regs("RegionsProgIdEELb1ELb1E") or 52,
-                                        64).actual)
+    # every team the register file holds (32/SM for the 32-register small-team
+    # kernel: the measured optimum, profiles/r2s2_cfg1_ab.txt)
+    per_sm1 = OCC.occupancy_for("b200", 265, ptxas_regs("RegionsProgIdEELb1ELb1E") or 52,
+                                64).actual
     R2, teams2 = 2000, sms * per_sm1
     a2 = torch.zeros(world * teams2 * 32, dtype=torch.float64, device=dev)
     rng = dict(first_team=rank * teams2, total_teams=world * teams2)

@@ -571,6 +571,18 @@ __device__ __forceinline__ void stage_region_if(const TeamCtx &t, int32_t fn,
                : "memory");
 }
 
+// The lean instantiation's staging: only {state, work_fn} and nargs (its
+// lists are always the window, which the workers address directly, and
+// Active is never counted), predicated on `p`: one store.
+__device__ __forceinline__ void stage_state_if(const TeamCtx &t, int32_t fn, int32_t nargs,
+                                               bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t"
+               "@q st.shared.v2.u32 [%0+8], {%2, %3};\n\t}" ::"r"(t.rt_s),
+               "r"(static_cast<uint32_t>(p)), "r"(state_word(kStaged, fn)),
+               "r"(static_cast<uint32_t>(nargs))
+               : "memory");
+}
+
 // All 32 lanes of a worker warp call this after the release barrier.
 // `mine` = this lane is a requested worker (tid < W); `m` = WarpMask::of(mine).
 // Fetch from an already loaded team state (the loop issues the loads right

@@ -85,6 +85,18 @@ constexpr int kMaxCaptures = 32;
 #endif
 constexpr bool kLeanJoinCompletes = OMPDS_LEAN_JOIN_COMPLETES != 0;
 
+// kPreloadEntries: the list entries are loaded with ld.volatile so ptxas
+// issues them with the team-state load, ahead of the phase test (plain loads
+// are sunk past it, onto the chain).  0: plain loads.
+#ifndef OMPDS_EARLY_ENTRIES
+#define OMPDS_EARLY_ENTRIES 1
+#endif
+#if OMPDS_EARLY_ENTRIES
+#define OMPDS_ENTRY_LD "ld.volatile.shared"
+#else
+#define OMPDS_ENTRY_LD "ld.shared"
+#endif
+
 // Region timeline (tools/timeline.cu only): clock64 stamps of the master's
 // and worker warp 0's steps for the first OMPDS_TIMELINE regions of team 0.
 #ifdef OMPDS_TIMELINE
@@ -286,7 +298,10 @@ struct Master {
       if (!lean_join)
         __syncwarp(); // every lane has read the state before the master stages
       OMPDS_TL(regions, 1);
-      stage_region_if(t, fn, nargs, t.window, leader);
+      if (lean_join)
+        stage_state_if(t, fn, nargs, leader); // lean: the list is the window
+      else
+        stage_region_if(t, fn, nargs, t.window, leader);
       const uint32_t sa = t.window_s;
       const int lane = static_cast<int>(lane_id());
       if (lane < nargs) // one predicated STS per lane for lists up to 32 entries
@@ -305,9 +320,12 @@ struct Master {
       bar_sync(kBarHandoff, team_threads); // join
       OMPDS_TL(regions, 4);
       OMPDS_TT(3);
-      if (lean_join)
-        retire_window_if(t, leader); // no lane reads the state back
-      else if (join_completes)
+      // Lean: the region is complete at the join; the state word keeps the
+      // staged fields until the next prepare overwrites them (no thread
+      // reads it in between: workers read it only after a release, the
+      // master only in kernel_deinit, which finish() precedes with the Idle
+      // store).
+      if (!lean_join && join_completes)
         complete_region(t, leader);
       barriers += 2;
       regions += 1;
@@ -330,6 +348,8 @@ struct Master {
     if (s == OMPDS_OK)
       s = OMPDS_ERR_INVALID;
     sync_status(s);
+    if (kLeanJoinCompletes)
+      retire_window_if(t, leader); // the workers must not see the last region staged
     bar_sync(kBarHandoff, team_threads); // release the workers
     bar_sync(kBarHandoff, team_threads); // join
     barriers += 2;
@@ -410,6 +430,8 @@ struct Master {
 
   __device__ __forceinline__ void finish() {
     int32_t s = 0;
+    if (lean && kLeanJoinCompletes && regions > 0)
+      retire_window_if(t, leader); // the last region's completion (see parallel_with)
     if (leader)
       s = kernel_deinit(t, kMaster);
     sync_status(s);
@@ -604,68 +626,92 @@ __global__ void __launch_bounds__(kSmall ? kSmallTeamThreads : OMPDS_GENERIC_LB_
     int32_t arrivals = 0;
     const bool count = !kLean && p.bar_arrivals != nullptr;
     w.arrivals = count ? &arrivals : nullptr;
-    for (int32_t rr = 0;; ++rr) {
-      bar_sync(kBarHandoff, team_threads); // await.work
-      arrivals += count;
-      OMPDS_TL(rr, 5);
-      const StagedState st = load_staged_state<!kLean>(t, wm.win_off);
-      if constexpr (kLean && PreloadEntries<Prog>::value) {
-        unsigned long long e0, e1, e2, e3;
-        asm volatile("ld.shared.u64 %0, [%4];\n\t" // the window is 8-byte aligned
-                     "ld.shared.u64 %1, [%4+8];\n\t"
-                     "ld.shared.u64 %2, [%4+16];\n\t"
-                     "ld.shared.u64 %3, [%4+24];"
-                     : "=l"(e0), "=l"(e1), "=l"(e2), "=l"(e3)
-                     : "r"(t.window_s)
-                     : "memory");
-        w.pre[0] = reinterpret_cast<void *>(e0);
-        w.pre[1] = reinterpret_cast<void *>(e1);
-        w.pre[2] = reinterpret_cast<void *>(e2);
-        w.pre[3] = reinterpret_cast<void *>(e3);
-        w.pre_ok = true;
-      }
-      Fetch f;
-      if (__builtin_expect(fetch_is_fast(st, wm), 1)) {
-        if constexpr (!(kLean && kLeanJoinCompletes))
-          fetch_account_fast(t, st, wm); // a staged region, no event log
-        f = fetch_from(st);
-      } else if constexpr (kLean) {
-        if (st.phase == kTerminated)
-          break; // termination sentinel (wf == null)
-        if (w.mine) // the master's prepare trapped: nothing is staged
-          t.trap(OMPDS_TRAP_PARALLEL_NOT_STAGED);
-        bar_sync(kBarHandoff, team_threads);
-        continue;
-      } else {
-        f = fetch_general(t, st, wm, w.mine);
-        if (f.fn < 0) {
-          if (f.status == OMPDS_OK)
-            break; // termination sentinel (wf == null)
-          bar_sync(kBarHandoff, team_threads); // trapped fetch: skip the region
-          arrivals += count;
-          continue;
+    // The worker loop, instantiated twice for programs that preload list
+    // entries: with 16-byte loads of a 16-byte aligned window, or 8-byte
+    // ones (a loop-invariant choice, made once, not per region).
+    auto run = [&](auto w16_tag) {
+      [[maybe_unused]] constexpr bool kW16 = decltype(w16_tag)::value;
+      for (int32_t rr = 0;; ++rr) {
+        bar_sync(kBarHandoff, team_threads); // await.work
+        arrivals += count;
+        OMPDS_TL(rr, 5);
+        const StagedState st = load_staged_state<!kLean>(t, wm.win_off);
+        if constexpr (kLean && PreloadEntries<Prog>::value) {
+          // volatile: issued with the state load, ahead of the phase test
+          // (ptxas sinks plain loads past it, onto the chain); two 16-byte
+          // loads when the window is 16-byte aligned (the depot size decides)
+          unsigned long long e0, e1, e2, e3;
+          if constexpr (kW16)
+            asm volatile(OMPDS_ENTRY_LD ".v2.u64 {%0, %1}, [%4];\n\t"
+                         OMPDS_ENTRY_LD ".v2.u64 {%2, %3}, [%4+16];"
+                         : "=l"(e0), "=l"(e1), "=l"(e2), "=l"(e3)
+                         : "r"(t.window_s)
+                         : "memory");
+          else
+            asm volatile(OMPDS_ENTRY_LD ".u64 %0, [%4];\n\t" // 8-byte aligned
+                         OMPDS_ENTRY_LD ".u64 %1, [%4+8];\n\t"
+                         OMPDS_ENTRY_LD ".u64 %2, [%4+16];\n\t"
+                         OMPDS_ENTRY_LD ".u64 %3, [%4+24];"
+                         : "=l"(e0), "=l"(e1), "=l"(e2), "=l"(e3)
+                         : "r"(t.window_s)
+                         : "memory");
+          w.pre[0] = reinterpret_cast<void *>(e0);
+          w.pre[1] = reinterpret_cast<void *>(e1);
+          w.pre[2] = reinterpret_cast<void *>(e2);
+          w.pre[3] = reinterpret_cast<void *>(e3);
+          w.pre_ok = true;
         }
+        Fetch f;
+        if (__builtin_expect(fetch_is_fast(st, wm), 1)) {
+          if constexpr (!(kLean && kLeanJoinCompletes))
+            fetch_account_fast(t, st, wm); // a staged region, no event log
+          f = fetch_from(st);
+        } else if constexpr (kLean) {
+          if (st.phase == kTerminated)
+            break; // termination sentinel (wf == null)
+          if (w.mine) // the master's prepare trapped: nothing is staged
+            t.trap(OMPDS_TRAP_PARALLEL_NOT_STAGED);
+          bar_sync(kBarHandoff, team_threads);
+          continue;
+        } else {
+          f = fetch_general(t, st, wm, w.mine);
+          if (f.fn < 0) {
+            if (f.status == OMPDS_OK)
+              break; // termination sentinel (wf == null)
+            bar_sync(kBarHandoff, team_threads); // trapped fetch: skip the region
+            arrivals += count;
+            continue;
+          }
+        }
+        OMPDS_TL(rr, 6);
+        w.args = f.args;
+        w.nargs = f.nargs;
+        w.region_index = rr;
+        const uint32_t plan = retire_plan(t, wm, f);
+        SharedVars sv = get_shared_variables(t, f);
+        OMPDS_TL(rr, 7);
+        Prog::region(f.fn, sv, w, a);
+        OMPDS_TL(rr, 8);
+        if constexpr (kLean) {
+          if constexpr (!kLeanJoinCompletes)
+            end_parallel_window(t, plan); // every list is the window, no log
+          // else: the master completes the region at the join
+        } else {
+          end_parallel_warp(t, plan);
+        }
+        OMPDS_TL(rr, 9);
+        bar_sync(kBarHandoff, team_threads); // barrier.parallel (join)
+        arrivals += count;
+        OMPDS_TL(rr, 10);
       }
-      OMPDS_TL(rr, 6);
-      w.args = f.args;
-      w.nargs = f.nargs;
-      w.region_index = rr;
-      const uint32_t plan = retire_plan(t, wm, f);
-      SharedVars sv = get_shared_variables(t, f);
-      OMPDS_TL(rr, 7);
-      Prog::region(f.fn, sv, w, a);
-      OMPDS_TL(rr, 8);
-      if constexpr (kLean) {
-        if constexpr (!kLeanJoinCompletes)
-          end_parallel_window(t, plan); // every list is the window, no log
-        // else: the master completes the region at the join
-      } else {
-        end_parallel_warp(t, plan);
-      }
-      OMPDS_TL(rr, 9);
-      bar_sync(kBarHandoff, team_threads); // barrier.parallel (join)
-      arrivals += count;
-      OMPDS_TL(rr, 10);
+    };
+    if constexpr (kLean && PreloadEntries<Prog>::value) {
+      if ((t.window_s & 15u) == 0)
+        run(std::true_type{});
+      else
+        run(std::false_type{});
+    } else {
+      run(std::false_type{});
     }
     if (count && w.mine) // worker threads of the reference's team (tid < W)
       p.bar_arrivals[size_t(blockIdx.x) * (p.workers + kWarp) + w.wid] = arrivals;
