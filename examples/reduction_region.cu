@@ -112,7 +112,42 @@ struct ReductionProg {
   }
 };
 
+// A program that stages more captures than its launch declared (n_caps):
+// region 0 shares one variable, region 1 asks for `nargs2` entries.  With
+// n_caps within the window the launcher picks the lean instantiation, whose
+// prepare refuses a list past the window (it has no list allocator): the
+// team traps, the workers
+// see no staged region and do not run region 0's body again
+// (tests/test_example_region.py: the lean instantiation's refused prepare).
+struct MisdeclaredProg {
+  struct Args {
+    unsigned long long *runs; // per team: region-0 bodies run (one per worker)
+    int32_t nargs2;
+  };
+  __device__ static void master(Master &m, const Args &a) {
+    if (m.parallel(0, 1) != OMPDS_OK)
+      return;
+    m.parallel(0, a.nargs2); // refused when it does not fit what the launch declared
+  }
+  __device__ static void region(int32_t, const SharedVars &, Worker &w, const Args &a) {
+    if (w.mine)
+      atomicAdd(a.runs + blockIdx.x, 1ull);
+  }
+};
+
 } // namespace
+
+extern "C" int32_t example_misdeclared(const ompds_launch *launch, int32_t nargs2,
+                                       unsigned long long *runs, ompds_team_stats *stats) {
+  if (!runs)
+    return OMPDS_ERR_INVALID;
+  FixedLayout lay;
+  const int32_t s = build_fixed_layout({8, 8}, 0, &lay);
+  if (s)
+    return s;
+  // declares one capture: the lean instantiation when it fits the window
+  return launch_generic<MisdeclaredProg>(launch, lay, 1, {runs, nargs2}, stats, nullptr);
+}
 
 extern "C" int32_t example_reduction(const ompds_launch *launch, const int32_t *x,
                                      int64_t n, long long *out,

@@ -21,6 +21,8 @@ def lib():
     lb.example_reduction.argtypes = [C.POINTER(L.Launch), C.c_void_p, C.c_int64, C.c_void_p,
                                      C.c_void_p]
     lb.example_reduction.restype = C.c_int32
+    lb.example_misdeclared.argtypes = [C.POINTER(L.Launch), C.c_int32, C.c_void_p, C.c_void_p]
+    lb.example_misdeclared.restype = C.c_int32
     return lb
 
 
@@ -99,3 +101,34 @@ def test_example_nested_program_matches_the_config3_oracle(teams, workers, slot,
     O.lib().orc_nested(1, teams, workers, regions, O.ptr(want))
     assert all(s.trap == 0 for s in res.team_stats())
     assert np.array_equal(a.cpu().numpy(), want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workers", [32, 96])
+def test_lean_refused_prepare_does_not_rerun_the_previous_region(workers):
+    """The lean instantiation defers a region's return to Idle to the next
+    staging store; a prepare it refuses (more entries than the launch
+    declared) must still leave the workers nothing staged: region 0's body
+    runs once per worker, the team traps, 2 handoffs per region reached."""
+    import torch
+    from paper_1711_10413_b200 import regions as RG
+    teams = 3
+    runs = torch.zeros(teams, dtype=torch.int64, device="cuda")
+    res = RG.Outputs(teams, runs.device, 0)
+    launch = RG.make_launch(teams, workers)
+    # 25 entries: past the 20-entry window the lean launch was sized for
+    L.check(lib().example_misdeclared(C.byref(launch), 25, C.c_void_p(runs.data_ptr()),
+                                      res.stats_ptr()), "example_misdeclared")
+    torch.cuda.synchronize()
+    assert runs.cpu().tolist() == [workers] * teams
+    for st in res.team_stats():
+        assert st.trap != 0
+        assert st.regions == 1
+        assert st.master_barriers == 4
+    # a second region that fits the window: both regions run
+    runs.zero_()
+    L.check(lib().example_misdeclared(C.byref(launch), 1, C.c_void_p(runs.data_ptr()),
+                                      res.stats_ptr()), "example_misdeclared")
+    torch.cuda.synchronize()
+    assert runs.cpu().tolist() == [2 * workers] * teams
+    assert all(st.trap == 0 and st.regions == 2 for st in res.team_stats())
