@@ -578,14 +578,22 @@ def regions_section(RG, torch, dist, dev, stream, sms, rank, world):
     # the malloc back-up scheme, "as large as an order of magnitude"): the
     # 4-capture region with the 20-entry window, with a 2-entry window so the
     # list spills to the team's global slab, and spilled to device malloc
+    # (window_general: the window list in the general instantiation -- forced
+    # by counting per-thread barrier arrivals -- so the placement comparison
+    # with the global lists, which only the general instantiation runs, is
+    # like for like)
     placement = {}
-    for name, pe, alloc in (("window", 20, 0), ("global_slab", 2, 0), ("device_malloc", 2, 1)):
+    for name, pe, alloc, gen in (("window", 20, 0, False), ("window_general", 20, 0, True),
+                                 ("global_slab", 2, 0, False), ("device_malloc", 2, 1, False)):
         row = {}
         for label, tm, rr in (("1team", 1, 2000), ("full", teams2, 200)):
             ap = torch.zeros(tm * 32, dtype=torch.float64, device=dev)
-            RG.run_regions(ap, tm, 32, 10, prealloc_entries=pe, list_allocator=alloc, stream=stream)
+            xkw = {"barrier_arrivals": torch.zeros(tm * 64, dtype=torch.int32, device=dev)} \
+                if gen else {}
+            RG.run_regions(ap, tm, 32, 10, prealloc_entries=pe, list_allocator=alloc,
+                           stream=stream, **xkw)
             ms_p = device_ms(stream, lambda: RG.run_regions(
-                ap, tm, 32, rr, prealloc_entries=pe, list_allocator=alloc, stream=stream))
+                ap, tm, 32, rr, prealloc_entries=pe, list_allocator=alloc, stream=stream, **xkw))
             row[f"ns_per_region_{label}"] = round(ms_p * 1e6 / rr, 1)
             row[f"regions_per_s_{label}"] = round(tm * rr / (ms_p * 1e-3), 0)
         placement[name] = row

@@ -583,6 +583,18 @@ __device__ __forceinline__ void stage_state_if(const TeamCtx &t, int32_t fn, int
                : "memory");
 }
 
+// Without an event log nothing observes a region's Active / retired counts
+// between its fetch and its join (the log is what records the workers'
+// fetch and retire order), so the master completes every such region at the
+// join -- freeing a heap list, returning the team to Idle -- and the
+// workers keep no count: their fetch is the state load and a branch, their
+// retirement nothing.  With an event log the workers retire as the
+// reference does.  0 keeps the worker-side accounting everywhere.
+#ifndef OMPDS_LEAN_JOIN_COMPLETES
+#define OMPDS_LEAN_JOIN_COMPLETES 1
+#endif
+constexpr bool kLeanJoinCompletes = OMPDS_LEAN_JOIN_COMPLETES != 0;
+
 // All 32 lanes of a worker warp call this after the release barrier.
 // `mine` = this lane is a requested worker (tid < W); `m` = WarpMask::of(mine).
 // Fetch from an already loaded team state (the loop issues the loads right
@@ -638,7 +650,8 @@ __device__ OMPDS_GENERAL_INLINE Fetch fetch_general(const TeamCtx &t, const Stag
   if (m.n == 0)
     return f;
   if (!t.events) { // staged, no log, reached through a general mask
-    fetch_account_fast(t, st, m);
+    if (!kLeanJoinCompletes)
+      fetch_account_fast(t, st, m);
     return f;
   }
   // staged, event log on
@@ -776,17 +789,15 @@ __device__ __forceinline__ void end_parallel_window(const TeamCtx &t, uint32_t p
     red_add_if(t.rt_s + Rt::kActive, (n << Rt::kRetiredShift) - n, leader);
   }
 }
-// Master warp, after the join barrier of a region it staged with the window
-// list and no event log, when the workers retired with fire-and-forget
-// atomics (several worker warps): the region was staged successfully, so
-// every one of the W workers fetched it and retired before arriving at the
-// join, and the join barrier orders all of those retirements before this
-// point -- retired == W and Active == 0 hold.  The master completes the
-// region's last retirement (the team returns to Idle) without re-reading
-// the word.  Sole-warp regions, global lists and logged regions were
-// completed by their last retiring worker.
+// Master warp, after the join barrier of a region staged with no event log
+// (completes_at_join): every one of the W workers fetched it and arrived at
+// the join after its body, and the join barrier orders all of their reads of
+// the staged region before this point.  The master completes the region --
+// the team returns to Idle (complete_region; a heap list is freed first,
+// retire_last) -- without re-reading any count.  Logged regions are
+// completed by their last retiring worker, in the reference's event order.
 __device__ __forceinline__ bool completes_at_join(const TeamCtx &t, int32_t workers) {
-  return workers > kWarp && t.events == nullptr;
+  return (kLeanJoinCompletes || workers > kWarp) && t.events == nullptr;
 }
 __device__ __forceinline__ void complete_region(const TeamCtx &t, bool leader) {
   retire_window_if(t, leader);

@@ -75,15 +75,9 @@ constexpr int kSmallTeamsPerSM = 32;
 
 constexpr int kMaxCaptures = 32;
 
-// Lean instantiation: the master completes every region at the join and is
-// the phase's only writer between kernel_init and kernel_deinit, so it keeps
-// the phase in a register (no shared-memory read on its prepare) and the
-// workers keep no Active / retired accounting (no fetch or retire stores on
-// their side of the chain).  0 restores the worker-side accounting.
-#ifndef OMPDS_LEAN_JOIN_COMPLETES
-#define OMPDS_LEAN_JOIN_COMPLETES 1
-#endif
-constexpr bool kLeanJoinCompletes = OMPDS_LEAN_JOIN_COMPLETES != 0;
+// (kLeanJoinCompletes, ompds_device.cuh: without an event log the master
+// completes every region at the join; the lean instantiation also keeps the
+// phase in a register and defers the completion store.)
 
 // kPreloadEntries: the list entries are loaded with ld.volatile so ptxas
 // issues them with the team-state load, ahead of the phase test (plain loads
@@ -417,8 +411,15 @@ struct Master {
     bar_sync(kBarHandoff, team_threads); // join
     OMPDS_TL(regions, 4);
     barriers += 2;
-    if (ok && list == t.window && join_completes)
-      complete_region(t, leader);
+    if (ok && join_completes) {
+      if (list == t.window) {
+        complete_region(t, leader);
+      } else { // the last retirement's work: free the heap list, Idle
+        if (leader)
+          retire_last(t);
+        __syncwarp();
+      }
+    }
     if (__builtin_expect(!ok, 0)) {
       if (!trap)
         trap = static_cast<int32_t>(packed & 0xffffffffu);
@@ -663,7 +664,7 @@ __global__ void __launch_bounds__(kSmall ? kSmallTeamThreads : OMPDS_GENERIC_LB_
         }
         Fetch f;
         if (__builtin_expect(fetch_is_fast(st, wm), 1)) {
-          if constexpr (!(kLean && kLeanJoinCompletes))
+          if constexpr (!kLeanJoinCompletes)
             fetch_account_fast(t, st, wm); // a staged region, no event log
           f = fetch_from(st);
         } else if constexpr (kLean) {
@@ -696,8 +697,8 @@ __global__ void __launch_bounds__(kSmall ? kSmallTeamThreads : OMPDS_GENERIC_LB_
           if constexpr (!kLeanJoinCompletes)
             end_parallel_window(t, plan); // every list is the window, no log
           // else: the master completes the region at the join
-        } else {
-          end_parallel_warp(t, plan);
+        } else if (!kLeanJoinCompletes || !(plan & 8u)) {
+          end_parallel_warp(t, plan); // with an event log: the workers retire
         }
         OMPDS_TL(rr, 9);
         bar_sync(kBarHandoff, team_threads); // barrier.parallel (join)
