@@ -283,9 +283,10 @@ struct Master {
     // The common case of prepare_parallel in one branch: every check passes,
     // the list fits the window and no event log is kept.  Everything else
     // (traps, a global list, events) takes parallel_general.
-    // Idle implies Active == 0.  Lean: the master wrote the phase last
-    // (kernel_init, or the previous region's completion at the join; a
-    // refused prepare leaves it) -- Idle, without reading it back.
+    // Idle implies Active == 0.  Lean: the team is Idle at every prepare
+    // (the master is the phase's only writer and a region is complete at
+    // its join; the word itself still shows the last region staged, see
+    // below), so the phase is not read back.
     const bool lean_join = lean && kLeanJoinCompletes;
     const uint32_t phase = lean_join ? uint32_t(kIdle) : load_phase(t);
     if (__builtin_expect(phase == uint32_t(kIdle) && nargs >= 0 && nargs <= fast_nargs, 1)) {
@@ -326,6 +327,8 @@ struct Master {
       return OMPDS_OK;
     }
     if (lean) {
+      if (lean_join) // Idle (see above): the word may still show the last region
+        return parallel_refused(prepare_check(kIdle, 0, nargs));
       const PrepareState st = load_prepare_state(t);
       return parallel_refused(prepare_check(st.phase, st.active, nargs));
     }

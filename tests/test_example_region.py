@@ -122,9 +122,18 @@ def test_lean_refused_prepare_does_not_rerun_the_previous_region(workers):
     torch.cuda.synchronize()
     assert runs.cpu().tolist() == [workers] * teams
     for st in res.team_stats():
-        assert st.trap != 0
+        assert st.trap == L.ERR_INVALID  # no list allocator in the lean launch
         assert st.regions == 1
         assert st.master_barriers == 4
+    # a negative count: the reference's own trap, even though the state word
+    # still shows region 0 staged (the lean completion is deferred)
+    runs.zero_()
+    L.check(lib().example_misdeclared(C.byref(launch), -1, C.c_void_p(runs.data_ptr()),
+                                      res.stats_ptr()), "example_misdeclared")
+    torch.cuda.synchronize()
+    assert runs.cpu().tolist() == [workers] * teams
+    assert all(st.trap == 8 and st.regions == 1  # OMPDS_TRAP_NEGATIVE_NARGS
+               for st in res.team_stats())
     # a second region that fits the window: both regions run
     runs.zero_()
     L.check(lib().example_misdeclared(C.byref(launch), 1, C.c_void_p(runs.data_ptr()),
