@@ -13,6 +13,10 @@
 #include "ompds.h"
 
 __global__ void empty_kernel() {}
+__global__ void flag_kernel(volatile unsigned *flag, unsigned v) {
+  __threadfence_system();
+  *flag = v;
+}
 
 int main() {
   cudaFree(nullptr);
@@ -30,6 +34,27 @@ int main() {
   }
   auto t1 = std::chrono::steady_clock::now();
   const double floor_us = std::chrono::duration<double, std::micro>(t1 - t0).count() / N;
+  // the same launch, completion observed by spinning on a mapped host word
+  unsigned *hflag = nullptr, *dflag = nullptr;
+  cudaHostAlloc(reinterpret_cast<void **>(&hflag), 64, cudaHostAllocMapped);
+  cudaHostGetDevicePointer(reinterpret_cast<void **>(&dflag), hflag, 0);
+  *hflag = 0;
+  t0 = std::chrono::steady_clock::now();
+  for (int i = 1; i <= N; ++i) {
+    flag_kernel<<<1, 1, 0, s>>>(dflag, unsigned(i));
+    while (*reinterpret_cast<volatile unsigned *>(hflag) != unsigned(i)) {
+    }
+  }
+  t1 = std::chrono::steady_clock::now();
+  const double spin_us = std::chrono::duration<double, std::micro>(t1 - t0).count() / N;
+  cudaStreamSynchronize(s);
+  // launch cost alone (the host side of one launch, no wait)
+  t0 = std::chrono::steady_clock::now();
+  for (int i = 0; i < N; ++i)
+    empty_kernel<<<1, 32, 0, s>>>();
+  t1 = std::chrono::steady_clock::now();
+  const double launch_us = std::chrono::duration<double, std::micro>(t1 - t0).count() / N;
+  cudaStreamSynchronize(s);
 
   ompds_runtime_config cfg{20, 0};
   ompds_team *h = nullptr;
@@ -57,8 +82,9 @@ int main() {
   }
   t1 = std::chrono::steady_clock::now();
   const double call_us = std::chrono::duration<double, std::micro>(t1 - t0).count() / (3.0 * N);
-  printf("{\"team_handle_us_per_call_c\": %.2f, \"empty_launch_sync_us\": %.2f, \"calls\": %d}\n",
-         call_us, floor_us, 3 * N);
+  printf("{\"team_handle_us_per_call_c\": %.2f, \"empty_launch_sync_us\": %.2f, "
+         "\"launch_spin_on_mapped_flag_us\": %.2f, \"launch_only_us\": %.2f, \"calls\": %d}\n",
+         call_us, floor_us, spin_us, launch_us, 3 * N);
   ompds_team_destroy(h);
   return 0;
 }
