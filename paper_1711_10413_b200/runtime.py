@@ -160,6 +160,8 @@ class TeamRuntime:
         self._fn_ids = {}
         self._events: List[RuntimeEvent] = []
         self._summary = L.RtSummary()
+        self._evbuf = (L.Event * 8)()  # reused by every call's log fetch
+        self._evtotal = C.c_int32()
         heap_ref = self.heap
         # keep the ctypes trampolines alive as long as the handle
         self._alloc = L.AllocFn(lambda nbytes, _u: int(heap_ref.allocate(int(nbytes))))
@@ -185,8 +187,10 @@ class TeamRuntime:
             return RtResult(False, trap_reason(status), status)
         lib = L.lib()
         lib.ompds_team_summary(self._h, C.byref(self._summary))
-        buf = (L.Event * 8)()
-        total = C.c_int32()
+        if self._summary.n_events <= len(self._events):
+            return RtResult()  # nothing new in the log
+        buf = self._evbuf
+        total = self._evtotal
         while True:
             first = len(self._events)
             st = lib.ompds_team_events(self._h, first, buf, 8, C.byref(total))
