@@ -658,7 +658,11 @@ def other_configs(RG, dev, stream, sms):
     # L2 "flush" by READING 256 MB: evicts a[] without leaving dirty lines
     # whose write-back would be charged to the timed kernel
     flush = torch.ones(64 << 20, dtype=torch.int32, device=dev)
-    t2, w2 = sms * 2, 480  # tools/sweep.py config2: one wave of 512-thread teams
+    # teams per SM x W: 4 x 224 measured best on this build (tools/
+    # config2_queued.py, profiles/r2s2_config2_geometry.txt); override with
+    # OMPDS_BENCH_C2=KxW for A/B runs
+    k2, w2 = (int(v) for v in os.environ.get("OMPDS_BENCH_C2", "4x224").split("x"))
+    t2 = sms * k2
     time.sleep(1.0)  # HBM-bound: start below the power cap the config-4 run left
     times = []
     st = RG.run_shared_array(a, t2, w2, d_init=d_init, stream=stream).team_stats()[0]

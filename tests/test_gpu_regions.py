@@ -498,14 +498,15 @@ def test_config2_view_not_16_byte_aligned(dtype, off):
 
 
 @pytest.mark.gpu
-def test_config2_bench_grid_full_size_matches_oracle():
-    """Config 2 as the bench runs it: 296 teams x 480 workers, 2^24 doubles,
-    d[] staged by TMA."""
+@pytest.mark.parametrize("teams,workers", [(592, 224), (296, 480)])
+def test_config2_bench_grid_full_size_matches_oracle(teams, workers):
+    """Config 2 as the bench runs it (592 teams x 224 workers; the earlier
+    296 x 480 grid too), 2^24 doubles, d[] staged by TMA."""
     n = 1 << 24
     a = torch.empty(n, dtype=torch.float64, device=DEV)
     RG.fill_uniform(a, 0x5eed01ac)
     d_init = torch.arange(256, dtype=torch.float64, device=DEV) * 3 + 1
-    out = RG.run_shared_array(a, 296, 480, d_init=d_init)
+    out = RG.run_shared_array(a, teams, workers, d_init=d_init)
     want = np.empty(n)
     O.lib().orc_fill(1, O.ptr(want), n, 0x5eed01ac, 0)
     O.lib().orc_shared_array(1, n, O.ptr(want))
