@@ -201,8 +201,9 @@ struct Master {
                        // after inlining): no event log, every list fits the
                        // window -- the general prepare path is compiled out
   bool join_completes; // the master completes the region at the join:
-                       // completes_at_join() (several worker warps, no event
-                       // log), or any lean launch (kLeanJoinCompletes)
+                       // completes_at_join() -- every launch without an event
+                       // log (kLeanJoinCompletes; else only several worker
+                       // warps without one), so every lean launch
   int32_t fast_nargs;  // the fast prepare applies to nargs <= this: the
                        // window size without an event log, -1 with one
   uint32_t team_threads;
