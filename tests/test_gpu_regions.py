@@ -80,7 +80,8 @@ def test_config1_int_analog_matches_reference(stem, regions):
 
 @pytest.mark.parametrize("teams,workers,regions", [(1, 32, 1), (3, 40, 7), (148, 96, 3),
                                                    (2, 992, 2), (5, 1, 4), (4, 40, 0),
-                                                   (148 * 18, 32, 50)])  # bench's whole-GPU grid
+                                                   (148 * 18, 32, 50),
+                                                   (148 * 32, 32, 2000)])  # bench's whole-GPU grid
 def test_config1_f64_and_int_match_oracle(teams, workers, regions):
     for dt, elem in ((torch.float64, 1), (torch.int32, 0)):
         a = torch.zeros(teams * workers, dtype=dt, device=DEV)
