@@ -754,7 +754,7 @@ def other_configs(RG, dev, stream, sms):
         "GBps_queued": round(16 * n2 / ms_queued / 1e6, 1),
         "timing": "ms: median of 10 launches, each after an L2 eviction and bracketed by "
                   f"CUDA events; ms_queued: {K} x [L2 evict; region] minus {K} x [L2 evict], "
-                  "queued back to back (ncu's kernel duration: 41.7 us, profiles/r2s2e_config2_ncu.json)",
+                  "queued back to back (ncu's kernel duration: 41.7 us, profiles/r2s2g_config2_ncu.json)",
         "smem_bytes_per_cta": st.smem_bytes, "depot_in_smem": st.depot_in_smem,
         "regs_per_thread": ptxas_regs("SharedArrayProgWideIdEELb1E"),
         "staging": ("cp.async.bulk (TMA) of d[256] into the depot slot, completed asynchronously "
